@@ -1,0 +1,186 @@
+/*
+ * fibra_cuda.h -- C-ABI of the B200-native batched fiber-network RVE solver.
+ *
+ * This is the drop-in boundary under the reference's batched-RVE interface
+ *   fibra::batch_response(const RveLibrary&, const BatchAssignment&, PackedStates&,
+ *                         const FiberLaw&, std::span<const Def3>, const RelaxConfig&,
+ *                         const StiffnessConfig&, WorkerPool&)
+ *   (/root/reference/proj/include/fibra/batch.hpp:71-77, body src/batch.cpp:155-187).
+ * Plain C: POD structs, int status codes, no exceptions and no torch types cross it.
+ * One context per host thread; calls on a context are serialized.
+ * The C++ shim that re-creates fibra::batch_response on top of this header is
+ * include/fibra_b200/batch_response.hpp; the ctypes binding is paper_2306_09427_b200/_capi.py.
+ */
+#ifndef FIBRA_CUDA_H
+#define FIBRA_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (per point and per call) ----------------------------------------
+ * Reference exception taxonomy (error.hpp:8-28) mapped to codes:                      */
+#define FIBRA_OK 0
+#define FIBRA_E_CONFIG 1          /* ConfigError (propagates out of batch_response)    */
+#define FIBRA_E_KINEMATICS 2      /* KinematicsError: det(F) <= 0 (network.cpp:255)    */
+#define FIBRA_E_COLLAPSE 3        /* SolverError: fiber collapse (network.cpp:291-293) */
+#define FIBRA_E_BAD_DT 4          /* SolverError: bad time step (relax.cpp:151-153)    */
+#define FIBRA_E_DIVERGED 5        /* SolverError: non-finite residual (relax.cpp:159)  */
+#define FIBRA_E_NOT_CONVERGED 6   /* SolverError: base not converged (stiffness.cpp:75)*/
+#define FIBRA_E_PROBE_FAILED 7    /* SolverError: probe q failed (stiffness.cpp:106-118)*/
+#define FIBRA_E_SINGULAR 8        /* SolverError: [M][T] singular (stiffness.cpp:33)   */
+#define FIBRA_E_CUDA 20           /* CUDA runtime error (call-level)                   */
+#define FIBRA_E_ARG 21            /* bad argument / call order (call-level)            */
+#define FIBRA_E_IO 22             /* IoError (network files)                           */
+
+/* ---- host-side network construction (product mirror of network.cpp / netgen.cpp) --- */
+typedef struct fibra_network fibra_network; /* immutable FiberNetwork (network.hpp:55-101) */
+
+typedef struct {          /* NetGenSpec netgen.hpp:16-33 (defaults in comments)      */
+  int32_t style;          /* 0 segments, 1 knn                                       */
+  int32_t fibers;         /* 200 */
+  int32_t nodes;          /* 60, knn only */
+  double half_length;     /* 0.3, segments only */
+  double merge_radius;    /* 0.05 */
+  int32_t neighbors;      /* 8 */
+  double align_bias;      /* 0 */
+  double align_axis[3];   /* {1,0,0} */
+  double fiber_area;      /* 1 */
+  double fiber_modulus;   /* 1 */
+  double box_half;        /* 0.5 */
+  double tol_bnd;         /* 1e-6 */
+} fibra_netgen_spec;
+
+/* Views into a network's storage: exactly the derived arrays the reference
+ * fibra::FiberNetwork exposes, so the reference-side shim fills it from its own object. */
+typedef struct {
+  int32_t n_nodes, n_fibers, n_free, n_boundary; /* n_free = free DOFs (DofMap::n_free) */
+  const double* coords;            /* 3N node order       FiberNetwork::coords()        */
+  const int32_t* fiber_nodes;      /* 2M (a,b)            fibers()[f].a/.b              */
+  const double* fiber_area;        /* M                   fibers()[f].area              */
+  const double* fiber_modulus;     /* M                   fibers()[f].modulus           */
+  const int32_t* packed_of_dof;    /* 3N                  dof_map().packed_of_dof       */
+  const double* packed_ref;        /* 3N packed order     packed_ref_coords()           */
+  const int32_t* fiber_packed_dofs;/* 6M                  fiber_packed_dofs()           */
+  const double* rest_length;       /* M                   rest_lengths()                */
+  const double* node_lump;         /* N node order        node_lumping()                */
+  const int32_t* boundary_nodes;   /* B ascending         boundary_nodes()              */
+  double box_half;                 /*                     box().half                    */
+  double max_ea;                   /*                     max_ea()                      */
+} fibra_net_desc;
+
+int fibra_network_create(const double* coords, int32_t n_nodes, const int32_t* fiber_nodes,
+                         const double* area, const double* modulus, int32_t n_fibers,
+                         double box_half, double tol_bnd, fibra_network** out);
+int fibra_network_generate(const fibra_netgen_spec* spec, uint64_t seed, fibra_network** out);
+int fibra_network_read(const char* path, double box_half, double tol_bnd, fibra_network** out);
+int fibra_network_write(const fibra_network* net, const char* path);
+int fibra_network_describe(const fibra_network* net, fibra_net_desc* out);
+void fibra_network_free(fibra_network* net);
+const char* fibra_host_last_error(void);
+/* init_batch random policy (batch.cpp:101-104): entry_of_point[p] = mt19937_64(seed)() % n */
+int fibra_assign_random(uint64_t seed, int32_t n_points, int32_t n_entries, int32_t* out);
+
+/* ---- solver configuration records ------------------------------------------------- */
+typedef struct {          /* FiberLaw network.hpp:27-38                              */
+  int32_t kind;           /* 0 linear, 1 exponential                                 */
+  double ea_scale;        /* 1.0 */
+  double nonlinearity;    /* 1.2 */
+  int32_t buckling_off;   /* 0 */
+} fibra_law;
+
+typedef struct {          /* RelaxConfig relax.hpp:15-26                             */
+  double damping;         /* 2.0 */
+  double tolerance;       /* 1e-6 */
+  int64_t max_iterations; /* 500000 */
+  double dt_safety;       /* 0.8 */
+  double density_scale;   /* 1.0 */
+  int32_t energy_check;   /* must be 0 on the device path (verification-only feature) */
+} fibra_relax_cfg;
+
+typedef struct {          /* StiffnessConfig stiffness.hpp:12-17                     */
+  double fd_rel_step;     /* 1e-5 */
+  int32_t reuse_warm;     /* 1 */
+} fibra_stiff_cfg;
+
+typedef struct {          /* RelaxReport relax.hpp:28-36                             */
+  int64_t iterations;
+  double residual, eps_eff, kinetic_fraction, dt;
+  int32_t converged;
+  double energy_drift;
+} fibra_relax_report;
+
+typedef struct {          /* PointResponse macrofem.hpp:48-51 + Response/ResponseStats
+                             stiffness.hpp:19-33; SymTensor3 order xx,yy,zz,yz,xz,xy;
+                             Mandel66 row-major                                        */
+  double sigma[6];
+  double spatial_c[36];
+  double pk2[6];
+  double material_a[36];
+  double stress_asymmetry;
+  fibra_relax_report base_report;
+  int32_t solves;
+  int64_t relax_iterations;
+  int32_t failed_probe;
+  int32_t status;         /* FIBRA_OK or the point's failure code                    */
+} fibra_point_result;
+
+typedef struct {          /* per-call counters for reporting                         */
+  int64_t solves;         /* DR solves run (base + probes)                           */
+  int64_t iterations;     /* sum of DR iterations over all solves                    */
+  int64_t fiber_iterations;  /* sum over solves of iterations * n_fibers             */
+  int64_t pipe_ops;       /* sum over solves of iterations * W_pipe(net)             */
+  float dr_kernel_ms;     /* device time of the persistent DR kernel                 */
+  float total_ms;         /* device time of the whole solve (prep + DR + post)       */
+  int32_t kernel_launches;
+} fibra_solve_stats;
+
+/* ---- device context ----------------------------------------------------------------- */
+typedef struct fibra_ctx fibra_ctx;
+
+int fibra_cuda_open(int device, fibra_ctx** out);
+int fibra_cuda_close(fibra_ctx* ctx);
+const char* fibra_cuda_last_error(const fibra_ctx* ctx);
+/* use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = own */
+int fibra_cuda_set_stream(fibra_ctx* ctx, void* cuda_stream);
+
+/* RveLibrary entries (batch.hpp:33-49): topology to HBM, batched SoA + per-node CSR. */
+int fibra_cuda_upload_library(fibra_ctx* ctx, const fibra_net_desc* entries, int32_t n);
+
+/* BatchAssignment (batch.hpp:53-55): allocates the device PackedStates, zero-filled like
+ * init_batch (batch.cpp:125-143); offsets are the prefix sums of 3*n_nodes. */
+int fibra_cuda_bind_points(fibra_ctx* ctx, const int32_t* entry_of_point, int32_t n_points);
+int fibra_cuda_reset_states(fibra_ctx* ctx);
+/* Warm data host->device: u (total dofs), t, iters, converged (n_points); any may be NULL */
+int fibra_cuda_upload_states(fibra_ctx* ctx, const double* u, const double* t,
+                             const int64_t* iters, const uint8_t* converged);
+/* Device->host writeback of PackedStates; any pointer may be NULL to skip that array. */
+int fibra_cuda_download_states(fibra_ctx* ctx, double* u, double* v, double* a, double* f_int,
+                               double* f_damp, double* mass, double* inv_mass, double* t,
+                               int64_t* iters, uint8_t* converged);
+
+/* batch_response: F (n x 9 row-major Def3) in, one result record per point out.
+ * want_tangent = 1: 1 base + 6 probe solves per point (constitutive_response,
+ * stiffness.cpp:153-175); 0: base solve only (stress).  Host pointers; blocks. */
+int fibra_cuda_solve(fibra_ctx* ctx, const double* F, const fibra_law* law,
+                     const fibra_relax_cfg* relax, const fibra_stiff_cfg* stiff,
+                     int32_t want_tangent, fibra_point_result* out);
+/* Same with F and out already in device memory; asynchronous on the context stream. */
+int fibra_cuda_solve_device(fibra_ctx* ctx, const double* F_dev, const fibra_law* law,
+                            const fibra_relax_cfg* relax, const fibra_stiff_cfg* stiff,
+                            int32_t want_tangent, fibra_point_result* out_dev);
+int fibra_cuda_synchronize(fibra_ctx* ctx);
+/* counters of the last solve (synchronizes) */
+int fibra_cuda_last_stats(fibra_ctx* ctx, fibra_solve_stats* out);
+int fibra_cuda_device_count(int* n);
+/* FP64-pipe roofline denominator measured on this device: independent DADD chains on every
+ * SM; returns lane-operations per second (one DADD/DMUL/DFMA lane = 1 op). */
+int fibra_cuda_fp64_peak(fibra_ctx* ctx, double* lane_ops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

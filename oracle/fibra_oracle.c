@@ -1,0 +1,887 @@
+/*
+ * fibra_oracle.c -- CPU restatement of the reference hot path.  TEST INFRASTRUCTURE:
+ * the parity checker for the B200 solver, never shipped or measured as the product.
+ * Build with -ffp-contract=off (proj/CMakeLists.txt:14-16) so every a*b+c rounds twice,
+ * exactly as the reference does.  See fibra_oracle.h for the pinning story.
+ *
+ * Every function cites the reference function it restates (paths under
+ * /root/reference/proj).  Floating-point expressions keep the reference's evaluation
+ * order (C evaluates a+b+c as (a+b)+c, like C++).
+ */
+#include "fibra_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+static const double kSqrt2 = 1.4142135623730951; /* tensor.cpp:11 */
+
+/* std::max / std::min semantics (first argument wins ties and NaN compares) */
+static inline double smax(double a, double b) { return (a < b) ? b : a; }
+static inline double smin(double a, double b) { return (b < a) ? b : a; }
+
+/* ------------------------------------------------------------------------- */
+/* FiberLaw  network.cpp:16-59                                               */
+/* ------------------------------------------------------------------------- */
+static double law_force(const or_law* law, double ea, double stretch) { /* :16-26 */
+  const double s = law->ea_scale * ea;
+  if (law->buckling_off && stretch < 1.0) return 0.0;
+  if (law->kind == 0) return s * (stretch - 1.0);
+  return s / law->nonlinearity * expm1(law->nonlinearity * (stretch - 1.0));
+}
+
+static double law_tangent(const or_law* law, double ea, double stretch) { /* :28-38 */
+  const double s = law->ea_scale * ea;
+  if (law->buckling_off && stretch < 1.0) return 0.0;
+  if (law->kind == 0) return s;
+  return s * exp(law->nonlinearity * (stretch - 1.0));
+}
+
+static double law_energy(const or_law* law, double ea, double stretch, double rl) { /* :40-53 */
+  const double s = law->ea_scale * ea;
+  if (law->buckling_off && stretch < 1.0) return 0.0;
+  const double e = stretch - 1.0;
+  if (law->kind == 0) return 0.5 * s * rl * e * e;
+  const double b = law->nonlinearity;
+  return rl * s / b * (expm1(b * e) / b - e);
+}
+
+static int law_validate(const or_law* law) { /* :55-59 */
+  if (!(law->ea_scale > 0)) return OR_CONFIG;
+  if (law->kind == 1 && !(law->nonlinearity > 0)) return OR_CONFIG;
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* FiberNetwork constructor  network.cpp:67-157                               */
+/* ------------------------------------------------------------------------- */
+static int cmp_pair(const void* x, const void* y) {
+  const int64_t a = *(const int64_t*)x, b = *(const int64_t*)y;
+  return (a > b) - (a < b);
+}
+
+int or_network_build(const double* coords, int nn, const int32_t* fa, const int32_t* fb,
+                     const double* area, const double* modulus, int nf, double h,
+                     double tol, or_network* net) {
+  memset(net, 0, sizeof *net);
+  if (nn <= 0) return OR_CONFIG;                         /* :71 */
+  if (!(h > 0)) return OR_CONFIG;                        /* :72 */
+  for (int i = 0; i < nn; ++i)                           /* :74-83 */
+    for (int k = 0; k < 3; ++k) {
+      const double c = coords[3 * i + k];
+      if (!isfinite(c)) return OR_CONFIG;
+      if (fabs(c) > h + tol) return OR_CONFIG;
+    }
+  net->n_nodes = nn;
+  net->n_fibers = nf;
+  net->box_half = h;
+  net->tol_bnd = tol;
+  net->coords = malloc(sizeof(double) * 3 * nn);
+  memcpy(net->coords, coords, sizeof(double) * 3 * nn);
+  net->fib_a = malloc(sizeof(int32_t) * (nf ? nf : 1));
+  net->fib_b = malloc(sizeof(int32_t) * (nf ? nf : 1));
+  net->area = malloc(sizeof(double) * (nf ? nf : 1));
+  net->modulus = malloc(sizeof(double) * (nf ? nf : 1));
+  net->rest_length = malloc(sizeof(double) * (nf ? nf : 1));
+  int64_t* keys = malloc(sizeof(int64_t) * (nf ? nf : 1));
+  double max_ea = 0;
+  for (int f = 0; f < nf; ++f) {                         /* :85-107 */
+    const int32_t a = fa[f], b = fb[f];
+    if (a < 0 || b < 0 || a >= nn || b >= nn || a == b) { free(keys); or_network_free(net); return OR_CONFIG; }
+    if (!(area[f] > 0) || !(modulus[f] > 0)) { free(keys); or_network_free(net); return OR_CONFIG; }
+    const int32_t lo = a < b ? a : b, hi = a < b ? b : a;
+    keys[f] = ((int64_t)lo << 32) | (int64_t)hi;
+    const double* xa = coords + 3 * a;
+    const double* xb = coords + 3 * b;
+    const double d0 = xb[0] - xa[0], d1 = xb[1] - xa[1], d2 = xb[2] - xa[2];
+    const double l0 = sqrt(d0 * d0 + d1 * d1 + d2 * d2); /* norm3, tensor.hpp:11-14 */
+    if (!(l0 > 0)) { free(keys); or_network_free(net); return OR_CONFIG; }
+    net->fib_a[f] = a;
+    net->fib_b[f] = b;
+    net->area[f] = area[f];
+    net->modulus[f] = modulus[f];
+    net->rest_length[f] = l0;
+    max_ea = smax(max_ea, area[f] * modulus[f]);
+  }
+  qsort(keys, nf, sizeof(int64_t), cmp_pair);            /* duplicate-fiber check :98-101 */
+  for (int f = 1; f < nf; ++f)
+    if (keys[f] == keys[f - 1]) { free(keys); or_network_free(net); return OR_CONFIG; }
+  free(keys);
+  net->max_ea = max_ea;
+
+  net->boundary_mask = calloc(nn, 1);                    /* :109-117 */
+  net->boundary_nodes = malloc(sizeof(int32_t) * nn);
+  int nb = 0;
+  for (int i = 0; i < nn; ++i) {
+    for (int k = 0; k < 3; ++k)
+      if (fabs(fabs(coords[3 * i + k]) - h) <= tol) net->boundary_mask[i] = 1;
+    if (net->boundary_mask[i]) net->boundary_nodes[nb++] = i;
+  }
+  net->n_boundary = nb;
+  if (nb == 0) { or_network_free(net); return OR_CONFIG; }
+
+  net->packed_of_dof = malloc(sizeof(int32_t) * 3 * nn); /* free-first packing :120-138 */
+  net->dof_of_packed = malloc(sizeof(int32_t) * 3 * nn);
+  int slot = 0;
+  for (int i = 0; i < nn; ++i)
+    if (!net->boundary_mask[i])
+      for (int k = 0; k < 3; ++k) {
+        net->packed_of_dof[3 * i + k] = slot;
+        net->dof_of_packed[slot] = 3 * i + k;
+        ++slot;
+      }
+  net->n_free = slot;
+  for (int i = 0; i < nn; ++i)
+    if (net->boundary_mask[i])
+      for (int k = 0; k < 3; ++k) {
+        net->packed_of_dof[3 * i + k] = slot;
+        net->dof_of_packed[slot] = 3 * i + k;
+        ++slot;
+      }
+  net->packed_ref = malloc(sizeof(double) * 3 * nn);     /* :140-143 */
+  for (int i = 0; i < nn; ++i)
+    for (int k = 0; k < 3; ++k) net->packed_ref[net->packed_of_dof[3 * i + k]] = coords[3 * i + k];
+  net->fiber_dofs = malloc(sizeof(int32_t) * 6 * (nf ? nf : 1)); /* :145-149 */
+  for (int f = 0; f < nf; ++f)
+    for (int k = 0; k < 3; ++k) {
+      net->fiber_dofs[6 * f + k] = net->packed_of_dof[3 * net->fib_a[f] + k];
+      net->fiber_dofs[6 * f + 3 + k] = net->packed_of_dof[3 * net->fib_b[f] + k];
+    }
+  net->node_lump = calloc(nn, sizeof(double));           /* :151-156 */
+  for (int f = 0; f < nf; ++f) {
+    const double half_seg = 0.5 * net->rest_length[f] * net->area[f];
+    net->node_lump[net->fib_a[f]] += half_seg;
+    net->node_lump[net->fib_b[f]] += half_seg;
+  }
+  return OR_OK;
+}
+
+void or_network_free(or_network* n) {
+  free(n->coords); free(n->fib_a); free(n->fib_b); free(n->area); free(n->modulus);
+  free(n->rest_length); free(n->boundary_mask); free(n->boundary_nodes);
+  free(n->packed_of_dof); free(n->dof_of_packed); free(n->packed_ref);
+  free(n->fiber_dofs); free(n->node_lump);
+  memset(n, 0, sizeof *n);
+}
+
+/* ------------------------------------------------------------------------- */
+/* small tensors  tensor.cpp                                                  */
+/* row-major 3x3 (Def3::m), SymTensor3 as {xx,yy,zz,yz,xz,xy}, Mandel66 row-major */
+/* ------------------------------------------------------------------------- */
+double or_det(const double m[9]) { /* Def3::det tensor.cpp:29-33 */
+  return m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+         m[2] * (m[3] * m[7] - m[4] * m[6]);
+}
+
+int or_inverse(const double m[9], double r[9]) { /* Def3::inverse tensor.cpp:35-49 */
+  const double d = or_det(m);
+  if (d == 0.0) return OR_KINEMATICS;
+  r[0] = (m[4] * m[8] - m[5] * m[7]) / d;
+  r[1] = (m[2] * m[7] - m[1] * m[8]) / d;
+  r[2] = (m[1] * m[5] - m[2] * m[4]) / d;
+  r[3] = (m[5] * m[6] - m[3] * m[8]) / d;
+  r[4] = (m[0] * m[8] - m[2] * m[6]) / d;
+  r[5] = (m[2] * m[3] - m[0] * m[5]) / d;
+  r[6] = (m[3] * m[7] - m[4] * m[6]) / d;
+  r[7] = (m[1] * m[6] - m[0] * m[7]) / d;
+  r[8] = (m[0] * m[4] - m[1] * m[3]) / d;
+  return OR_OK;
+}
+
+static void transpose3(const double m[9], double r[9]) { /* tensor.cpp:51-56 */
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r[3 * i + j] = m[3 * j + i];
+}
+
+static void apply3(const double m[9], const double x[3], double y[3]) { /* tensor.cpp:58-62 */
+  y[0] = m[0] * x[0] + m[1] * x[1] + m[2] * x[2];
+  y[1] = m[3] * x[0] + m[4] * x[1] + m[5] * x[2];
+  y[2] = m[6] * x[0] + m[7] * x[1] + m[8] * x[2];
+}
+
+void or_matmul(const double a[9], const double b[9], double r[9]) { /* tensor.cpp:64-73 */
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      double s = 0;
+      for (int k = 0; k < 3; ++k) s += a[3 * i + k] * b[3 * k + j];
+      r[3 * i + j] = s;
+    }
+}
+
+static double sym_get(const double s[6], int i, int j) { /* SymTensor3::operator() tensor.cpp:75-79 */
+  if (i == j) return i == 0 ? s[0] : (i == 1 ? s[1] : s[2]);
+  const int k = i + j;
+  return k == 1 ? s[5] : (k == 2 ? s[4] : s[3]);
+}
+
+void or_sym_full(const double s[6], double a[9]) { /* SymTensor3::full tensor.cpp:90-99 */
+  a[0] = s[0]; a[4] = s[1]; a[8] = s[2];
+  a[5] = a[7] = s[3];
+  a[2] = a[6] = s[4];
+  a[1] = a[3] = s[5];
+}
+
+void or_sym_from_full(const double a[9], double s[6]) { /* tensor.cpp:101-110 */
+  s[0] = a[0];
+  s[1] = a[4];
+  s[2] = a[8];
+  s[3] = 0.5 * (a[5] + a[7]);
+  s[4] = 0.5 * (a[2] + a[6]);
+  s[5] = 0.5 * (a[1] + a[3]);
+}
+
+static double sym_frobenius(const double a[6]) { /* tensor.hpp:53 + ddot tensor.cpp:112-115 */
+  return sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2] +
+              2.0 * (a[3] * a[3] + a[4] * a[4] + a[5] * a[5]));
+}
+
+void or_mandel(const double s[6], double v[6]) { /* tensor.cpp:127-136 */
+  v[0] = s[0];
+  v[1] = s[1];
+  v[2] = s[2];
+  v[3] = kSqrt2 * s[3];
+  v[4] = kSqrt2 * s[4];
+  v[5] = kSqrt2 * s[5];
+}
+
+static void unmandel(const double v[6], double s[6]) { /* tensor.cpp:138-147 */
+  s[0] = v[0];
+  s[1] = v[1];
+  s[2] = v[2];
+  s[3] = v[3] / kSqrt2;
+  s[4] = v[4] / kSqrt2;
+  s[5] = v[5] / kSqrt2;
+}
+
+static void m66_matmul(const double a[36], const double b[36], double r[36]) { /* tensor.cpp:159-168 */
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) {
+      double s = 0;
+      for (int k = 0; k < 6; ++k) s += a[6 * i + k] * b[6 * k + j];
+      r[6 * i + j] = s;
+    }
+}
+
+static const int kMI[6] = {0, 1, 2, 1, 0, 0}; /* tensor.hpp:104-105 */
+static const int kMJ[6] = {0, 1, 2, 2, 2, 1};
+
+void or_mandel_M_of_U(const double u[6], double m[36]) { /* tensor.cpp:238-256 */
+  for (int p = 0; p < 6; ++p) {
+    const int k = kMI[p], l = kMJ[p];
+    const double wp = p < 3 ? 1.0 : kSqrt2;
+    for (int q = 0; q < 6; ++q) {
+      const int r = kMI[q], s = kMJ[q];
+      const double wq = q < 3 ? 1.0 : kSqrt2;
+      double v = 0.0;
+      v += (k == s ? sym_get(u, r, l) : 0.0);
+      v += (l == s ? sym_get(u, r, k) : 0.0);
+      v += (k == r ? sym_get(u, s, l) : 0.0);
+      v += (l == r ? sym_get(u, s, k) : 0.0);
+      m[6 * p + q] = 0.25 * wp * wq * v;
+    }
+  }
+}
+
+void or_probing_matrix(double t[36]) { /* tensor.cpp:258-273 */
+  const double h = 0.5;
+  const double s = 0.5 * kSqrt2;
+  const double rows[36] = {h, 0, 0, 0, s, s,  0, h, 0, s, 0, s,  0, 0, h, s, s, 0,
+                           0, 0, 0, 1, 0, 0,  0, 0, 0, 0, 1, 0,  0, 0, 0, 0, 0, 1};
+  memcpy(t, rows, sizeof rows);
+}
+
+void or_probing_direction(int q, double dir[6]) { /* tensor.cpp:275-284 */
+  double t[36], col[6];
+  or_probing_matrix(t);
+  for (int i = 0; i < 6; ++i) col[i] = t[6 * i + q];
+  unmandel(col, dir);
+}
+
+int or_push_forward_stiffness(const double a[36], const double f[9], double c[36]) {
+  /* tensor.cpp:286-300 */
+  const double j = or_det(f);
+  if (!(j > 0.0)) return OR_KINEMATICS;
+  double b[36], ft[9];
+  transpose3(f, ft);
+  for (int q = 0; q < 6; ++q) {
+    double e[6] = {0, 0, 0, 0, 0, 0}, s[6], sf[9], t1[9], fs[9], sym[6], col[6];
+    e[q] = 1.0;
+    unmandel(e, s);
+    or_sym_full(s, sf);
+    or_matmul(f, sf, t1);
+    or_matmul(t1, ft, fs);
+    or_sym_from_full(fs, sym);
+    or_mandel(sym, col);
+    for (int p = 0; p < 6; ++p) b[6 * p + q] = col[p];
+  }
+  double bt[36], ba[36], bab[36];
+  for (int i = 0; i < 6; ++i)
+    for (int k = 0; k < 6; ++k) bt[6 * i + k] = b[6 * k + i];
+  m66_matmul(b, a, ba);
+  m66_matmul(ba, bt, bab);
+  const double inv = 1.0 / j;
+  for (int i = 0; i < 36; ++i) c[i] = bab[i] * inv;
+  return OR_OK;
+}
+
+int or_pull_back_stress(const double sig[6], const double f[9], double out[6]) {
+  /* tensor.cpp:309-315 */
+  const double j = or_det(f);
+  if (!(j > 0.0)) return OR_KINEMATICS;
+  double finv[9], finvt[9], sf[9], t1[9], s[9], sym[6];
+  if (or_inverse(f, finv)) return OR_KINEMATICS;
+  transpose3(finv, finvt);
+  or_sym_full(sig, sf);
+  or_matmul(finv, sf, t1);
+  or_matmul(t1, finvt, s);
+  or_sym_from_full(s, sym);
+  for (int i = 0; i < 6; ++i) out[i] = sym[i] * j;
+  return OR_OK;
+}
+
+/* Symmetric 3x3 eigensolver (cyclic Jacobi).  RESTATEMENT of the Eigen
+ * SelfAdjointEigenSolver call in polar_decompose tensor.cpp:208-215; Eigen's bits are
+ * not reproducible here (Eigen absent), parity across that boundary is tolerance-only.
+ * The device solver (csrc/tensor.cuh) runs the identical sequence of IEEE operations. */
+static void jacobi3(double a[9], double q[9]) {
+  for (int i = 0; i < 9; ++i) q[i] = (i % 4 == 0) ? 1.0 : 0.0;
+  static const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < 3; ++r) {
+      const int p = P[r], qq = Q[r];
+      const double apq = a[3 * p + qq];
+      const double app = a[3 * p + p], aqq = a[3 * qq + qq];
+      if (fabs(apq) <= 1e-18 * (fabs(app) + fabs(aqq))) {
+        a[3 * p + qq] = a[3 * qq + p] = 0.0;
+        continue;
+      }
+      rotated = 1;
+      const double tau = (aqq - app) / (2.0 * apq);
+      const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
+                                  : -1.0 / (-tau + sqrt(1.0 + tau * tau));
+      const double c = 1.0 / sqrt(1.0 + t * t);
+      const double s = t * c;
+      a[3 * p + p] = app - t * apq;
+      a[3 * qq + qq] = aqq + t * apq;
+      a[3 * p + qq] = a[3 * qq + p] = 0.0;
+      const int o = 3 - p - qq;
+      const double arp = a[3 * o + p], arq = a[3 * o + qq];
+      a[3 * o + p] = a[3 * p + o] = c * arp - s * arq;
+      a[3 * o + qq] = a[3 * qq + o] = s * arp + c * arq;
+      for (int k = 0; k < 3; ++k) {
+        const double qkp = q[3 * k + p], qkq = q[3 * k + qq];
+        q[3 * k + p] = c * qkp - s * qkq;
+        q[3 * k + qq] = s * qkp + c * qkq;
+      }
+    }
+    if (!rotated) break;
+  }
+}
+
+int or_polar_decompose(const double f[9], double rot[9], double u6[6]) {
+  /* tensor.cpp:203-224 */
+  const double j = or_det(f);
+  if (!(j > 0.0)) return OR_KINEMATICS;
+  double ft[9], c[9], q[9];
+  transpose3(f, ft);
+  or_matmul(ft, f, c);
+  jacobi3(c, q);
+  double lam[3] = {c[0], c[4], c[8]};
+  if (lam[0] <= 0.0 || lam[1] <= 0.0 || lam[2] <= 0.0) return OR_KINEMATICS;
+  double sq[3], isq[3];
+  for (int k = 0; k < 3; ++k) {
+    sq[k] = sqrt(lam[k]);
+    isq[k] = 1.0 / sq[k];
+  }
+  double u[9], uinv[9];
+  for (int i = 0; i < 3; ++i)
+    for (int jj = 0; jj < 3; ++jj) {
+      double s = 0, si = 0;
+      for (int k = 0; k < 3; ++k) {
+        s += (q[3 * i + k] * sq[k]) * q[3 * jj + k];
+        si += (q[3 * i + k] * isq[k]) * q[3 * jj + k];
+      }
+      u[3 * i + jj] = s;
+      uinv[3 * i + jj] = si;
+    }
+  or_matmul(f, uinv, rot);
+  or_sym_from_full(u, u6);
+  return OR_OK;
+}
+
+/* 6x6 full-pivot LU solve of ([M][T])^T [A]^T = [P]^T.  RESTATEMENT of
+ * Eigen::FullPivLU (stiffness.cpp:26-39): largest |entry| pivot of the trailing block
+ * (first in column-major scan), rank threshold |pivot| > 6*eps*max|pivot|, forward
+ * then backward substitution, column permutation undone last. */
+static int fullpiv_solve6(const double a_in[36], const double rhs[36], double x[36]) {
+  double lu[36], c[36];
+  int rt[6], ct[6];
+  memcpy(lu, a_in, sizeof lu);
+  double maxpivot = 0;
+  int nonzero = 6;
+  for (int k = 0; k < 6; ++k) {
+    double big = -1.0;
+    int br = k, bc = k;
+    for (int jj = k; jj < 6; ++jj)
+      for (int i = k; i < 6; ++i) {
+        const double v = fabs(lu[6 * i + jj]);
+        if (v > big) { big = v; br = i; bc = jj; }
+      }
+    if (big == 0.0) {
+      nonzero = k;
+      for (int i = k; i < 6; ++i) rt[i] = ct[i] = i;
+      break;
+    }
+    if (big > maxpivot) maxpivot = big;
+    rt[k] = br;
+    ct[k] = bc;
+    if (br != k)
+      for (int jj = 0; jj < 6; ++jj) { double t = lu[6 * k + jj]; lu[6 * k + jj] = lu[6 * br + jj]; lu[6 * br + jj] = t; }
+    if (bc != k)
+      for (int i = 0; i < 6; ++i) { double t = lu[6 * i + k]; lu[6 * i + k] = lu[6 * i + bc]; lu[6 * i + bc] = t; }
+    if (k < 5) {
+      const double piv = lu[6 * k + k];
+      for (int i = k + 1; i < 6; ++i) lu[6 * i + k] /= piv;
+      for (int jj = k + 1; jj < 6; ++jj)
+        for (int i = k + 1; i < 6; ++i) lu[6 * i + jj] -= lu[6 * i + k] * lu[6 * k + jj];
+    }
+  }
+  const double thr = maxpivot * (DBL_EPSILON * 6.0);
+  int rank = 0;
+  for (int i = 0; i < nonzero; ++i) rank += fabs(lu[6 * i + i]) > thr;
+  if (rank != 6) return OR_SINGULAR;
+  memcpy(c, rhs, sizeof c);
+  for (int k = 0; k < 6; ++k)
+    if (rt[k] != k)
+      for (int jj = 0; jj < 6; ++jj) { double t = c[6 * k + jj]; c[6 * k + jj] = c[6 * rt[k] + jj]; c[6 * rt[k] + jj] = t; }
+  for (int jj = 0; jj < 6; ++jj) {
+    for (int k = 0; k < 6; ++k)          /* unit lower, column oriented */
+      for (int i = k + 1; i < 6; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
+    for (int k = 5; k >= 0; --k) {       /* upper, column oriented */
+      c[6 * k + jj] /= lu[6 * k + k];
+      for (int i = 0; i < k; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
+    }
+  }
+  for (int k = 5; k >= 0; --k)
+    if (ct[k] != k)
+      for (int jj = 0; jj < 6; ++jj) { double t = c[6 * k + jj]; c[6 * k + jj] = c[6 * ct[k] + jj]; c[6 * ct[k] + jj] = t; }
+  memcpy(x, c, sizeof c);
+  return OR_OK;
+}
+
+int or_material_stiffness_from_probes(const double u[6], const double base_pk2[6],
+                                      const double probe_pk2[36], double h, double a[36]) {
+  /* stiffness.cpp:15-41 */
+  double base[6], p[36], m[36], t[36], mt[36], mtt[36], pt[36], at[36];
+  or_mandel(base_pk2, base);
+  for (int q = 0; q < 6; ++q) {
+    double col[6];
+    or_mandel(probe_pk2 + 6 * q, col);
+    for (int i = 0; i < 6; ++i) p[6 * i + q] = (col[i] - base[i]) / h;
+  }
+  or_mandel_M_of_U(u, m);
+  or_probing_matrix(t);
+  m66_matmul(m, t, mt);
+  for (int i = 0; i < 6; ++i)
+    for (int jj = 0; jj < 6; ++jj) {
+      mtt[6 * i + jj] = mt[6 * jj + i];
+      pt[6 * i + jj] = p[6 * jj + i];
+    }
+  const int st = fullpiv_solve6(mtt, pt, at);
+  if (st) return st;
+  for (int i = 0; i < 6; ++i)
+    for (int jj = 0; jj < 6; ++jj) a[6 * i + jj] = at[6 * jj + i];
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* BLAS-1 contract  kernels_scalar.cpp:7-65 (4 interleaved partials)          */
+/* ------------------------------------------------------------------------- */
+double or_norm2_sq(int64_t n, const double* x) { /* kernels_scalar.cpp:20-33 */
+  double s[4] = {0, 0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) s[i & 3] += x[i] * x[i];
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+double or_weighted_sq(int64_t n, const double* w, const double* x) { /* :35-48 */
+  double s[4] = {0, 0, 0, 0};
+  for (int64_t i = 0; i < n; ++i) s[i & 3] += w[i] * (x[i] * x[i]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+/* ------------------------------------------------------------------------- */
+/* forces, BC, stress  network.cpp                                            */
+/* ------------------------------------------------------------------------- */
+int or_apply_affine_bc(const or_network* net, const double F[9], or_state st) {
+  /* network.cpp:254-269 */
+  const double j = or_det(F);
+  if (!(j > 0)) return OR_KINEMATICS;
+  for (int b = 0; b < net->n_boundary; ++b) {
+    const int node = net->boundary_nodes[b];
+    const double* x = net->coords + 3 * node;
+    double fx[3];
+    apply3(F, x, fx);
+    for (int k = 0; k < 3; ++k) {
+      const int p = net->packed_of_dof[3 * node + k];
+      st.u[p] = fx[k] - x[k];
+      st.v[p] = 0.0;
+      st.a[p] = 0.0;
+    }
+  }
+  if (st.converged) *st.converged = 0;
+  return OR_OK;
+}
+
+int or_internal_forces_cfl(const or_network* net, const or_law* law, const double* u,
+                           double* f_int, const double* mred_l0, double* min_dtsq_out) {
+  /* force_loop<WithCfl> network.cpp:275-311 */
+  const int nd = 3 * net->n_nodes;
+  for (int i = 0; i < nd; ++i) f_int[i] = 0.0;
+  const double* ref = net->packed_ref;
+  double min_dtsq = INFINITY;
+  for (int f = 0; f < net->n_fibers; ++f) {
+    const int32_t* p = net->fiber_dofs + 6 * f;
+    const double dx = (ref[p[3]] + u[p[3]]) - (ref[p[0]] + u[p[0]]);
+    const double dy = (ref[p[4]] + u[p[4]]) - (ref[p[1]] + u[p[1]]);
+    const double dz = (ref[p[5]] + u[p[5]]) - (ref[p[2]] + u[p[2]]);
+    const double len = sqrt(dx * dx + dy * dy + dz * dz);
+    const double l0 = net->rest_length[f];
+    if (len <= 1e-8 * l0) return OR_COLLAPSE;
+    const double stretch = len / l0;
+    const double ea = net->area[f] * net->modulus[f];
+    const double n_ax = law_force(law, ea, stretch);
+    const double g = n_ax / len;
+    f_int[p[0]] -= g * dx;
+    f_int[p[1]] -= g * dy;
+    f_int[p[2]] -= g * dz;
+    f_int[p[3]] += g * dx;
+    f_int[p[4]] += g * dy;
+    f_int[p[5]] += g * dz;
+    if (mred_l0) {
+      const double kt = smax(fabs(law_tangent(law, ea, stretch)), law->ea_scale * ea);
+      min_dtsq = smin(min_dtsq, mred_l0[f] / kt);
+    }
+  }
+  if (min_dtsq_out) *min_dtsq_out = min_dtsq;
+  return OR_OK;
+}
+
+double or_strain_energy(const or_network* net, const or_law* law, const double* u) {
+  /* relax.cpp:57-72 */
+  const double* ref = net->packed_ref;
+  double e = 0;
+  for (int f = 0; f < net->n_fibers; ++f) {
+    const int32_t* p = net->fiber_dofs + 6 * f;
+    const double dx = (ref[p[3]] + u[p[3]]) - (ref[p[0]] + u[p[0]]);
+    const double dy = (ref[p[4]] + u[p[4]]) - (ref[p[1]] + u[p[1]]);
+    const double dz = (ref[p[5]] + u[p[5]]) - (ref[p[2]] + u[p[2]]);
+    const double len = sqrt(dx * dx + dy * dy + dz * dz);
+    const double l0 = net->rest_length[f];
+    e += law_energy(law, net->area[f] * net->modulus[f], len / l0, l0);
+  }
+  return e;
+}
+
+int or_homogenized_stress(const or_network* net, const or_state* st, const double F[9],
+                          double sigma[6], double* asym_out) {
+  /* network.cpp:341-372 */
+  if (!st->converged || !*st->converged) return OR_NOT_CONVERGED_STATE;
+  const double h = net->box_half;
+  const double vol = or_det(F) * (8.0 * h * h * h);
+  const double* ref = net->packed_ref;
+  double s[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int b = 0; b < net->n_boundary; ++b) {
+    const int node = net->boundary_nodes[b];
+    double r[3], x[3];
+    for (int k = 0; k < 3; ++k) {
+      const int p = net->packed_of_dof[3 * node + k];
+      r[k] = st->f_int[p];
+      x[k] = ref[p] + st->u[p];
+    }
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) s[i][j] += r[i] * x[j];
+  }
+  double raw[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) raw[3 * i + j] = s[i][j] / vol;
+  double asym = 0, mag = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      asym += (raw[3 * i + j] - raw[3 * j + i]) * (raw[3 * i + j] - raw[3 * j + i]);
+      mag += raw[3 * i + j] * raw[3 * i + j];
+    }
+  or_sym_from_full(raw, sigma);
+  *asym_out = mag > 0 ? sqrt(asym / mag) : 0.0;
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* relax_solve  relax.cpp:93-191                                              */
+/* ------------------------------------------------------------------------- */
+static int relax_validate(const or_relax_cfg* c) { /* relax.cpp:12-19 */
+  if (!(c->damping >= 0)) return OR_CONFIG;
+  if (!(c->tolerance > 0)) return OR_CONFIG;
+  if (c->max_iterations < 1) return OR_CONFIG;
+  if (!(c->dt_safety > 0) || c->dt_safety > 1) return OR_CONFIG;
+  if (!(c->density_scale > 0)) return OR_CONFIG;
+  return OR_OK;
+}
+
+int or_relax_solve(const or_network* net, const or_law* law, const double F[9],
+                   const or_relax_cfg* cfg, or_state st, int warm_reuse,
+                   or_relax_report* rep) {
+  memset(rep, 0, sizeof *rep);
+  int rc = relax_validate(cfg);
+  if (rc) return rc;
+  if ((rc = law_validate(law))) return rc;
+  const int n_dof = st.n_dof, n_free = st.n_free;
+  if (n_dof != 3 * net->n_nodes || n_free != net->n_free) return OR_CONFIG;
+
+  /* setup_mass relax.cpp:25-44 */
+  double max_lump = 0;
+  for (int i = 0; i < net->n_nodes; ++i) {
+    if (!(net->node_lump[i] > 0)) return OR_CONFIG;
+    max_lump = smax(max_lump, net->node_lump[i]);
+  }
+  const double scale = cfg->density_scale / max_lump;
+  for (int i = 0; i < net->n_nodes; ++i) {
+    const double m = net->node_lump[i] * scale;
+    for (int k = 0; k < 3; ++k) {
+      const int p = net->packed_of_dof[3 * i + k];
+      st.mass[p] = m;
+      st.inv_mass[p] = 1.0 / m;
+    }
+  }
+  if (!warm_reuse)                                       /* relax.cpp:104-105 */
+    for (int i = 0; i < n_free; ++i) st.u[i] = 0.0;
+  for (int i = 0; i < n_dof; ++i) st.v[i] = st.a[i] = st.f_damp[i] = 0.0; /* :106-108 */
+  if ((rc = or_apply_affine_bc(net, F, st))) return rc;   /* :109 */
+
+  double* mred = malloc(sizeof(double) * (net->n_fibers ? net->n_fibers : 1)); /* :46-55 */
+  for (int f = 0; f < net->n_fibers; ++f) {
+    const double ma = st.mass[net->fiber_dofs[6 * f]];
+    const double mb = st.mass[net->fiber_dofs[6 * f + 3]];
+    mred[f] = ma * mb / (ma + mb) * net->rest_length[f];
+  }
+  const double force_floor = law->ea_scale * net->max_ea * 1e-12; /* :112 */
+  double* u = st.u;
+  double* v = st.v;
+  double* a = st.a;
+  double* fi = st.f_int;
+  double* fdmp = st.f_damp;
+  const int64_t nf = n_free, nfix = n_dof - n_free;
+  const double c = cfg->damping;
+
+  double min_dtsq = 0;
+  if ((rc = or_internal_forces_cfl(net, law, u, fi, mred, &min_dtsq))) { free(mred); return rc; }
+  double residual = sqrt(or_norm2_sq(nf, fi));
+  double react = sqrt(or_norm2_sq(nfix, fi + n_free));
+  double eps_eff = cfg->tolerance * smax(react, force_floor);
+  rep->eps_eff = eps_eff;
+  rep->residual = residual;
+  if (residual <= eps_eff) {                             /* :138-143 */
+    rep->converged = 1;
+    if (st.converged) *st.converged = 1;
+    rep->kinetic_fraction = 0.0;
+    free(mred);
+    return OR_OK;
+  }
+  for (int64_t i = 0; i < nf; ++i) {                     /* accel :145 */
+    const double d = c * st.mass[i] * v[i];
+    fdmp[i] = d;
+    a[i] = -(fi[i] + d) * st.inv_mass[i];
+  }
+  int64_t n = 0;
+  while (n < cfg->max_iterations) {                      /* hot loop :148-179 */
+    ++n;
+    const double dt = cfg->dt_safety * sqrt(min_dtsq);
+    if (!isfinite(dt) || !(dt > 0)) { free(mred); return OR_BAD_DT; }
+    if (st.t) *st.t += dt;
+    const double hdt = 0.5 * dt;
+    for (int64_t i = 0; i < nf; ++i) v[i] += hdt * a[i];
+    for (int64_t i = 0; i < nf; ++i) u[i] += dt * v[i];
+    if ((rc = or_internal_forces_cfl(net, law, u, fi, mred, &min_dtsq))) { free(mred); return rc; }
+    residual = sqrt(or_norm2_sq(nf, fi));
+    if (!isfinite(residual)) { free(mred); return OR_DIVERGED; }
+    react = sqrt(or_norm2_sq(nfix, fi + n_free));
+    eps_eff = cfg->tolerance * smax(react, force_floor);
+    for (int64_t i = 0; i < nf; ++i) {
+      const double d = c * st.mass[i] * v[i];
+      fdmp[i] = d;
+      a[i] = -(fi[i] + d) * st.inv_mass[i];
+    }
+    for (int64_t i = 0; i < nf; ++i) v[i] += hdt * a[i];
+    rep->dt = dt;
+    if (residual <= eps_eff) {
+      rep->converged = 1;
+      break;
+    }
+  }
+  rep->iterations = n;                                   /* exit :181-190 */
+  rep->residual = residual;
+  rep->eps_eff = eps_eff;
+  rep->energy_drift = 0;
+  const double ke = 0.5 * or_weighted_sq(nf, st.mass, v);
+  const double se = or_strain_energy(net, law, u);
+  rep->kinetic_fraction = (ke + se) > 0 ? ke / (ke + se) : 0.0;
+  if (st.iters) *st.iters += n;
+  if (st.converged) *st.converged = rep->converged ? 1 : 0;
+  free(mred);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* constitutive_response  stiffness.cpp:66-175                                 */
+/* ------------------------------------------------------------------------- */
+int or_constitutive_response(const or_network* net, const or_law* law, const double F[9],
+                             const or_relax_cfg* rcfg, double fd_rel_step, int reuse_warm,
+                             int want_tangent, or_state st, or_response* out) {
+  memset(out, 0, sizeof *out);
+  out->failed_probe = -1;
+  if (!(fd_rel_step > 0) || fd_rel_step >= 1e-2) return OR_CONFIG; /* :10-13 */
+  /* solve_base :66-83 */
+  double R[9], U[6], fu[9];
+  int rc = or_polar_decompose(F, R, U);
+  if (rc) return rc;
+  or_sym_full(U, fu);
+  or_relax_report rep;
+  rc = or_relax_solve(net, law, fu, rcfg, st, 1, &rep);
+  if (rc) return rc;
+  if (!rep.converged) return OR_NOT_CONVERGED;
+  double sigma_u[6], asym, pk2[6];
+  if ((rc = or_homogenized_stress(net, &st, fu, sigma_u, &asym))) return rc;
+  if ((rc = or_pull_back_stress(sigma_u, fu, pk2))) return rc;
+  out->solves = 1;
+  out->relax_iterations = rep.iterations;
+  out->base_report = rep;
+  memcpy(out->pk2, pk2, sizeof pk2);
+  out->stress_asymmetry = asym;
+
+  if (want_tangent) {
+    const double h = fd_rel_step * sym_frobenius(U); /* probe_step :125-127 */
+    const int nd = st.n_dof;
+    double* buf = calloc((size_t)7 * nd, sizeof(double));
+    double tsc = 0;
+    int64_t isc = 0;
+    uint8_t csc = 0;
+    or_state sc = {buf, buf + nd, buf + 2 * nd, buf + 3 * nd, buf + 4 * nd, buf + 5 * nd,
+                   buf + 6 * nd, &tsc, &isc, &csc, st.n_free, nd};
+    double probes[36];
+    for (int q = 0; q < 6; ++q) { /* probe_pk2s :86-123 */
+      double dir[6], up[6], fq[9];
+      or_probing_direction(q, dir);
+      for (int i = 0; i < 6; ++i) up[i] = U[i] + dir[i] * h;
+      or_sym_full(up, fq);
+      if (!(or_det(fq) > 0)) { free(buf); return OR_PROBE_FAILED; }
+      if (reuse_warm) memcpy(sc.u, st.u, sizeof(double) * nd);
+      or_relax_report pr;
+      rc = or_relax_solve(net, law, fq, rcfg, sc, reuse_warm, &pr);
+      if (rc) {
+        out->failed_probe = q;
+        free(buf);
+        return rc == OR_CONFIG ? rc : OR_PROBE_FAILED;
+      }
+      ++out->solves;
+      out->relax_iterations += pr.iterations;
+      if (!pr.converged) { out->failed_probe = q; free(buf); return OR_PROBE_FAILED; }
+      double sq[6], aq;
+      if ((rc = or_homogenized_stress(net, &sc, fq, sq, &aq))) { free(buf); return rc; }
+      if ((rc = or_pull_back_stress(sq, fq, probes + 6 * q))) { free(buf); return rc; }
+    }
+    free(buf);
+    if ((rc = or_material_stiffness_from_probes(U, pk2, probes, h, out->material_a))) return rc;
+    if ((rc = or_push_forward_stiffness(out->material_a, F, out->spatial_c))) return rc;
+  }
+  double su[9], rt[9], t1[9], s9[9];
+  or_sym_full(sigma_u, su);
+  transpose3(R, rt);
+  or_matmul(R, su, t1);
+  or_matmul(t1, rt, s9);
+  or_sym_from_full(s9, out->sigma);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* batch_response  batch.cpp:155-187                                          */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  const or_network* const* entries;
+  const int32_t* entry_of_point;
+  int n_points;
+  const int64_t* offsets;
+  double *u, *v, *a, *f_int, *f_damp, *mass, *inv_mass, *t;
+  int64_t* iters;
+  uint8_t* converged;
+  const int32_t* n_free;
+  const or_law* law;
+  const double* F;
+  const or_relax_cfg* rcfg;
+  double fd;
+  int reuse, tangent;
+  or_response* out;
+  int32_t* status;
+  int next;
+  int config_error;
+  pthread_mutex_t mu;
+} batch_job;
+
+static void solve_point(batch_job* j, int p) {
+  const or_network* net = j->entries[j->entry_of_point[p]];
+  const int64_t lo = j->offsets[p];
+  const int nd = (int)(j->offsets[p + 1] - lo);
+  or_state st = {j->u + lo, j->v + lo, j->a + lo, j->f_int + lo, j->f_damp + lo,
+                 j->mass + lo, j->inv_mass + lo, j->t + p, j->iters + p, j->converged + p,
+                 j->n_free[p], nd};
+  or_response r;
+  const int rc = or_constitutive_response(net, j->law, j->F + 9 * p, j->rcfg, j->fd, j->reuse,
+                                          j->tangent, st, &r);
+  if (rc == OR_CONFIG) {
+    pthread_mutex_lock(&j->mu);
+    j->config_error = 1;
+    pthread_mutex_unlock(&j->mu);
+  }
+  if (rc) {
+    memset(&j->out[p], 0, sizeof(or_response)); /* value-initialized slot */
+    j->out[p].failed_probe = -1;
+  } else {
+    j->out[p] = r;
+  }
+  j->status[p] = rc;
+}
+
+static void* batch_worker(void* arg) {
+  batch_job* j = arg;
+  for (;;) {
+    pthread_mutex_lock(&j->mu);
+    const int p = j->next++;
+    pthread_mutex_unlock(&j->mu);
+    if (p >= j->n_points) return NULL;
+    solve_point(j, p);
+  }
+}
+
+int or_batch_response(const or_network* const* entries, const int32_t* entry_of_point,
+                      int n_points, const int64_t* offsets, double* u, double* v, double* a,
+                      double* f_int, double* f_damp, double* mass, double* inv_mass, double* t,
+                      int64_t* iters, uint8_t* converged, const int32_t* n_free,
+                      const or_law* law, const double* F, const or_relax_cfg* rcfg,
+                      double fd_rel_step, int reuse_warm, int want_tangent, int n_threads,
+                      or_response* out, int32_t* status) {
+  batch_job j = {entries, entry_of_point, n_points, offsets, u, v, a, f_int, f_damp, mass,
+                 inv_mass, t, iters, converged, n_free, law, F, rcfg, fd_rel_step, reuse_warm,
+                 want_tangent, out, status, 0, 0};
+  pthread_mutex_init(&j.mu, NULL);
+  if (n_threads <= 1) {
+    for (int p = 0; p < n_points; ++p) solve_point(&j, p);
+  } else {
+    pthread_t* th = malloc(sizeof(pthread_t) * n_threads);
+    for (int i = 0; i < n_threads; ++i) pthread_create(&th[i], NULL, batch_worker, &j);
+    for (int i = 0; i < n_threads; ++i) pthread_join(th[i], NULL);
+    free(th);
+  }
+  pthread_mutex_destroy(&j.mu);
+  return j.config_error ? OR_CONFIG : OR_OK;
+}

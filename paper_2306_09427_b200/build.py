@@ -1,0 +1,60 @@
+"""Build the in-tree CUDA library ``paper_2306_09427_b200/lib/libfibra_b200.so``.
+
+sm_100a only (``-gencode arch=compute_100a,code=sm_100a``).  ``--fmad=false`` is part of
+the numerical contract: the reference forbids FMA contraction (proj/CMakeLists.txt:14-16)
+and the DR trajectory is reproduced bit for bit.  Host C++ gets ``-ffp-contract=off`` for
+the same reason (the network generator must emit the reference's exact coordinates).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_DIR = os.path.join(HERE, "lib")
+LIB = os.path.join(LIB_DIR, "libfibra_b200.so")
+SOURCES = [
+    os.path.join(HERE, "csrc", "fibra_cuda.cu"),
+    os.path.join(HERE, "csrc", "host", "network.cpp"),
+    os.path.join(HERE, "csrc", "host", "netgen.cpp"),
+]
+DEPS = SOURCES + [
+    os.path.join(HERE, "csrc", "dr_kernel.cuh"),
+    os.path.join(HERE, "csrc", "tensor.cuh"),
+    os.path.join(HERE, "csrc", "host", "host_internal.hpp"),
+    os.path.join(ROOT, "include", "fibra_cuda.h"),
+]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    os.makedirs(LIB_DIR, exist_ok=True)
+    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "--fmad=false", "-lineinfo",
+           "-Xptxas", "-v" if verbose else "-O3",
+           "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
+           "-shared", "-o", LIB + ".tmp", *SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc build of libfibra_b200.so failed")
+    if verbose:
+        sys.stderr.write(r.stderr)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
