@@ -189,7 +189,8 @@ def main():
     n = len(F)
     lib = P.RveLibrary([net])
     assign = P.BatchAssignment(np.zeros(n, np.int32))
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream(device=local)  # explicit stream shared by torch and the solver
+    torch.cuda.set_stream(stream)
     db = P.DeviceBatch(lib, assign, device=local, stream=stream.cuda_stream)
     rec_bytes = P.RESULT_DTYPE.itemsize
     F_dev = torch.from_numpy(F).to(f"cuda:{local}")
