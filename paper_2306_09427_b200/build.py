@@ -4,6 +4,10 @@ sm_100a only (``-gencode arch=compute_100a,code=sm_100a``).  ``--fmad=false`` is
 the numerical contract: the reference forbids FMA contraction (proj/CMakeLists.txt:14-16)
 and the DR trajectory is reproduced bit for bit.  Host C++ gets ``-ffp-contract=off`` for
 the same reason (the network generator must emit the reference's exact coordinates).
+
+``FIBRA_PHASE_PROF=1`` builds the diagnostics variant ``libfibra_b200_prof.so`` whose DR
+kernel accumulates per-warp phase cycle counters (see dr_kernel.cuh FB_PROF); the loader
+picks it when the same variable is set at run time.
 """
 from __future__ import annotations
 
@@ -14,16 +18,20 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_DIR = os.path.join(HERE, "lib")
-LIB = os.path.join(LIB_DIR, "libfibra_b200.so")
+PROF = bool(os.environ.get("FIBRA_PHASE_PROF"))
+LIB = os.path.join(LIB_DIR, "libfibra_b200_prof.so" if PROF else "libfibra_b200.so")
 SOURCES = [
     os.path.join(HERE, "csrc", "fibra_cuda.cu"),
     os.path.join(HERE, "csrc", "host", "network.cpp"),
     os.path.join(HERE, "csrc", "host", "netgen.cpp"),
+    os.path.join(HERE, "csrc", "host", "schedule.cpp"),
 ]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "dr_kernel.cuh"),
     os.path.join(HERE, "csrc", "tensor.cuh"),
+    os.path.join(HERE, "csrc", "fastmath.cuh"),
     os.path.join(HERE, "csrc", "host", "host_internal.hpp"),
+    os.path.join(HERE, "csrc", "host", "schedule.hpp"),
     os.path.join(ROOT, "include", "fibra_cuda.h"),
 ]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -45,6 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xptxas", "-v" if verbose else "-O3",
            "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
            "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
+           *(["-DFIBRA_PHASE_PROF=1"] if PROF else []),
            "-shared", "-o", LIB + ".tmp", *SOURCES]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -9,51 +9,60 @@
 //   homogenized_stress    src/network.cpp:341-372
 //   probe_pk2s            src/stiffness.cpp:86-123 (probes are tickets n..7n-1)
 //
-// Bitwise contract with the reference: compiled with --fmad=false,
-// IEEE div/sqrt; x = ref + u rounded per node; each node's force is accumulated from +0.0
-// over its incident fibers in ascending fiber id (CSR, no atomics), reproducing
-// f[a] -= g*d / f[b] += g*d of network.cpp:298-303; the damped update follows
-// kernels_scalar.cpp:15-17 and relax.cpp:155-166 literally.
+// Bitwise contract with the reference: --fmad=false, IEEE div/sqrt
+// (fastmath.cuh replays nvcc's own sequences); x = ref + u rounded per node; each node's
+// force is accumulated from +0.0 over its incident fibers in ascending fiber id (CSR, no
+// atomics), reproducing f[a] -= g*d / f[b] += g*d of network.cpp:298-303; the damped update
+// follows kernels_scalar.cpp:15-17 and relax.cpp:155-166 literally.
 //
 // Per DR iteration the CTA runs two phases separated by __syncthreads():
-//   fiber phase: each thread evaluates FPT register-resident fibers from x in shared
-//                memory and writes g*d (SoA) to shared memory;
-//   node phase:  each thread owns NPT nodes (state u, v, a, f, f_damp in registers),
+//   fiber phase: each thread evaluates FPT register-resident fibers, reading x records
+//                (24-byte AoS) from shared memory and writing g*d records;
+//   node phase:  each thread owns NPT nodes (u and the half-step velocity in registers),
 //                gathers its CSR list, applies the damped central-difference update and
-//                writes the next x.
-// The convergence reduction of iteration k is off the critical path: node threads store
-// one |f|^2 partial per node, and during fiber phase k+1 the last warp reduces them
-// (tree order) and publishes the decision; node phase k+1 acts on it and, if iteration k
-// converged, emits the state of iteration k (held in registers), discarding the
-// speculative step.  A tree sum differs from the reference's 4-lane interleaved sum
-// (kernels_scalar.cpp:20-33) in the last ulps, so whenever |R - eps| <= 1e-10 eps (or a
-// value is non-finite) the CTA recomputes both norms in the reference order before
-// deciding; the reported residual/eps_eff are always the reference-order values.
+//                writes the next x record.
+// Slots are placed by host/schedule.cpp so the random gathers are (mostly) bank-conflict
+// free; empty fiber/node slots hold harmless dummies so the hot loop has no per-slot
+// branches.  CSR lists are padded to even length with a record of +0.0 (f + 0.0 == f for
+// every f the accumulation can produce, since it starts at +0.0 and never reaches -0.0).
+// The convergence reduction is off the critical path: node threads store one |f|^2
+// partial per node; during the next fiber phase the last warp reduces them (tree order)
+// and the following node phase reads the verdict, one iteration late.  The CTA keeps two
+// checkpoints of (u, v_half, t, dt) in global memory; when a verdict says "stop at k"
+// (converged, iteration cap, non-finite, or a near tie |R - eps| <= 1e-10 eps where the
+// tree sum could disagree with the reference's 4-lane sum) it restores the newest
+// checkpoint at or before k, replays to k -- bit-identical, the arithmetic is
+// deterministic -- and decides at k with the reference-order sums.
 #pragma once
 
 #include <cstdint>
 
+#include "fastmath.cuh"
 #include "fibra_cuda.h"
 #include "tensor.cuh"
 
 namespace fibra_b200 {
 
-struct EntryDev {        // one RveLibrary entry in HBM (batched SoA + CSR)
-  int n_nodes, n_fibers, n_free_nodes, pad0;
-  double max_lump, max_ea, box_volume, pad1;
-  const double* ref;     // 3N, packed DOF order (node pn owns dofs 3pn..3pn+2)
-  const double* lump;    // N, packed node order
-  const int* fiber_ab;   // M, a | b << 16 (packed node ids)
-  const double* l0;      // M rest lengths
-  const double* ea;      // M area*modulus
-  const int* csr_off;    // N+1
-  const int* csr_ent;    // 2M, fiber << 1 | (node is endpoint a)
+struct EntryDev {          // one RveLibrary entry in HBM, already in slot order
+  int n_nodes, n_fibers, n_free_nodes, n_fix_nodes;
+  int f0, node_slots, fiber_slots, gd_slots;  // gd_slots includes dummies + zero record
+  int thread_slots, pad0, pad1, pad2;         // NPT*T (two dummy x records follow)
+  double max_lump, max_ea, box_volume, pad3;
+  const int* slot_pn;      // [thread_slots] packed node id per slot, -1 empty
+  const double* slot_ref;  // [3*thread_slots] reference coordinates by slot
+  const double* slot_lump; // [thread_slots] lumping weight by slot (1 when empty)
+  const int* csr_off;      // [thread_slots+1] (even-length lists)
+  const int* csr_ent;      // 24*gslot | (node is the stored tail) << 31
+  const int* fib_ab;       // [fiber_slots] 24*tail_slot | 24*head_slot << 16
+  const int* fib_g;        // [fiber_slots] 24*gslot
+  const int* fib_id;       // [fiber_slots] reference fiber id, -1 dummy
+  const double* fib_l0;    // [fiber_slots]
+  const double* fib_ea;    // [fiber_slots] area*modulus
 };
 
-struct SolveOut {        // one DR solve (base or probe)
-  double sigma_u[6];
-  double asym;
-  double pk2[6];
+struct SolveOut {          // one DR solve (base or probe)
+  double moment[9];        // sum over boundary nodes of r_i x_j (network.cpp:347-358)
+  double box_volume;
   long long iterations;
   double residual, eps_eff, kinetic_fraction, dt;
   int converged;
@@ -73,25 +82,37 @@ struct DrParams {
   int* base_flag;              // per point: 0 pending, 1 converged, 2 failed
   int* ticket;
   unsigned long long* counters;  // [0] iterations [1] fiber-iterations [2] pipe ops [3] solves
+  double* ckpt;                // [grid][2][6][ck_stride]
+  int ck_stride, ck_interval;
   int n_points, n_solves;
-  int nmax, mmax;              // smem layout capacity
+  int x_bytes, g_bytes, part_slots, csr_cap;  // shared-memory layout capacities
   int reuse_warm;
   int law_buckling_off;
   double ea_scale, nonlinearity;
   double damping, tolerance, dt_safety, density_scale;
   long long max_iterations;
+  unsigned long long* phase_prof;  // optional [grid][NW][4] cycle accumulators
 };
 
 enum : int { kDecConv = 1, kDecExact = 2, kDecNonfinite = 4 };
 
+// Per-warp phase cycle counters, compiled only into the diagnostics build
+// (FIBRA_PHASE_PROF=1 python -m paper_2306_09427_b200.build -> lib/libfibra_b200_prof.so).
+#ifdef FIBRA_PHASE_PROF
+#define FB_PROF(...) __VA_ARGS__
+#else
+#define FB_PROF(...)
+#endif
+
 struct __align__(16) DrCtl {
   int solve, point, q, entry;
-  int flag, collapse, pad0, pad1;
-  int dec;
-  double dec_res, dec_eps;
+  int flag, collapse, dec, pad0;
+  long long ck_k[2];
+  double ck_t[2], ck_dt[2];
   double warp_min[32];
   double ex[12];
   double t;
+  double force_floor;
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -112,16 +133,23 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
-__device__ __forceinline__ double flip(double x, int neg) {  // x or -x, exact
-  return __longlong_as_double(__double_as_longlong(x) ^ (static_cast<long long>(neg) << 63));
+// x or -x, exact: xor of the CSR entry's bit 31 into the sign bit (one LOP3)
+__device__ __forceinline__ double signed_by(double x, int entry) {
+  return __hiloint2double(__double2hiint(x) ^ (entry & static_cast<int>(0x80000000u)),
+                          __double2loint(x));
+}
+
+template <class Tp>
+__device__ __forceinline__ Tp* sm_at(unsigned char* base, int byte_off) {
+  return reinterpret_cast<Tp*>(base + byte_off);
 }
 
 // axial force N(lambda) and tangent (network.cpp:16-38); s = ea_scale*ea
 template <int LAW>
 __device__ __forceinline__ double law_force(double s, double stretch, int buckling_off,
                                             double B) {
+  if (LAW == 0) return (buckling_off && stretch < 1.0) ? 0.0 : s * (stretch - 1.0);
   if (buckling_off && stretch < 1.0) return 0.0;
-  if (LAW == 0) return s * (stretch - 1.0);
   return s / B * expm1(B * (stretch - 1.0));
 }
 
@@ -142,40 +170,37 @@ __device__ __forceinline__ double law_energy(double s, double stretch, double rl
   return rl * s / B * (expm1(B * e) / B - e);
 }
 
-template <int T, int FPT, int NPT, int LAW>
-__global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(DrParams P) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// UEA: every fiber of the library has the same area*modulus (true for generated
+// networks), so the axial stiffness s = ea_scale*EA is one scalar instead of FPT registers.
+template <int T, int FPT, int NPT, int LAW, int MINB, bool UEA>
+__global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
   __shared__ DrCtl ctl;
   constexpr int NW = T / 32;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
 
-  // shared layout: [A: 3*nmax x SoA / exact scratch][B: gd SoA 3*mmax | exit scratch]
-  //                [spart: nmax][csr_off: nmax+1][csr_ent: 2*mmax]
-  const int nmax = P.nmax, mmax = P.mmax;
-  const int bsize = (3 * mmax > 6 * nmax + mmax) ? 3 * mmax : 6 * nmax + mmax;
-  double* sx = reinterpret_cast<double*>(smem_raw);
-  double* sy = sx + nmax;
-  double* sz = sy + nmax;
-  double* regB = sz + nmax;
-  double* gx = regB;
-  double* gy = gx + mmax;
-  double* gz = gy + mmax;
-  double* spart = regB + bsize;
-  int* coff = reinterpret_cast<int*>(spart + nmax);
-  int* cent = coff + nmax + 1;
+  // shared layout: [X: x records (24 B/slot) | exact scratch][G: g*d records | exit scratch]
+  //                [SPART: |f|^2 per node slot][CSR off][CSR entries]
+  unsigned char* X = smem;
+  unsigned char* G = smem + P.x_bytes;
+  double* spart = reinterpret_cast<double*>(G + P.g_bytes);
+  int* coff = reinterpret_cast<int*>(spart + P.part_slots);
+  int* cent = coff + P.part_slots + 1;
+  double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
 
   const double B = P.nonlinearity;
   const int bo = P.law_buckling_off;
 
   // register-resident topology of the loaded entry
-  int fab[FPT];
-  double fl0[FPT], fs[FPT], fthr[FPT], fmred[FPT];
+  int fab[FPT], fgo[FPT];
+  double fl0[FPT], fs[FPT], fmred[FPT];
   int nbeg[NPT], nend[NPT];
-  double nref[NPT][3], nm[NPT], ninv[NPT], ncm[NPT];
+  double nref[NPT][3], ninv[NPT], ncm[NPT];
   int cur_entry = -1;
-  int N = 0, M = 0, NFN = 0;
-  double max_lump = 1, force_floor = 0, box_volume = 1;
+  int N = 0, M = 0, NFN = 0, F0 = 0, NFIX = 0, NSLOT = 0;
+  double s_uni = 0;  // UEA: the common ea_scale*EA
+#define SJ(j) (UEA ? s_uni : fs[j])
 
   for (;;) {
     if (tid == 0) {
@@ -223,94 +248,109 @@ __global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(Dr
       N = E.n_nodes;
       M = E.n_fibers;
       NFN = E.n_free_nodes;
-      max_lump = E.max_lump;
-      box_volume = E.box_volume;
-      force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
-      for (int i = tid; i <= N; i += T) coff[i] = E.csr_off[i];
-      for (int i = tid; i < 2 * M; i += T) cent[i] = E.csr_ent[i];
+      NFIX = E.n_fix_nodes;
+      F0 = E.f0;
+      NSLOT = E.node_slots;
+      s_uni = P.ea_scale * E.fib_ea[0];
+      const int n_ent = E.csr_off[E.thread_slots];
+      for (int i = tid; i <= E.thread_slots; i += T) coff[i] = E.csr_off[i];
+      for (int i = tid; i < n_ent; i += T) cent[i] = E.csr_ent[i];
+      for (int i = tid; i < E.thread_slots; i += T) spart[i] = 0.0;
+      // dummy x records for empty fiber slots, and the zero g*d record (last record)
+      if (tid < 6) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid == 3) ? 1.0 : 0.0;
+      if (tid < 3) sm_at<double>(G, 24 * (E.gd_slots - 1))[tid] = 0.0;
 #pragma unroll
       for (int j = 0; j < FPT; ++j) {
         const int f = j * T + tid;
-        if (f < M) {
-          fab[j] = E.fiber_ab[f];
-          fl0[j] = E.l0[f];
-          fs[j] = P.ea_scale * E.ea[f];
-          fthr[j] = 1e-8 * fl0[j];
-        }
+        fab[j] = E.fib_ab[f];
+        fgo[j] = E.fib_g[f];
+        fl0[j] = E.fib_l0[f];
+        if (!UEA) fs[j] = P.ea_scale * E.fib_ea[f];
       }
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
-        const int pn = j * T + tid;
-        if (pn < N) {
-          nbeg[j] = E.csr_off[pn];
-          nend[j] = E.csr_off[pn + 1];
-          nref[j][0] = E.ref[3 * pn];
-          nref[j][1] = E.ref[3 * pn + 1];
-          nref[j][2] = E.ref[3 * pn + 2];
-        }
+        const int sl = j * T + tid;
+        nbeg[j] = E.csr_off[sl];
+        nend[j] = E.csr_off[sl + 1];
+        nref[j][0] = E.slot_ref[3 * sl];
+        nref[j][1] = E.slot_ref[3 * sl + 1];
+        nref[j][2] = E.slot_ref[3 * sl + 2];
       }
     }
-    (void)max_lump;
     // ---- per-solve setup (relax.cpp:95-145) ----
-    const double* F = P.solve_F + 9 * s;
     double Fm[9];
 #pragma unroll
-    for (int i = 0; i < 9; ++i) Fm[i] = F[i];
+    for (int i = 0; i < 9; ++i) Fm[i] = P.solve_F[9 * s + i];
     const long long off = P.offsets[p];
     const bool is_base = q < 0;
     double lmin = INFINITY;
 #pragma unroll
-    for (int j = 0; j < FPT; ++j) {
-      const int f = j * T + tid;
-      if (f < M) {  // reduced_mass_l0 relax.cpp:46-55; CFL at stretch-independent kt
-        const double ma = E.lump[fab[j] & 0xffff] * scale;
-        const double mb = E.lump[fab[j] >> 16] * scale;
+    for (int j = 0; j < FPT; ++j) {  // reduced_mass_l0 relax.cpp:46-55
+      const int ta = (fab[j] & 0xffff) / 24, hb = (fab[j] >> 16) / 24;
+      if (ta < E.thread_slots) {
+        const double ma = E.slot_lump[ta] * scale;
+        const double mb = E.slot_lump[hb] * scale;
         fmred[j] = ma * mb / (ma + mb) * fl0[j];
-        if (LAW == 0) {
-          const double kt = smax(fabs(law_tangent<0>(fs[j], 1.0, 0, B)), fs[j]);
-          lmin = smin(lmin, fmred[j] / kt);
-        }
+      } else {
+        fmred[j] = INFINITY;  // dummy fiber
+      }
+      if (LAW == 0) {  // linear: the CFL bound is stretch independent
+        const double kt = smax(fabs(law_tangent<0>(SJ(j), 1.0, 0, B)), SJ(j));
+        lmin = smin(lmin, fmred[j] / kt);
       }
     }
-    double u[NPT][3], vh[NPT][3];                       // current (speculative) state
-    double pu[NPT][3], pv[NPT][3], pa[NPT][3], pf[NPT][3], pfd[NPT][3];  // state of pass k-1
+    double u[NPT][3], vh[NPT][3];
 #pragma unroll
     for (int j = 0; j < NPT; ++j) {
-      const int pn = j * T + tid;
-      if (pn < N) {
-        nm[j] = E.lump[pn] * scale;
-        ninv[j] = 1.0 / nm[j];
-        ncm[j] = P.damping * nm[j];
-        if (pn < NFN) {
-          if (is_base) {  // WarmStart::reuse from the packed state (stiffness.cpp:157)
+      const int sl = j * T + tid;
+      const int pn = E.slot_pn[sl];
+      const double m = E.slot_lump[sl] * scale;
+      ninv[j] = 1.0 / m;
+      ncm[j] = P.damping * m;
+      if (sl < F0) {
+        if (pn < 0) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) u[j][c] = P.u[off + 3 * pn + c];
-          } else if (P.reuse_warm) {  // probe: copy of the converged base u (:100-101)
+          for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
+        } else if (is_base) {  // WarmStart::reuse from the packed state (stiffness.cpp:157)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) u[j][c] = __ldcg(P.u + off + 3 * pn + c);
-          } else {
+          for (int c = 0; c < 3; ++c) u[j][c] = P.u[off + 3 * pn + c];
+        } else if (P.reuse_warm) {  // probe: copy of the converged base u (:100-101)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
-          }
-        } else {  // affine BC (network.cpp:254-269), Def3::apply tensor.cpp:58-62
-          const double X0 = nref[j][0], X1 = nref[j][1], X2 = nref[j][2];
+          for (int c = 0; c < 3; ++c) u[j][c] = __ldcg(P.u + off + 3 * pn + c);
+        } else {
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const double fx = Fm[3 * c] * X0 + Fm[3 * c + 1] * X1 + Fm[3 * c + 2] * X2;
-            u[j][c] = fx - nref[j][c];
-          }
+          for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
         }
+      } else {  // affine BC (network.cpp:254-269), Def3::apply tensor.cpp:58-62
+        const double X0 = nref[j][0], X1 = nref[j][1], X2 = nref[j][2];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          vh[j][c] = 0.0;
-          pu[j][c] = pv[j][c] = pa[j][c] = pf[j][c] = pfd[j][c] = 0.0;
+          const double fx = Fm[3 * c] * X0 + Fm[3 * c + 1] * X1 + Fm[3 * c + 2] * X2;
+          u[j][c] = fx - nref[j][c];
         }
-        sx[pn] = nref[j][0] + u[j][0];
-        sy[pn] = nref[j][1] + u[j][1];
-        sz[pn] = nref[j][2] + u[j][2];
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) vh[j][c] = 0.0;
+      double* xr = sm_at<double>(X, 24 * sl);
+      xr[0] = nref[j][0] + u[j][0];
+      xr[1] = nref[j][1] + u[j][1];
+      xr[2] = nref[j][2] + u[j][2];
+      if (sl < F0) {  // checkpoint "resume at pass 0": u_0, v = 0
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ckpt[c * P.ck_stride + sl] = u[j][c];
+          ckpt[(3 + c) * P.ck_stride + sl] = 0.0;
+        }
       }
     }
-    if (tid == 0) ctl.t = is_base ? P.t[p] : 0.0;
+    if (tid == 0) {
+      ctl.t = is_base ? P.t[p] : 0.0;
+      ctl.ck_k[0] = 0;
+      ctl.ck_k[1] = -1;
+      ctl.ck_t[0] = ctl.t;
+      ctl.ck_dt[0] = 0.0;
+      ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
+    }
     if (LAW == 0) {
       lmin = warp_min(lmin);
       if (lane == 0) ctl.warp_min[warp] = lmin;
@@ -324,117 +364,222 @@ __global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(Dr
       dt_const = P.dt_safety * sqrt(mn);
     }
 
-    long long k = 0;        // index of the force pass the next fiber phase evaluates
+    int k = 0;              // force pass the next fiber phase evaluates
+    int target = -1;        // pass at which to stop and decide exactly (replay mode)
+    int ck_count = 1;       // passes until the next checkpoint (resume points C, 2C, ...)
     double dt_k = 0;        // dt of iteration k (0 for the initial pass)
-    double dt_last = 0;     // dt of the last committed iteration
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
-    long long n_done = 0;   // iterations of the returned state
     bool rewrite_fixed = false;
 
+    FB_PROF(long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, tq = 0;)
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
-      if (k >= 1 && warp == NW - 1) {  // decision for pass k-1 (tree-order sums)
+      FB_PROF(tq = clock64());
+      if (target < 0 && k >= 1 && warp == NW - 1) {  // verdict for pass k-1, tree order
         double sf = 0, sfix = 0;
-        for (int i = lane; i < NFN; i += 32) sf += spart[i];
-        for (int i = NFN + lane; i < N; i += 32) sfix += spart[i];
+        for (int i = lane; i < F0; i += 32) sf += spart[i];
+        for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
         sf = warp_sum(sf);
         sfix = warp_sum(sfix);
         if (lane == 0) {
           const double res = sqrt(sf);
-          const double eps = P.tolerance * smax(sqrt(sfix), force_floor);
+          const double eps = P.tolerance * smax(sqrt(sfix), ctl.force_floor);
           int d = (res <= eps) ? kDecConv : 0;
           if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
           else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
           ctl.dec = d;
         }
       }
-      double kmin = INFINITY;
-      bool collapsed = false;
+      if (LAW != 0 && warp == NW - 1 && lane == 0) ctl.warp_min[warp] = INFINITY;
+      if (warp != NW - 1) {  // the reducer warp owns no fibers (host/schedule.cpp)
+        double kmin = INFINITY;
+        bool collapsed = false, fast = true;
+        double dx[FPT], dy[FPT], dz[FPT], g[FPT];
 #pragma unroll
-      for (int j = 0; j < FPT; ++j) {
-        const int f = j * T + tid;
-        if (f < M) {
-          const int ia = fab[j] & 0xffff, ib = fab[j] >> 16;
-          const double dx = sx[ib] - sx[ia];
-          const double dy = sy[ib] - sy[ia];
-          const double dz = sz[ib] - sz[ia];
-          const double len = sqrt(dx * dx + dy * dy + dz * dz);
-          collapsed |= (len <= fthr[j]);
-          const double stretch = len / fl0[j];
-          const double g = law_force<LAW>(fs[j], stretch, bo, B) / len;
-          gx[f] = g * dx;
-          gy[f] = g * dy;
-          gz[f] = g * dz;
-          if (LAW != 0) {
-            const double kt = smax(fabs(law_tangent<LAW>(fs[j], stretch, bo, B)), fs[j]);
+        for (int j = 0; j < FPT; ++j) {
+          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
+          const double* xb_ = sm_at<double>(X, fab[j] >> 16);
+          dx[j] = xb_[0] - xa_[0];
+          dy[j] = xb_[1] - xa_[1];
+          dz[j] = xb_[2] - xa_[2];
+          bool o1, o2, o3 = true;
+          const double len = sqrt_fast(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j], o1);
+          collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
+          const double stretch = div_fast(len, fl0[j], o2);
+          if (LAW == 0) {
+            g[j] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+          } else {
+            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
             kmin = smin(kmin, fmred[j] / kt);
           }
+          fast = fast && o1 && o2 && o3;
+        }
+        if (!__all_sync(0xffffffffu, fast)) {  // rare: special operands -> built-in ops
+#pragma unroll
+          for (int j = 0; j < FPT; ++j) {
+            const double len = sqrt(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j]);
+            const double stretch = len / fl0[j];
+            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < FPT; ++j) {
+          double* gr = sm_at<double>(G, fgo[j]);
+          gr[0] = g[j] * dx[j];
+          gr[1] = g[j] * dy[j];
+          gr[2] = g[j] * dz[j];
+        }
+        if (collapsed) ctl.collapse = 1;
+        if (LAW != 0) {
+          kmin = warp_min(kmin);
+          if (lane == 0) ctl.warp_min[warp] = kmin;
         }
       }
-      if (collapsed) ctl.collapse = 1;
-      if (LAW != 0) {
-        kmin = warp_min(kmin);
-        if (lane == 0) ctl.warp_min[warp] = kmin;
-      }
+      FB_PROF({ const long long t1 = clock64(); pc0 += t1 - tq; tq = t1; })
       __syncthreads();
+      FB_PROF({ const long long t1 = clock64(); pc1 += t1 - tq; tq = t1; })
 
       // ================= node phase (pass k) =================
-      if (k >= 1) {
-        int d = ctl.dec;
-        if (d & kDecExact) {  // reference-order norms of f_{k-1}
+      if (target < 0 && k >= 1) {
+        const int d = ctl.dec;
+        if ((d & (kDecConv | kDecExact)) || k - 1 == P.max_iterations) {
+          // stop at k-1: replay from the newest checkpoint that resumes at or before it
+          target = k - 1;
+          const int b = (ctl.ck_k[0] <= target && (ctl.ck_k[1] > target || ctl.ck_k[0] > ctl.ck_k[1])) ? 0 : 1;
+          k = static_cast<int>(ctl.ck_k[b]);
+          dt_k = ctl.ck_dt[b];
+          const double* ck = ckpt + b * 6 * P.ck_stride;
 #pragma unroll
           for (int j = 0; j < NPT; ++j) {
-            const int pn = j * T + tid;
-            if (pn < N)
+            const int sl = j * T + tid;
+            if (sl < F0) {
 #pragma unroll
-              for (int c = 0; c < 3; ++c) sx[3 * pn + c] = pf[j][c];
+              for (int c = 0; c < 3; ++c) {
+                u[j][c] = __ldcg(ck + c * P.ck_stride + sl);
+                vh[j][c] = __ldcg(ck + (3 + c) * P.ck_stride + sl);
+              }
+            }
+            double* xr = sm_at<double>(X, 24 * sl);
+            xr[0] = nref[j][0] + u[j][0];
+            xr[1] = nref[j][1] + u[j][1];
+            xr[2] = nref[j][2] + u[j][2];
           }
-          __syncthreads();
-          if (tid < 8) {
-            const int base = tid < 4 ? 0 : 3 * NFN;
-            const int len = tid < 4 ? 3 * NFN : 3 * (N - NFN);
-            double acc = 0;
-            for (int i = tid & 3; i < len; i += 4) acc += sx[base + i] * sx[base + i];
-            ctl.ex[tid] = acc;
+          if (tid == 0) {
+            ctl.t = ctl.ck_t[b];
+            ctl.collapse = 0;
           }
+          rewrite_fixed = false;
           __syncthreads();
-          const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
-          const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
-          const double eps = P.tolerance * smax(react, force_floor);
-          d = (res <= eps) ? kDecConv : 0;
-          if (!isfinite(res)) d |= kDecNonfinite;
-          rewrite_fixed = true;
-          __syncthreads();  // everyone has read ctl.ex before it can be reused
+          continue;
         }
-        if (d & kDecNonfinite) {
-          status = FIBRA_E_DIVERGED;
-          n_done = k - 1;
-          break;
-        }
-        if (d & kDecConv) {
-          conv = 1;
-          n_done = k - 1;
-          break;
-        }
-        if (k - 1 == P.max_iterations) {
-          n_done = k - 1;
-          break;
-        }
-        // commit iteration k
+      }
+      if (k >= 1) {  // commit iteration k (relax.cpp:150-153)
         if (!isfinite(dt_k) || !(dt_k > 0)) {
           status = FIBRA_E_BAD_DT;
-          n_done = k - 1;
           break;
         }
         if (tid == 0) ctl.t += dt_k;
-        dt_last = dt_k;
       }
       if (ctl.collapse) {
         status = FIBRA_E_COLLAPSE;
-        n_done = k > 0 ? k - 1 : 0;
         break;
       }
+      const double h_k = 0.5 * dt_k;
+      double fk[NPT][3];
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int sl = j * T + tid;
+        double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
+        for (int i = nbeg[j]; i < nend[j]; i += 2) {  // even-length lists
+          const int e0 = cent[i], e1 = cent[i + 1];
+          const double* g0 = sm_at<double>(G, e0 & 0x7fffffff);
+          const double* g1 = sm_at<double>(G, e1 & 0x7fffffff);
+          const double a0 = g0[0], a1 = g0[1], a2 = g0[2];
+          const double b0 = g1[0], b1 = g1[1], b2 = g1[2];
+          f0 = f0 + signed_by(a0, e0);
+          f1 = f1 + signed_by(a1, e0);
+          f2 = f2 + signed_by(a2, e0);
+          f0 = f0 + signed_by(b0, e1);
+          f1 = f1 + signed_by(b1, e1);
+          f2 = f2 + signed_by(b2, e1);
+        }
+        fk[j][0] = f0;
+        fk[j][1] = f1;
+        fk[j][2] = f2;
+        spart[sl] = f0 * f0 + f1 * f1 + f2 * f2;
+      }
+      if (k == target) {
+        // ---- exact verdict at the target pass (reference-order norms) ----
+        double* SF = reinterpret_cast<double*>(X);
+        __syncthreads();  // every x read of this pass is done; SF reuses X
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+          const int pn = E.slot_pn[j * T + tid];
+          if (pn >= 0)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) SF[3 * pn + c] = fk[j][c];
+        }
+        __syncthreads();
+        if (tid < 8) {
+          const int base = tid < 4 ? 0 : 3 * NFN;
+          const int len = tid < 4 ? 3 * NFN : 3 * NFIX;
+          double acc = 0;
+          for (int i = tid & 3; i < len; i += 4) acc += SF[base + i] * SF[base + i];
+          ctl.ex[tid] = acc;
+        }
+        __syncthreads();
+        const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
+        const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
+        const double eps = P.tolerance * smax(react, ctl.force_floor);
+        __syncthreads();  // ctl.ex consumed before anyone reuses it
+        const bool nonfinite = k >= 1 && !isfinite(res);
+        conv = res <= eps;
+        if (nonfinite || conv || k == P.max_iterations) {
+          if (nonfinite) {
+            status = FIBRA_E_DIVERGED;
+            break;
+          }
+          // Final state of iteration k, written straight to the exit scratch (SF already
+          // holds f) and, for base solves, to the PackedStates (batch.cpp:169-176).  Doing
+          // it here keeps no exit arrays alive across the DR loop.
+          double* SX = reinterpret_cast<double*>(G);
+          double* SW = SX + 3 * N;
+#pragma unroll
+          for (int j = 0; j < NPT; ++j) {
+            const int sl = j * T + tid;
+            const int pn = E.slot_pn[sl];
+            if (pn < 0) continue;
+            const double m = E.slot_lump[sl] * scale;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double fd = 0.0, acc = 0.0, vv = 0.0;  // fixed dofs / 0-iteration exit
+              if (sl < F0 && k >= 1) {
+                fd = ncm[j] * vh[j][c];                // kernels_scalar.cpp:15-17
+                acc = -(fk[j][c] + fd) * ninv[j];
+                vv = vh[j][c] + h_k * acc;             // relax.cpp:166
+              }
+              SX[3 * pn + c] = nref[j][c] + u[j][c];
+              if (sl < F0) SW[3 * pn + c] = m * (vv * vv);
+              if (is_base) {
+                const long long d = off + 3 * pn + c;
+                P.u[d] = u[j][c];
+                P.v[d] = vv;
+                P.a[d] = acc;
+                P.f_int[d] = fk[j][c];
+                P.f_damp[d] = fd;
+                P.mass[d] = m;
+                P.inv_mass[d] = ninv[j];
+              }
+            }
+          }
+          break;
+        }
+        target = -1;  // near tie that did not stop: continue normally
+        rewrite_fixed = true;
+      }
+      // ---- damped update + speculative half step / drift of iteration k+1 ----
       double dt_next;
       if (LAW == 0) {
         dt_next = dt_const;
@@ -443,98 +588,86 @@ __global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(Dr
         for (int w = 0; w < NW; ++w) mn = smin(mn, ctl.warp_min[w]);
         dt_next = P.dt_safety * sqrt(mn);
       }
-      const double h_k = 0.5 * dt_k;
       const double h_n = 0.5 * dt_next;
+      const bool save = target < 0 && --ck_count == 0;
+      const int sb = (ctl.ck_k[0] < ctl.ck_k[1]) ? 0 : 1;  // overwrite the older buffer
+      if (save) ck_count = P.ck_interval;
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
-        const int pn = j * T + tid;
-        if (pn < N) {
-          double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
-          for (int i = nbeg[j]; i < nend[j]; ++i) {
-            const int en = cent[i];
-            const int fi = en >> 1, neg = en & 1;
-            f0 = f0 + flip(gx[fi], neg);
-            f1 = f1 + flip(gy[fi], neg);
-            f2 = f2 + flip(gz[fi], neg);
+        const int sl = j * T + tid;
+        double* xr = sm_at<double>(X, 24 * sl);
+        if (sl < F0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double fd = ncm[j] * vh[j][c];              // kernels_scalar.cpp:15-17
+            const double acc = -(fk[j][c] + fd) * ninv[j];
+            const double vv = (k >= 1) ? vh[j][c] + h_k * acc : vh[j][c];  // relax.cpp:166
+            vh[j][c] = vv + h_n * acc;                          // relax.cpp:155
+            u[j][c] = u[j][c] + dt_next * vh[j][c];             // relax.cpp:156
           }
-          spart[pn] = f0 * f0 + f1 * f1 + f2 * f2;
-          const double fv[3] = {f0, f1, f2};
-          if (pn < NFN) {
+          xr[0] = nref[j][0] + u[j][0];
+          xr[1] = nref[j][1] + u[j][1];
+          xr[2] = nref[j][2] + u[j][2];
+          if (save) {
+            double* ck = ckpt + sb * 6 * P.ck_stride;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-              const double fd = ncm[j] * vh[j][c];                // kernels_scalar.cpp:15-17
-              const double acc = -(fv[c] + fd) * ninv[j];
-              const double vv = (k >= 1) ? vh[j][c] + h_k * acc : vh[j][c];  // relax.cpp:166
-              pu[j][c] = u[j][c];
-              pv[j][c] = vv;
-              pa[j][c] = acc;
-              pf[j][c] = fv[c];
-              pfd[j][c] = fd;
-              vh[j][c] = vv + h_n * acc;                          // relax.cpp:155
-              u[j][c] = u[j][c] + dt_next * vh[j][c];             // relax.cpp:156
-            }
-            sx[pn] = nref[j][0] + u[j][0];
-            sy[pn] = nref[j][1] + u[j][1];
-            sz[pn] = nref[j][2] + u[j][2];
-          } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-              pu[j][c] = u[j][c];
-              pf[j][c] = fv[c];
-            }
-            if (rewrite_fixed) {
-              sx[pn] = nref[j][0] + u[j][0];
-              sy[pn] = nref[j][1] + u[j][1];
-              sz[pn] = nref[j][2] + u[j][2];
+              ck[c * P.ck_stride + sl] = u[j][c];
+              ck[(3 + c) * P.ck_stride + sl] = vh[j][c];
             }
           }
+        } else if (rewrite_fixed) {
+          xr[0] = nref[j][0] + u[j][0];
+          xr[1] = nref[j][1] + u[j][1];
+          xr[2] = nref[j][2] + u[j][2];
         }
       }
       rewrite_fixed = false;
+      FB_PROF({ const long long t1 = clock64(); pc2 += t1 - tq; tq = t1; })
+      __syncthreads();
+      FB_PROF({ const long long t1 = clock64(); pc3 += t1 - tq; tq = t1; })
+      if (save && tid == 0) {  // after the barrier: every thread has chosen `sb`
+        ctl.ck_k[sb] = k + 1;
+        ctl.ck_t[sb] = ctl.t;
+        ctl.ck_dt[sb] = dt_next;
+      }
       dt_k = dt_next;
       ++k;
-      __syncthreads();
     }
 
     // ================= exit (relax.cpp:181-190, network.cpp:341-372) =================
-    // Uniform across the CTA: every thread took the same break.
-    __syncthreads();
-    double* SF = sx;                 // f of the returned state, flat packed order (3N)
-    double* SX = regB;               // x = ref + u (3N)
-    double* SW = regB + 3 * nmax;    // m v^2 over free dofs (3*NFN)
-    double* SE = regB + 6 * nmax;    // per-fiber strain energy (M)
+    // Uniform across the CTA.  On a normal stop k == target and the final state of
+    // iteration k is already in the exit scratch / PackedStates; solver errors skip all
+    // of it (the reference leaves a partially updated state behind on a throw).
+    const int n_done = (status == FIBRA_OK) ? k : (k > 0 ? k - 1 : 0);
+    FB_PROF(if (P.phase_prof && lane == 0) {
+      unsigned long long* pp = P.phase_prof + (static_cast<size_t>(blockIdx.x) * NW + warp) * 4;
+      pp[0] += pc0; pp[1] += pc1; pp[2] += pc2; pp[3] += pc3;
+    })
     const bool zero_iter = (n_done == 0);
-#pragma unroll
-    for (int j = 0; j < NPT; ++j) {
-      const int pn = j * T + tid;
-      if (pn < N) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          SF[3 * pn + c] = pf[j][c];
-          SX[3 * pn + c] = nref[j][c] + pu[j][c];
-          if (pn < NFN) SW[3 * pn + c] = nm[j] * (pv[j][c] * pv[j][c]);
-        }
-      }
-    }
     __syncthreads();
-    if (!zero_iter && status == FIBRA_OK) {
+    double* SF = reinterpret_cast<double*>(X);                 // f, flat packed order (3N)
+    double* SX = reinterpret_cast<double*>(G);                 // x = ref + u (3N)
+    double* SW = SX + 3 * N;                                   // m v^2, free dofs (3*NFN)
+    double* SE = SW + 3 * NFN;                                 // strain energy per fiber (M)
+    if (status == FIBRA_OK && !zero_iter) {
 #pragma unroll
       for (int j = 0; j < FPT; ++j) {
-        const int f = j * T + tid;
-        if (f < M) {  // strain_energy relax.cpp:57-72
-          const int ia = fab[j] & 0xffff, ib = fab[j] >> 16;
-          const double dx = SX[3 * ib] - SX[3 * ia];
-          const double dy = SX[3 * ib + 1] - SX[3 * ia + 1];
-          const double dz = SX[3 * ib + 2] - SX[3 * ia + 2];
+        const int f = E.fib_id[j * T + tid];
+        if (f >= 0) {  // strain_energy relax.cpp:57-72 (reference fiber id order)
+          const int ta = E.slot_pn[(fab[j] & 0xffff) / 24], hb = E.slot_pn[(fab[j] >> 16) / 24];
+          const double dx = SX[3 * hb] - SX[3 * ta];
+          const double dy = SX[3 * hb + 1] - SX[3 * ta + 1];
+          const double dz = SX[3 * hb + 2] - SX[3 * ta + 2];
           const double len = sqrt(dx * dx + dy * dy + dz * dz);
-          SE[f] = law_energy<LAW>(fs[j], len / fl0[j], fl0[j], bo, B);
+          SE[f] = law_energy<LAW>(SJ(j), len / fl0[j], fl0[j], bo, B);
         }
       }
     }
-    if (tid < 12) {  // reference-order reductions (4 interleaved partials)
+    if (status == FIBRA_OK && tid < 12) {  // reference-order reductions (4 partials)
       const int r = tid & 3, which = tid >> 2;
       const double* src = which == 0 ? SF : (which == 1 ? SF + 3 * NFN : SW);
-      const int len = which == 1 ? 3 * (N - NFN) : 3 * NFN;
+      const int len = which == 1 ? 3 * NFIX : 3 * NFN;
       double acc = 0;
       if (which < 2)
         for (int i = r; i < len; i += 4) acc += src[i] * src[i];
@@ -545,74 +678,55 @@ __global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(Dr
     __syncthreads();
     if (tid == 0) {
       SolveOut o = {};
-      const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
-      const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
-      o.residual = res;
-      o.eps_eff = P.tolerance * smax(react, force_floor);
       o.iterations = n_done;
-      o.dt = dt_last;
-      o.converged = conv;
       o.status = status;
-      if (status == FIBRA_OK && !zero_iter) {
-        const double ke = 0.5 * ((ctl.ex[8] + ctl.ex[9]) + (ctl.ex[10] + ctl.ex[11]));
-        double se = 0;
-        for (int f = 0; f < M; ++f) se += SE[f];
-        o.kinetic_fraction = (ke + se) > 0 ? ke / (ke + se) : 0.0;
-      }
-      if (status == FIBRA_OK && conv) {  // homogenized stress + pull-back
-        const double vol = det3(Fm) * box_volume;
-        double sm[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        for (int pn = NFN; pn < N; ++pn)
-          for (int i = 0; i < 3; ++i)
-            for (int jj = 0; jj < 3; ++jj) sm[i][jj] += SF[3 * pn + i] * SX[3 * pn + jj];
-        double raw[9];
-        for (int i = 0; i < 3; ++i)
-          for (int jj = 0; jj < 3; ++jj) raw[3 * i + jj] = sm[i][jj] / vol;
-        double asym = 0, mag = 0;
-        for (int i = 0; i < 3; ++i)
-          for (int jj = 0; jj < 3; ++jj) {
-            asym += (raw[3 * i + jj] - raw[3 * jj + i]) * (raw[3 * i + jj] - raw[3 * jj + i]);
-            mag += raw[3 * i + jj] * raw[3 * i + jj];
+      if (status == FIBRA_OK) {
+        const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
+        const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
+        o.residual = res;
+        o.eps_eff = P.tolerance * smax(react, ctl.force_floor);
+        o.dt = zero_iter ? 0.0 : dt_k;
+        o.converged = conv;
+        if (!zero_iter) {
+          const double ke = 0.5 * ((ctl.ex[8] + ctl.ex[9]) + (ctl.ex[10] + ctl.ex[11]));
+          double se = 0;
+          for (int f = 0; f < M; ++f) se += SE[f];
+          o.kinetic_fraction = (ke + se) > 0 ? ke / (ke + se) : 0.0;
+        }
+        if (conv) {  // homogenized_stress moment sums, boundary nodes ascending
+          // (network.cpp:347-358); the division by J V, symmetrization and pull-back run in
+          // post_kernel so their register footprint stays out of this kernel
+          double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+          for (int pn = NFN; pn < N; ++pn) {
+            const double r0 = SF[3 * pn], r1 = SF[3 * pn + 1], r2 = SF[3 * pn + 2];
+            const double x0 = SX[3 * pn], x1 = SX[3 * pn + 1], x2 = SX[3 * pn + 2];
+            sm[0] += r0 * x0; sm[1] += r0 * x1; sm[2] += r0 * x2;
+            sm[3] += r1 * x0; sm[4] += r1 * x1; sm[5] += r1 * x2;
+            sm[6] += r2 * x0; sm[7] += r2 * x1; sm[8] += r2 * x2;
           }
-        sym_from_full(raw, o.sigma_u);
-        o.asym = mag > 0 ? sqrt(asym / mag) : 0.0;
-        if (!pull_back_stress(o.sigma_u, Fm, o.pk2)) o.status = FIBRA_E_KINEMATICS;
-      } else if (status == FIBRA_OK) {
-        o.status = q < 0 ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;
+          for (int i = 0; i < 9; ++i) o.moment[i] = sm[i];
+          o.box_volume = E.box_volume;
+        } else {
+          o.status = q < 0 ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;
+        }
       }
       P.out[s] = o;
       if (is_base) {
         P.t[p] = ctl.t;
-        if (status == FIBRA_OK) {  // an exception leaves iters/converged untouched
+        if (status == FIBRA_OK) {  // a throw leaves iters untouched (relax.cpp:187)
           P.iters[p] += n_done;
           P.converged[p] = static_cast<unsigned char>(conv);
+        } else {
+          P.converged[p] = 0;      // apply_affine_bc already cleared it (network.cpp:268)
         }
       }
       atomicAdd(P.counters + 0, static_cast<unsigned long long>(n_done));
       atomicAdd(P.counters + 1, static_cast<unsigned long long>(n_done) * M);
       atomicAdd(P.counters + 2, static_cast<unsigned long long>(n_done) *
-                                    (51ull * M + 12ull * 3 * NFN + 2ull * 3 * (N - NFN)));
+                                    (51ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
       atomicAdd(P.counters + 3, 1ull);
     }
-    if (is_base) {  // PackedStates writeback of the base solve (batch.cpp:169-176)
-#pragma unroll
-      for (int j = 0; j < NPT; ++j) {
-        const int pn = j * T + tid;
-        if (pn < N) {
-          const bool fr = pn < NFN;
-#pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const long long d = off + 3 * pn + c;
-            P.u[d] = pu[j][c];
-            P.v[d] = fr ? pv[j][c] : 0.0;
-            P.a[d] = (fr && !zero_iter) ? pa[j][c] : 0.0;
-            P.f_int[d] = pf[j][c];
-            P.f_damp[d] = (fr && !zero_iter) ? pfd[j][c] : 0.0;
-            P.mass[d] = nm[j];
-            P.inv_mass[d] = ninv[j];
-          }
-        }
-      }
+    if (is_base) {
       __syncthreads();
       if (tid == 0) {
         const int ok = (P.out[s].status == FIBRA_OK) ? 1 : 2;
@@ -622,6 +736,7 @@ __global__ void __launch_bounds__(T, (T <= 256 ? 2 : 1)) dr_persistent_kernel(Dr
     }
     __syncthreads();
   }
+#undef SJ
 }
 
 }  // namespace fibra_b200

@@ -13,11 +13,14 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "dr_kernel.cuh"
+#include "host/schedule.hpp"
 #include "fibra_cuda.h"
 #include "tensor.cuh"
 
@@ -66,9 +69,27 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
   prep[p] = o;
 }
 
+// homogenized_stress (network.cpp:341-372) from the boundary moment sums of a converged
+// solve, then pull_back_stress (tensor.cpp:309-315) at the solve's stretch Fs
+__device__ bool finish_stress(const SolveOut& o, const double* Fs, double* sigma,
+                              double* asym_out, double* pk2) {
+  const double vol = det3(Fs) * o.box_volume;
+  double raw[9];
+  for (int i = 0; i < 9; ++i) raw[i] = o.moment[i] / vol;
+  double asym = 0, mag = 0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      asym += (raw[3 * i + j] - raw[3 * j + i]) * (raw[3 * i + j] - raw[3 * j + i]);
+      mag += raw[3 * i + j] * raw[3 * i + j];
+    }
+  sym_from_full(raw, sigma);
+  *asym_out = mag > 0 ? sqrt(asym / mag) : 0.0;
+  return pull_back_stress(sigma, Fs, pk2);
+}
+
 __global__ void post_kernel(int n, const double* __restrict__ F, int want_tangent,
                             const PrepOut* __restrict__ prep, const SolveOut* __restrict__ out,
-                            fibra_point_result* res) {
+                            const double* __restrict__ solve_F, fibra_point_result* res) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   fibra_point_result r;
@@ -79,20 +100,23 @@ __global__ void post_kernel(int n, const double* __restrict__ F, int want_tangen
   int status = pr.status ? pr.status : b.status;
   int failed_probe = -1;
   int64_t its = b.iterations;
-  double probe_pk2[36];
+  double sigma_u[6], asym = 0, pk2[6], probe_pk2[36];
+  if (!status && !finish_stress(b, solve_F + 9 * p, sigma_u, &asym, pk2))
+    status = FIBRA_E_KINEMATICS;
   if (!status && want_tangent) {
     for (int q = 0; q < 6 && !status; ++q) {
-      const SolveOut& o = out[n + 6 * p + q];
-      if (o.status) {
+      const int s = n + 6 * p + q;
+      const SolveOut& o = out[s];
+      double sq[6], aq;
+      if (o.status || !finish_stress(o, solve_F + 9 * s, sq, &aq, probe_pk2 + 6 * q)) {
         status = FIBRA_E_PROBE_FAILED;
         failed_probe = q;
       } else {
         its += o.iterations;
-        for (int i = 0; i < 6; ++i) probe_pk2[6 * q + i] = o.pk2[i];
       }
     }
     if (!status) {
-      if (!material_stiffness_from_probes(pr.U, b.pk2, probe_pk2, pr.h, r.material_a))
+      if (!material_stiffness_from_probes(pr.U, pk2, probe_pk2, pr.h, r.material_a))
         status = FIBRA_E_SINGULAR;
       else {
         double f[9];
@@ -109,9 +133,9 @@ __global__ void post_kernel(int n, const double* __restrict__ F, int want_tangen
     res[p] = z;
     return;
   }
-  rotate_stress(pr.R, b.sigma_u, r.sigma);
-  for (int i = 0; i < 6; ++i) r.pk2[i] = b.pk2[i];
-  r.stress_asymmetry = b.asym;
+  rotate_stress(pr.R, sigma_u, r.sigma);
+  for (int i = 0; i < 6; ++i) r.pk2[i] = pk2[i];
+  r.stress_asymmetry = asym;
   r.base_report.iterations = b.iterations;
   r.base_report.residual = b.residual;
   r.base_report.eps_eff = b.eps_eff;
@@ -145,21 +169,30 @@ __global__ void fp64_peak_kernel(double* sink, int iters, double c) {
 using KernelFn = void (*)(DrParams);
 
 struct Variant {
-  int T, FPT, NPT, LAW;
-  KernelFn fn;
+  int T, FPT, NPT, MINB;
+  KernelFn fn[2][2];  // [law: linear, exponential][uniform EA]
 };
 
-#define FB_V(T, F, N, L) {T, F, N, L, &dr_persistent_kernel<T, F, N, L>}
+// Ordered by preference: the first variant whose capacity covers every library entry wins.
+// MINB = 2 keeps two CTAs (two RVEs) per SM so one CTA's barrier wait is covered by the
+// other's work.
+#define FB_V(T, F, N, B)                                                                 \
+  {T, F, N, B,                                                                             \
+   {{&dr_persistent_kernel<T, F, N, 0, B, false>, &dr_persistent_kernel<T, F, N, 0, B, true>}, \
+    {&dr_persistent_kernel<T, F, N, 1, B, false>, &dr_persistent_kernel<T, F, N, 1, B, true>}}}
 static const Variant kVariants[] = {
-    FB_V(512, 1, 1, 0), FB_V(512, 2, 1, 0), FB_V(512, 4, 1, 0), FB_V(512, 4, 2, 0),
-    FB_V(512, 8, 2, 0), FB_V(512, 8, 4, 0), FB_V(256, 4, 2, 0), FB_V(256, 2, 1, 0),
-    FB_V(512, 1, 1, 1), FB_V(512, 2, 1, 1), FB_V(512, 4, 1, 1), FB_V(512, 4, 2, 1),
-    FB_V(512, 8, 2, 1), FB_V(512, 8, 4, 1), FB_V(256, 4, 2, 1), FB_V(256, 2, 1, 1),
+    FB_V(256, 3, 1, 2),  // <= 256 node slots, <= 768 fibers
+    FB_V(384, 3, 1, 2),  // <= 384 node slots, <= 1152 fibers (config 1/2 networks)
+    FB_V(512, 2, 1, 2),  // <= 512 node slots, <= 1024 fibers
+    FB_V(512, 4, 1, 1),  // <= 512 node slots, <= 2048 fibers
+    FB_V(512, 6, 2, 1),  // <= 1024 node slots, <= 3072 fibers
+    FB_V(768, 7, 2, 1),  // <= 1536 node slots, <= 5376 fibers (ragged config-3 tail)
 };
 #undef FB_V
 
 struct DeviceEntry {
   EntryDev dev;
+  Schedule sched;
   std::vector<void*> allocs;
   bool config_ok = true;
   std::string config_err;
@@ -177,7 +210,9 @@ struct fibra_ctx {
   std::string err;
   std::vector<DeviceEntry> entries;
   EntryDev* d_entries = nullptr;
-  int nmax = 0, mmax = 0;
+  const Variant* variant = nullptr;
+  bool uniform_ea = false;  // every entry has a single area*modulus over its fibers
+  int x_bytes = 0, g_bytes = 0, part_slots = 0, csr_cap = 0, ck_stride = 0;
   // points
   int n_points = 0;
   std::vector<int32_t> entry_of_point;
@@ -198,11 +233,15 @@ struct fibra_ctx {
   fibra_point_result* d_res = nullptr;
   double* h_F = nullptr;                 // pinned staging
   fibra_point_result* h_res = nullptr;   // pinned staging
+  double* d_ckpt = nullptr;
+  size_t ckpt_cap = 0;
   int* d_ticket = nullptr;
   unsigned long long* d_counters = nullptr;
   cudaEvent_t ev[4] = {};
   int last_solves = 0;
   int last_launches = 0;
+  unsigned long long* phase_prof = nullptr;
+  size_t phase_prof_n = 0;
 };
 
 namespace {
@@ -212,10 +251,10 @@ int set_err(fibra_ctx* c, int code, const std::string& what) {
   return code;
 }
 
-#define FB_CUDA(ctx, call)                                                           \
-  do {                                                                               \
-    cudaError_t e_ = (call);                                                         \
-    if (e_ != cudaSuccess)                                                           \
+#define FB_CUDA(ctx, call)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
       return set_err(ctx, FIBRA_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
@@ -265,7 +304,7 @@ void free_library(fibra_ctx* c) {
   c->entries.clear();
   cudaFree(c->d_entries);
   c->d_entries = nullptr;
-  c->nmax = c->mmax = 0;
+  c->variant = nullptr;
 }
 
 int ensure_scratch(fibra_ctx* c, int n) {
@@ -286,28 +325,18 @@ int ensure_scratch(fibra_ctx* c, int n) {
   return FIBRA_OK;
 }
 
-size_t smem_bytes(int nmax, int mmax) {
-  const size_t bsize = std::max<size_t>(3 * static_cast<size_t>(mmax), 6 * static_cast<size_t>(nmax) + mmax);
-  return sizeof(double) * (3 * static_cast<size_t>(nmax) + bsize + nmax) +
-         sizeof(int) * (nmax + 1 + 2 * static_cast<size_t>(mmax));
-}
+size_t align16(size_t b) { return (b + 15) & ~static_cast<size_t>(15); }
 
-const Variant* pick_variant(int nmax, int mmax, int law) {
-  // smallest register footprint that covers the largest entry; prefer T=512
-  const Variant* best = nullptr;
-  for (const Variant& v : kVariants) {
-    if (v.LAW != law || v.T != 512) continue;
-    if (v.FPT * v.T < mmax || v.NPT * v.T < nmax) continue;
-    if (!best || v.FPT + 3 * v.NPT < best->FPT + 3 * best->NPT) best = &v;
-  }
-  return best;
+size_t smem_bytes(const fibra_ctx* c) {
+  return static_cast<size_t>(c->x_bytes) + c->g_bytes + 8ull * c->part_slots +
+         4ull * (c->part_slots + 1) + 4ull * c->csr_cap;
 }
 
 int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
                  const fibra_relax_cfg* rc, const fibra_stiff_cfg* sc, int want_tangent,
                  fibra_point_result* dres) {
   const int n = c->n_points;
-  if (!c->d_entries || n == 0 && c->entry_of_point.empty())
+  if (!c->d_entries || !c->variant)
     return set_err(c, FIBRA_E_ARG, "upload_library and bind_points must precede solve");
   // configuration validation (ConfigError propagates: relax.cpp:12-19, network.cpp:55-59,
   // stiffness.cpp:10-13)
@@ -329,16 +358,24 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   if (n == 0) return FIBRA_OK;
   int r;
   if ((r = ensure_scratch(c, n))) return r;
-  const Variant* v = pick_variant(c->nmax, c->mmax, law->kind);
-  if (!v) return set_err(c, FIBRA_E_ARG, "RVE too large for the resident kernel variants");
-  const size_t smem = smem_bytes(c->nmax, c->mmax);
-  FB_CUDA(c, cudaFuncSetAttribute(v->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const Variant* v = c->variant;
+  KernelFn fn = v->fn[law->kind][c->uniform_ea ? 1 : 0];
+  const size_t smem = smem_bytes(c);
+  FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
   int per_sm = 0;
-  FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v->fn, v->T, smem));
+  FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v->T, smem));
   if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "DR kernel does not fit on an SM");
   const int n_solves = want_tangent ? 7 * n : n;
   const int grid = std::min(n_solves, per_sm * c->n_sm);
+  const size_t ck = static_cast<size_t>(grid) * 12 * c->ck_stride;
+  if (ck > c->ckpt_cap) {
+    cudaFree(c->d_ckpt);
+    c->d_ckpt = nullptr;
+    c->ckpt_cap = 0;
+    FB_CUDA(c, cudaMalloc(&c->d_ckpt, ck * sizeof(double)));
+    c->ckpt_cap = ck;
+  }
 
   DrParams P;
   P.entries = c->d_entries;
@@ -360,10 +397,15 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.base_flag = c->d_flag;
   P.ticket = c->d_ticket;
   P.counters = c->d_counters;
+  P.ckpt = c->d_ckpt;
+  P.ck_stride = c->ck_stride;
+  P.ck_interval = 8;
   P.n_points = n;
   P.n_solves = n_solves;
-  P.nmax = c->nmax;
-  P.mmax = c->mmax;
+  P.x_bytes = c->x_bytes;
+  P.g_bytes = c->g_bytes;
+  P.part_slots = c->part_slots;
+  P.csr_cap = c->csr_cap;
   P.reuse_warm = sc ? sc->reuse_warm : 1;
   P.law_buckling_off = law->buckling_off;
   P.ea_scale = law->ea_scale;
@@ -373,6 +415,17 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.dt_safety = rc->dt_safety;
   P.density_scale = rc->density_scale;
   P.max_iterations = rc->max_iterations;
+  P.phase_prof = nullptr;
+  if (getenv("FIBRA_PHASE_PROF")) {  // diagnostics: per-warp phase cycle accumulators
+    static unsigned long long* buf = nullptr;
+    static size_t cap = 0;
+    const size_t need = static_cast<size_t>(grid) * (v->T / 32) * 4;
+    if (need > cap) { cudaFree(buf); cudaMalloc(&buf, need * 8); cap = need; }
+    cudaMemsetAsync(buf, 0, need * 8, c->stream);
+    P.phase_prof = buf;
+    c->phase_prof = buf;
+    c->phase_prof_n = need;
+  }
 
   cudaStream_t st = c->stream;
   FB_CUDA(c, cudaEventRecord(c->ev[0], st));
@@ -383,15 +436,56 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
                                                 c->d_prep, c->d_solveF, c->d_skip, c->d_flag);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
-  v->fn<<<grid, v->T, smem, st>>>(P);
+  fn<<<grid, v->T, smem, st>>>(P);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[2], st));
-  post_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, c->d_prep, c->d_out, dres);
+  post_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, c->d_prep, c->d_out,
+                                                c->d_solveF, dres);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[3], st));
   c->last_solves = n_solves;
   c->last_launches = 3;
   return FIBRA_OK;
+}
+
+// packed-node view of one reference FiberNetwork (free-first packing, network.cpp:120-143)
+struct PackedNet {
+  int N = 0, M = 0, NFN = 0;
+  std::vector<double> ref, lump;       // by packed node
+  std::vector<int> a, b;               // fiber endpoints as packed nodes
+  std::vector<double> l0, ea;
+  double max_lump = 0;
+  bool ok = true;
+  std::string err;
+};
+
+PackedNet pack(const fibra_net_desc& d) {
+  PackedNet P;
+  P.N = d.n_nodes;
+  P.M = d.n_fibers;
+  P.NFN = d.n_free / 3;
+  std::vector<int> node_of_pn(P.N);
+  for (int node = 0; node < P.N; ++node) node_of_pn[d.packed_of_dof[3 * node] / 3] = node;
+  P.ref.assign(d.packed_ref, d.packed_ref + 3 * static_cast<size_t>(P.N));
+  P.lump.resize(P.N);
+  for (int pn = 0; pn < P.N; ++pn) {
+    P.lump[pn] = d.node_lump[node_of_pn[pn]];
+    if (!(P.lump[pn] > 0) && P.ok) {  // setup_mass relax.cpp:29-31
+      P.ok = false;
+      P.err = "node " + std::to_string(node_of_pn[pn]) + " has no incident fibers (singular mass)";
+    }
+    P.max_lump = (P.max_lump < P.lump[pn]) ? P.lump[pn] : P.max_lump;
+  }
+  P.a.resize(P.M);
+  P.b.resize(P.M);
+  P.l0.assign(d.rest_length, d.rest_length + P.M);
+  P.ea.resize(P.M);
+  for (int f = 0; f < P.M; ++f) {
+    P.a[f] = d.fiber_packed_dofs[6 * f] / 3;
+    P.b[f] = d.fiber_packed_dofs[6 * f + 3] / 3;
+    P.ea[f] = d.fiber_area[f] * d.fiber_modulus[f];  // FiberNetwork::fiber_ea
+  }
+  return P;
 }
 
 }  // namespace
@@ -433,6 +527,7 @@ int fibra_cuda_close(fibra_ctx* c) {
   free_points(c);
   free_scratch(c);
   free_library(c);
+  cudaFree(c->d_ckpt);
   cudaFree(c->d_ticket);
   cudaFree(c->d_counters);
   for (auto& e : c->ev) cudaEventDestroy(e);
@@ -461,75 +556,144 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   free_library(c);
-  c->entries.resize(n);
-  std::vector<EntryDev> host(n);
+  std::vector<PackedNet> nets;
+  nets.reserve(n);
   for (int i = 0; i < n; ++i) {
     const fibra_net_desc& d = entries[i];
+    if (d.n_nodes <= 0 || d.n_fibers < 0 || d.n_free % 3 != 0)
+      return set_err(c, FIBRA_E_ARG, "malformed library entry " + std::to_string(i));
+    nets.push_back(pack(d));
+  }
+  // one kernel variant for the whole library: the first whose capacity covers every entry
+  c->entries.resize(n);
+  for (const Variant& v : kVariants) {
+    bool ok = true;
+    for (int i = 0; i < n && ok; ++i) {
+      const PackedNet& P = nets[i];
+      ok = build_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.FPT, v.NPT,
+                          c->entries[i].sched) &&
+           c->entries[i].sched.node_slots * 24 < 65536;
+    }
+    if (ok) {
+      c->variant = &v;
+      break;
+    }
+  }
+  if (!c->variant)
+    return set_err(c, FIBRA_E_ARG, "RVE too large for the resident kernel variants");
+  c->uniform_ea = true;
+  for (const PackedNet& P : nets)
+    for (int f = 1; f < P.M && c->uniform_ea; ++f) c->uniform_ea = (P.ea[f] == P.ea[0]);
+  std::vector<EntryDev> host(n);
+  int max_ts = 0, max_gbytes = 0, max_ent = 0;
+  for (int i = 0; i < n; ++i) {
+    const PackedNet& P = nets[i];
     DeviceEntry& de = c->entries[i];
-    const int N = d.n_nodes, M = d.n_fibers;
-    if (N <= 0 || N >= 65536 || M < 0 || d.n_free % 3 != 0)
-      return set_err(c, FIBRA_E_ARG, "unsupported network size in library entry " + std::to_string(i));
-    // packed-node views of the reference layout (free-first packing, network.cpp:120-143)
-    std::vector<int> node_of_pn(N);
-    for (int node = 0; node < N; ++node) node_of_pn[d.packed_of_dof[3 * node] / 3] = node;
-    std::vector<double> lump(N);
-    double max_lump = 0;
-    for (int pn = 0; pn < N; ++pn) {
-      lump[pn] = d.node_lump[node_of_pn[pn]];
-      if (!(lump[pn] > 0) && de.config_ok) {  // setup_mass relax.cpp:29-31
-        de.config_ok = false;
-        de.config_err = "node " + std::to_string(node_of_pn[pn]) +
-                        " has no incident fibers (singular mass)";
+    const Schedule& S = de.sched;
+    de.config_ok = P.ok;
+    de.config_err = P.err;
+    const int TS = c->variant->NPT * c->variant->T;  // thread slots; dummy x records at TS, TS+1
+    const int FS = S.fiber_slots;
+    std::vector<int> slot_pn(TS, -1);
+    std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
+    for (int sl = 0; sl < S.node_slots; ++sl) {
+      const int pn = S.pn_of_slot[sl];
+      slot_pn[sl] = pn;
+      if (pn < 0) continue;
+      for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
+      slot_lump[sl] = P.lump[pn];
+    }
+    // g*d records: [real (schedule)] [dummies of empty fiber slots, bank = lane] [zero]
+    std::vector<int> gslot_of_fslot(FS, -1);
+    int dummy_per_lane[16] = {0};
+    for (int fs = 0; fs < FS; ++fs)
+      if (S.fiber_of_fslot[fs] < 0) gslot_of_fslot[fs] = S.gd_slots + 16 * dummy_per_lane[fs % 16]++ + fs % 16;
+    int max_dummy = 0;
+    for (int l = 0; l < 16; ++l) max_dummy = std::max(max_dummy, dummy_per_lane[l]);
+    const int zero_rec = S.gd_slots + 16 * max_dummy;
+    const int gd_total = zero_rec + 1;
+    // CSR by slot, ascending fiber id, padded to even length with the zero record;
+    // entry = g*d record byte offset | (node is the stored tail) << 31
+    std::vector<std::vector<int>> lists(TS);
+    for (int f = 0; f < P.M; ++f) {
+      const int g = 24 * S.gslot_of_fiber[f];
+      const int ts = S.slot_of_pn[S.tail_pn[f]], hs = S.slot_of_pn[S.head_pn[f]];
+      lists[ts].push_back(f);
+      lists[hs].push_back(f);
+      (void)g;
+    }
+    std::vector<int> off(TS + 1, 0), ent;
+    for (int sl = 0; sl < TS; ++sl) {
+      auto& L = lists[sl];
+      std::sort(L.begin(), L.end());  // reference accumulation order (network.cpp:298-303)
+      const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
+      for (int f : L) {
+        const int g = 24 * S.gslot_of_fiber[f];
+        ent.push_back(pn == S.tail_pn[f] ? static_cast<int>(g | 0x80000000u) : g);
       }
-      max_lump = (max_lump < lump[pn]) ? lump[pn] : max_lump;
+      if (L.size() % 2) ent.push_back(24 * zero_rec);
+      off[sl + 1] = static_cast<int>(ent.size());
     }
-    std::vector<int> ab(M);
-    std::vector<double> ea(M);
-    std::vector<int> off(N + 1, 0), ent(2 * static_cast<size_t>(M));
-    for (int f = 0; f < M; ++f) {
-      const int a = d.fiber_packed_dofs[6 * f] / 3, b = d.fiber_packed_dofs[6 * f + 3] / 3;
-      ab[f] = a | (b << 16);
-      ea[f] = d.fiber_area[f] * d.fiber_modulus[f];  // FiberNetwork::fiber_ea
-      ++off[a + 1];
-      ++off[b + 1];
-    }
-    for (int pn = 0; pn < N; ++pn) off[pn + 1] += off[pn];
-    std::vector<int> fill(off.begin(), off.end() - 1);
-    for (int f = 0; f < M; ++f) {  // ascending fiber id within every node's list
-      const int a = ab[f] & 0xffff, b = ab[f] >> 16;
-      ent[fill[a]++] = (f << 1) | 1;
-      ent[fill[b]++] = (f << 1);
+    std::vector<int> fab(FS), fg(FS), fid(FS, -1);
+    std::vector<double> fl0(FS, 0.5), fea(FS, 1.0);
+    for (int fs = 0; fs < FS; ++fs) {
+      const int f = S.fiber_of_fslot[fs];
+      if (f < 0) {  // dummy: unit segment between the two dummy x records
+        fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
+        fg[fs] = 24 * gslot_of_fslot[fs];
+        continue;
+      }
+      fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
+      fg[fs] = 24 * S.gslot_of_fiber[f];
+      fid[fs] = f;
+      fl0[fs] = P.l0[f];
+      fea[fs] = P.ea[f];
     }
     EntryDev& E = host[i];
-    E.n_nodes = N;
-    E.n_fibers = M;
-    E.n_free_nodes = d.n_free / 3;
-    E.max_lump = max_lump;
-    E.max_ea = d.max_ea;
-    E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;  // RveBox::volume
-    auto up = [&](auto** dst, const auto* src, size_t count) -> int {
-      using Tp = std::remove_const_t<std::remove_pointer_t<decltype(src)>>;
+    E.n_nodes = P.N;
+    E.n_fibers = P.M;
+    E.n_free_nodes = P.NFN;
+    E.n_fix_nodes = P.N - P.NFN;
+    E.f0 = S.f0;
+    E.node_slots = S.node_slots;
+    E.fiber_slots = FS;
+    E.gd_slots = gd_total;
+    E.thread_slots = TS;
+    E.max_lump = P.max_lump;
+    E.max_ea = entries[i].max_ea;
+    E.box_volume = 8.0 * entries[i].box_half * entries[i].box_half * entries[i].box_half;
+    auto up = [&](auto** dst, const auto& vec) -> int {
+      using Tp = typename std::decay_t<decltype(vec)>::value_type;
       Tp* p = nullptr;
-      FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(count, 1) * sizeof(Tp)));
+      FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(vec.size(), 1) * sizeof(Tp)));
       de.allocs.push_back(p);
-      if (count) FB_CUDA(c, cudaMemcpy(p, src, count * sizeof(Tp), cudaMemcpyHostToDevice));
+      if (!vec.empty())
+        FB_CUDA(c, cudaMemcpy(p, vec.data(), vec.size() * sizeof(Tp), cudaMemcpyHostToDevice));
       *dst = p;
       return FIBRA_OK;
     };
     int rc;
-    if ((rc = up(&E.ref, d.packed_ref, 3 * static_cast<size_t>(N)))) return rc;
-    if ((rc = up(&E.lump, lump.data(), N))) return rc;
-    if ((rc = up(&E.fiber_ab, ab.data(), M))) return rc;
-    if ((rc = up(&E.l0, d.rest_length, M))) return rc;
-    if ((rc = up(&E.ea, ea.data(), M))) return rc;
-    if ((rc = up(&E.csr_off, off.data(), N + 1))) return rc;
-    if ((rc = up(&E.csr_ent, ent.data(), 2 * static_cast<size_t>(M)))) return rc;
+    if ((rc = up(&E.slot_pn, slot_pn))) return rc;
+    if ((rc = up(&E.slot_ref, slot_ref))) return rc;
+    if ((rc = up(&E.slot_lump, slot_lump))) return rc;
+    if ((rc = up(&E.csr_off, off))) return rc;
+    if ((rc = up(&E.csr_ent, ent))) return rc;
+    if ((rc = up(&E.fib_ab, fab))) return rc;
+    if ((rc = up(&E.fib_g, fg))) return rc;
+    if ((rc = up(&E.fib_id, fid))) return rc;
+    if ((rc = up(&E.fib_l0, fl0))) return rc;
+    if ((rc = up(&E.fib_ea, fea))) return rc;
     de.dev = E;
-    c->nmax = std::max(c->nmax, N);
-    c->mmax = std::max(c->mmax, M);
+    max_ts = std::max(max_ts, TS);
+    max_ent = std::max(max_ent, static_cast<int>(ent.size()));
+    const int gb = std::max(24 * gd_total, 8 * (3 * P.N + 3 * P.NFN + P.M));
+    max_gbytes = std::max(max_gbytes, gb);
   }
-  c->nmax = (c->nmax + 1) & ~1;  // keep double/int regions aligned
-  c->mmax = (c->mmax + 1) & ~1;
+  c->x_bytes = static_cast<int>(align16(24 * static_cast<size_t>(max_ts + 2)));
+  c->g_bytes = static_cast<int>(align16(max_gbytes));
+  c->part_slots = max_ts;
+  c->csr_cap = max_ent;
+  c->ck_stride = max_ts;
   FB_CUDA(c, cudaMalloc(&c->d_entries, sizeof(EntryDev) * n));
   FB_CUDA(c, cudaMemcpy(c->d_entries, host.data(), sizeof(EntryDev) * n, cudaMemcpyHostToDevice));
   return FIBRA_OK;
@@ -653,6 +817,14 @@ int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {
   FB_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]));
   cudaFree(sink);
   *out = 8.0 * iters * static_cast<double>(blocks) * threads / (ms * 1e-3);
+  return FIBRA_OK;
+}
+
+int fibra_cuda_phase_profile(fibra_ctx* c, unsigned long long* out, size_t cap, size_t* n) {
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
+  *n = c->phase_prof_n;
+  if (c->phase_prof && out && cap >= c->phase_prof_n)
+    FB_CUDA(c, cudaMemcpy(out, c->phase_prof, c->phase_prof_n * 8, cudaMemcpyDeviceToHost));
   return FIBRA_OK;
 }
 

@@ -17,3 +17,17 @@ db.reset_states()
 rec = db.solve(F, relax_cfg=cfg, want_tangent=False)
 s = db.last_stats()
 print(s, "us/iter/CTA:", s["dr_kernel_ms"] * 1e3 / its)
+if os.environ.get("FIBRA_PHASE_PROF"):
+    import ctypes as C
+    from paper_2306_09427_b200 import _capi
+    L = _capi.load()
+    nn = C.c_size_t()
+    L.fibra_cuda_phase_profile(db._ctx, None, 0, C.byref(nn))
+    buf = (C.c_uint64 * nn.value)()
+    L.fibra_cuda_phase_profile(db._ctx, buf, nn.value, C.byref(nn))
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 4).astype(float) / its
+    nw = a.shape[0] // (len(F) if len(F) < 296 else 296)
+    print("per-iteration cycles per warp (mean over CTAs): fiber, bar1, node, bar2")
+    a = a.reshape(-1, nw, 4)
+    for w in range(nw):
+        print(w, np.round(a[:, w].mean(0), 1))
