@@ -192,6 +192,7 @@ def main():
     stream = torch.cuda.Stream(device=local)  # explicit stream shared by torch and the solver
     torch.cuda.set_stream(stream)
     db = P.DeviceBatch(lib, assign, device=local, stream=stream.cuda_stream)
+    peak = db.fp64_peak()  # FP64-pipe roofline denominator, measured while the GPU is idle
     rec_bytes = P.RESULT_DTYPE.itemsize
     F_dev = torch.from_numpy(F).to(f"cuda:{local}")
     out_dev = torch.empty(n * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
@@ -271,7 +272,6 @@ def main():
     d2h = n * rec_bytes + 7 * tot * 8 + n * (8 + 8 + 1)
 
     if rank == 0:
-        peak = db.fp64_peak()
         achieved = all_pipe / world / (max_dr_ms * 1e-3)  # per-GPU FP64-pipe lane-ops/s
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

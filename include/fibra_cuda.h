@@ -179,6 +179,9 @@ int fibra_cuda_device_count(int* n);
 /* FP64-pipe roofline denominator measured on this device: independent DADD chains on every
  * SM; returns lane-operations per second (one DADD/DMUL/DFMA lane = 1 op). */
 int fibra_cuda_fp64_peak(fibra_ctx* ctx, double* lane_ops_per_s);
+/* Self-test: the DR kernel's branch-free division / square root (csrc/fastmath.cuh) against
+ * the built-in IEEE operators on n pseudo-random operand pairs; counts bit mismatches. */
+int fibra_cuda_selftest_fastmath(fibra_ctx* ctx, uint64_t n, uint64_t seed, uint64_t* mismatches);
 /* Diagnostics: with FIBRA_PHASE_PROF set in the environment, the last solve accumulated
  * per-warp cycles [fiber work, barrier 1, node work, barrier 2] for every CTA. */
 int fibra_cuda_phase_profile(fibra_ctx* ctx, unsigned long long* out, size_t cap, size_t* n);

@@ -150,6 +150,53 @@ __global__ void post_kernel(int n, const double* __restrict__ F, int want_tangen
   res[p] = r;
 }
 
+// Self-test of fastmath.cuh: div_fast / sqrt_fast (+ the built-in fallback the DR kernel
+// applies when the predicate fails) against the built-in IEEE operators, bit for bit.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  return x ^ (x >> 33);
+}
+
+__device__ __forceinline__ double operand(unsigned long long r, int mode) {
+  // mode 0: |exponent| <= 64 around 1; mode 1: any finite exponent; mode 2: raw bits
+  // (zeros, denormals, inf, NaN); mode 3: short-mantissa values (exact cases)
+  const unsigned long long sign = (r >> 63) << 63;
+  const unsigned long long mant = r & 0x000fffffffffffffull;
+  unsigned long long e;
+  if (mode == 0) e = 1023 - 64 + ((r >> 52) & 127);
+  else if (mode == 1) e = 1 + ((r >> 52) % 2046);
+  else if (mode == 2) return __longlong_as_double(static_cast<long long>(r));
+  else return static_cast<double>(static_cast<long long>(r >> 40) % 4096) * 0.125;
+  return __longlong_as_double(static_cast<long long>(sign | (e << 52) | mant));
+}
+
+__device__ __forceinline__ bool same_bits(double x, double y) {
+  return __double_as_longlong(x) == __double_as_longlong(y) || (isnan(x) && isnan(y));
+}
+
+__global__ void fastmath_selftest_kernel(unsigned long long n, unsigned long long seed,
+                                         unsigned long long* bad) {
+  unsigned long long local = 0;
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+       i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+    const unsigned long long r0 = mix64(seed ^ (2 * i)), r1 = mix64(seed ^ (2 * i + 1));
+    const int mode = static_cast<int>(i & 3);
+    const double a = operand(r0, mode), b = operand(r1, mode == 3 ? 0 : mode);
+    bool ok;
+    double q = div_fast(a, b, ok);
+    if (!ok) q = a / b;
+    local += !same_bits(q, a / b);
+    const double x = mode == 2 ? a : fabs(a);
+    double s = sqrt_fast(x, ok);
+    if (!ok) s = sqrt(x);
+    local += !same_bits(s, sqrt(x));
+  }
+  if (local) atomicAdd(bad, local);
+}
+
 // FP64 pipe peak probe: 8 independent DADD chains per thread, 1024 threads per SM
 __global__ void fp64_peak_kernel(double* sink, int iters, double c) {
   double x[8];
@@ -803,20 +850,40 @@ int fibra_cuda_solve_device(fibra_ctx* c, const double* F_dev, const fibra_law* 
   return launch_solve(c, F_dev, law, relax, stiff, want_tangent, out_dev);
 }
 
+int fibra_cuda_selftest_fastmath(fibra_ctx* c, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  FB_CUDA(c, cudaSetDevice(c->device));
+  unsigned long long* d = nullptr;
+  FB_CUDA(c, cudaMalloc(&d, sizeof(unsigned long long)));
+  FB_CUDA(c, cudaMemsetAsync(d, 0, sizeof(unsigned long long), c->stream));
+  fastmath_selftest_kernel<<<4 * c->n_sm, 256, 0, c->stream>>>(n, seed, d);
+  FB_CUDA(c, cudaGetLastError());
+  unsigned long long h = 0;
+  FB_CUDA(c, cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d);
+  *mismatches = h;
+  return FIBRA_OK;
+}
+
 int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {
   FB_CUDA(c, cudaSetDevice(c->device));
   double* sink = nullptr;
   FB_CUDA(c, cudaMalloc(&sink, 1024 * sizeof(double)));
   const int iters = 1 << 16, blocks = 4 * c->n_sm, threads = 256;
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
   fp64_peak_kernel<<<blocks, threads, 0, c->stream>>>(sink, 64, 1e-9);  // warm-up
-  FB_CUDA(c, cudaEventRecord(c->ev[0], c->stream));
-  fp64_peak_kernel<<<blocks, threads, 0, c->stream>>>(sink, iters, 1e-9);
-  FB_CUDA(c, cudaEventRecord(c->ev[3], c->stream));
-  FB_CUDA(c, cudaEventSynchronize(c->ev[3]));
-  float ms = 0;
-  FB_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]));
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {  // best of three, stream otherwise idle
+    FB_CUDA(c, cudaEventRecord(c->ev[0], c->stream));
+    fp64_peak_kernel<<<blocks, threads, 0, c->stream>>>(sink, iters, 1e-9);
+    FB_CUDA(c, cudaEventRecord(c->ev[3], c->stream));
+    FB_CUDA(c, cudaEventSynchronize(c->ev[3]));
+    float ms = 0;
+    FB_CUDA(c, cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]));
+    best = std::min(best, ms);
+  }
   cudaFree(sink);
-  *out = 8.0 * iters * static_cast<double>(blocks) * threads / (ms * 1e-3);
+  *out = 8.0 * iters * static_cast<double>(blocks) * threads / (best * 1e-3);
   return FIBRA_OK;
 }
 

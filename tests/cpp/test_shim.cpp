@@ -1,0 +1,104 @@
+// Drop-in check: the reference's own types and generator (compiled from /root/reference,
+// oracle/_ref/obj) feed include/fibra_b200/batch_response.hpp, which runs on the B200
+// through fibra_cuda.h; results are compared bit for bit with the oracle's batch_response.
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <span>
+#include <vector>
+
+#include "fibra/netgen.hpp"
+#include "fibra_b200/batch_response.hpp"
+#include "fibra_oracle.h"
+
+using namespace fibra;
+
+static double u01(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
+
+int main() {
+  RveLibrary lib;
+  NetGenSpec spec;
+  spec.style = NetGenSpec::Style::knn;
+  spec.nodes = 14;
+  spec.fibers = 38;
+  spec.neighbors = 9;
+  lib.entries.push_back(generate_network(spec, 101));
+  spec.nodes = 12;
+  spec.fibers = 32;
+  lib.entries.push_back(generate_network(spec, 102));
+  const int n = 8;
+  BatchAssignment assign;
+  std::mt19937_64 pick(7);
+  for (int p = 0; p < n; ++p) assign.entry_of_point.push_back(static_cast<int32_t>(pick() % 2));
+  PackedStates st;  // init_batch (batch.cpp:94-145) without the Eigen-dependent TU
+  st.offsets.assign(n + 1, 0);
+  for (int p = 0; p < n; ++p) {
+    const FiberNetwork& net = lib.entries[assign.entry_of_point[p]];
+    st.offsets[p + 1] = st.offsets[p] + net.n_dof();
+    st.n_free.push_back(net.n_free());
+  }
+  const size_t tot = st.offsets.back();
+  for (auto* v : {&st.u, &st.v, &st.a, &st.f_int, &st.f_damp, &st.mass, &st.inv_mass}) v->assign(tot, 0.0);
+  st.t.assign(n, 0.0);
+  st.iters.assign(n, 0);
+  st.converged.assign(n, 0);
+  std::vector<Def3> fs;
+  std::mt19937_64 rng(55);  // test_batch.cpp:149-157
+  for (int p = 0; p < n; ++p) {
+    Def3 f = Def3::identity();
+    f(0, 0) += 0.01 + 0.05 * u01(rng);
+    f(1, 1) -= 0.0 + 0.02 * u01(rng);
+    f(0, 1) += 0.0 + 0.02 * u01(rng);
+    fs.push_back(f);
+  }
+  WorkerPool pool(1);
+  const BatchResult br = fibra_b200::batch_response(lib, assign, st, FiberLaw{}, fs, RelaxConfig{},
+                                                    StiffnessConfig{}, pool);
+  // oracle
+  std::vector<or_network> onets(2);
+  std::vector<const or_network*> optr;
+  for (int e = 0; e < 2; ++e) {
+    const FiberNetwork& net = lib.entries[e];
+    std::vector<double> c(3 * net.n_nodes()), ar, mo;
+    std::vector<int32_t> fa, fb;
+    for (int i = 0; i < net.n_nodes(); ++i)
+      for (int k = 0; k < 3; ++k) c[3 * i + k] = net.coords()[i][k];
+    for (const Fiber& f : net.fibers()) {
+      fa.push_back(f.a);
+      fb.push_back(f.b);
+      ar.push_back(f.area);
+      mo.push_back(f.modulus);
+    }
+    if (or_network_build(c.data(), net.n_nodes(), fa.data(), fb.data(), ar.data(), mo.data(),
+                         net.n_fibers(), 0.5, 1e-6, &onets[e])) return 2;
+    optr.push_back(&onets[e]);
+  }
+  std::vector<double> u(tot, 0), v(tot, 0), a(tot, 0), fi(tot, 0), fd(tot, 0), m(tot, 0), im(tot, 0), t(n, 0);
+  std::vector<int64_t> it(n, 0);
+  std::vector<uint8_t> cv(n, 0);
+  std::vector<double> F(9 * n);
+  for (int p = 0; p < n; ++p)
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) F[9 * p + 3 * i + j] = fs[p](i, j);
+  or_law law{0, 1.0, 1.2, 0};
+  or_relax_cfg rc{2.0, 1e-6, 500000, 0.8, 1.0};
+  std::vector<or_response> out(n);
+  std::vector<int32_t> status(n);
+  or_batch_response(optr.data(), assign.entry_of_point.data(), n, st.offsets.data(), u.data(), v.data(),
+                    a.data(), fi.data(), fd.data(), m.data(), im.data(), t.data(), it.data(), cv.data(),
+                    st.n_free.data(), &law, F.data(), &rc, 1e-5, 1, 1, 1, out.data(), status.data());
+  int bad = 0;
+  for (int p = 0; p < n; ++p) {
+    const double s6[6] = {br.responses[p].sigma.xx, br.responses[p].sigma.yy, br.responses[p].sigma.zz,
+                          br.responses[p].sigma.yz, br.responses[p].sigma.xz, br.responses[p].sigma.xy};
+    bad += std::memcmp(s6, out[p].sigma, sizeof s6) != 0;
+    bad += std::memcmp(&br.responses[p].spatial_c.m[0][0], out[p].spatial_c, sizeof out[p].spatial_c) != 0;
+    bad += br.stats[p].solves != 7 || br.stats[p].relax_iterations != out[p].relax_iterations;
+  }
+  bad += !br.failed.empty();
+  bad += std::memcmp(st.u.data(), u.data(), tot * 8) != 0;
+  bad += std::memcmp(st.f_int.data(), fi.data(), tot * 8) != 0;
+  std::printf("%s: %d mismatches over %d points (sigma, C, stats, PackedStates)\n",
+              bad ? "FAIL" : "OK", bad, n);
+  return bad ? 1 : 0;
+}

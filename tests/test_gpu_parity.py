@@ -158,3 +158,16 @@ def test_config1_tangent_bitwise(oracle_lib):
         assert same_bits(br.responses[p].spatial_c, resp[p]["spatial_c"])
         assert br.stats[p].relax_iterations == resp[p]["relax_iterations"]
     check_states(gst, ost)
+
+
+def test_cpp_dropin_shim_bitwise():
+    """include/fibra_b200/batch_response.hpp driven by the reference's own C++ types and
+    generator (tests/cpp/test_shim.cpp, built here by `make -C tests/cpp`)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "build", "test_shim")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/build/test_shim not built (needs /root/reference)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "OK" in r.stdout
