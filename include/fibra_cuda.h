@@ -83,6 +83,11 @@ void fibra_network_free(fibra_network* net);
 const char* fibra_host_last_error(void);
 /* init_batch random policy (batch.cpp:101-104): entry_of_point[p] = mt19937_64(seed)() % n */
 int fibra_assign_random(uint64_t seed, int32_t n_points, int32_t n_entries, int32_t* out);
+/* Diagnostics: quality of the bank-aware slot schedule (csrc/host/schedule.cpp) of one
+ * network for a kernel shape (T threads, FPT fibers and NPT nodes per thread).
+ * out[6] = {fits, conflicting fiber groups, gather excess wavefronts, gather steps,
+ *           g*d records, node slots}. */
+int fibra_schedule_report(const fibra_net_desc* net, int T, int FPT, int NPT, int64_t* out);
 
 /* ---- solver configuration records ------------------------------------------------- */
 typedef struct {          /* FiberLaw network.hpp:27-38                              */

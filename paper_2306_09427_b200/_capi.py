@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "ok", 1: "config", 2: "kinematics", 3: "collapse", 4: "bad_dt
 EXPORTS = [
     "fibra_network_create", "fibra_network_generate", "fibra_network_read",
     "fibra_network_write", "fibra_network_describe", "fibra_network_free",
-    "fibra_host_last_error", "fibra_assign_random",
+    "fibra_host_last_error", "fibra_assign_random", "fibra_schedule_report",
     "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
@@ -119,6 +119,7 @@ def load(build_if_missing: bool = True):
         "fibra_network_free": (None, [vp]),
         "fibra_host_last_error": (C.c_char_p, []),
         "fibra_assign_random": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, _ip]),
+        "fibra_schedule_report": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, _lp]),
         "fibra_cuda_open": (C.c_int, [C.c_int, pp]),
         "fibra_cuda_close": (C.c_int, [vp]),
         "fibra_cuda_last_error": (C.c_char_p, [vp]),

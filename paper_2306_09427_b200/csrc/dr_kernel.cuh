@@ -46,13 +46,14 @@ namespace fibra_b200 {
 struct EntryDev {          // one RveLibrary entry in HBM, already in slot order
   int n_nodes, n_fibers, n_free_nodes, n_fix_nodes;
   int f0, node_slots, fiber_slots, gd_slots;  // gd_slots includes dummies + zero record
-  int thread_slots, pad0, pad1, pad2;         // NPT*T (two dummy x records follow)
+  int thread_slots, max_pairs, pad1, pad2;    // NPT*T (two dummy x records follow)
   double max_lump, max_ea, box_volume, pad3;
   const int* slot_pn;      // [thread_slots] packed node id per slot, -1 empty
   const double* slot_ref;  // [3*thread_slots] reference coordinates by slot
   const double* slot_lump; // [thread_slots] lumping weight by slot (1 when empty)
-  const int* csr_off;      // [thread_slots+1] (even-length lists)
-  const int* csr_ent;      // 24*gslot | (node is the stored tail) << 31
+  const int* csr_npairs;   // [thread_slots] CSR entry pairs per slot (lists padded to even)
+  const int2* csr_pairs;   // [max_pairs][thread_slots] step-major: lanes read consecutive
+                           // pairs; entry = 24*gslot | (node is the stored tail) << 31
   const int* fib_ab;       // [fiber_slots] 24*tail_slot | 24*head_slot << 16
   const int* fib_g;        // [fiber_slots] 24*gslot
   const int* fib_id;       // [fiber_slots] reference fiber id, -1 dummy
@@ -96,6 +97,11 @@ struct DrParams {
 
 enum : int { kDecConv = 1, kDecExact = 2, kDecNonfinite = 4 };
 
+// Checkpoints of (u, v_half) are taken at resume passes 0, C, 2C, ... alternating between
+// two buffers (buffer (r/C)&1 holds resume pass r); a stop detected one pass late replays
+// at most 2C passes.
+constexpr int kCkInterval = 8;
+
 // Per-warp phase cycle counters, compiled only into the diagnostics build
 // (FIBRA_PHASE_PROF=1 python -m paper_2306_09427_b200.build -> lib/libfibra_b200_prof.so).
 #ifdef FIBRA_PHASE_PROF
@@ -107,8 +113,7 @@ enum : int { kDecConv = 1, kDecExact = 2, kDecNonfinite = 4 };
 struct __align__(16) DrCtl {
   int solve, point, q, entry;
   int flag, collapse, dec, pad0;
-  long long ck_k[2];
-  double ck_t[2], ck_dt[2];
+  double ck_t[2], ck_dt[2];  // checkpoint buffers: t after, dt of, the resume pass
   double warp_min[32];
   double ex[12];
   double t;
@@ -185,8 +190,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   unsigned char* X = smem;
   unsigned char* G = smem + P.x_bytes;
   double* spart = reinterpret_cast<double*>(G + P.g_bytes);
-  int* coff = reinterpret_cast<int*>(spart + P.part_slots);
-  int* cent = coff + P.part_slots + 1;
+  int2* cent = reinterpret_cast<int2*>(spart + P.part_slots);  // step-major CSR pairs
   double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
 
   const double B = P.nonlinearity;
@@ -195,10 +199,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   // register-resident topology of the loaded entry
   int fab[FPT], fgo[FPT];
   double fl0[FPT], fs[FPT], fmred[FPT];
-  int nbeg[NPT], nend[NPT];
+  int npair[NPT];
   double nref[NPT][3], ninv[NPT], ncm[NPT];
   int cur_entry = -1;
-  int N = 0, M = 0, NFN = 0, F0 = 0, NFIX = 0, NSLOT = 0;
   double s_uni = 0;  // UEA: the common ea_scale*EA
 #define SJ(j) (UEA ? s_uni : fs[j])
 
@@ -243,18 +246,13 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
     const EntryDev& E = P.entries[e];
     const double scale = P.density_scale / E.max_lump;  // setup_mass relax.cpp:35-43
+    // sizes are re-read from E where needed: keeping them live across the DR loop costs
+    // registers the 2-CTA/SM budget does not have
+    const int F0 = E.f0, NSLOT = E.node_slots;
     if (e != cur_entry) {
       cur_entry = e;
-      N = E.n_nodes;
-      M = E.n_fibers;
-      NFN = E.n_free_nodes;
-      NFIX = E.n_fix_nodes;
-      F0 = E.f0;
-      NSLOT = E.node_slots;
       s_uni = P.ea_scale * E.fib_ea[0];
-      const int n_ent = E.csr_off[E.thread_slots];
-      for (int i = tid; i <= E.thread_slots; i += T) coff[i] = E.csr_off[i];
-      for (int i = tid; i < n_ent; i += T) cent[i] = E.csr_ent[i];
+      for (int i = tid; i < E.max_pairs * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
       for (int i = tid; i < E.thread_slots; i += T) spart[i] = 0.0;
       // dummy x records for empty fiber slots, and the zero g*d record (last record)
       if (tid < 6) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid == 3) ? 1.0 : 0.0;
@@ -270,8 +268,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
-        nbeg[j] = E.csr_off[sl];
-        nend[j] = E.csr_off[sl + 1];
+        npair[j] = E.csr_npairs[sl];
         nref[j][0] = E.slot_ref[3 * sl];
         nref[j][1] = E.slot_ref[3 * sl + 1];
         nref[j][2] = E.slot_ref[3 * sl + 2];
@@ -286,7 +283,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     double lmin = INFINITY;
 #pragma unroll
     for (int j = 0; j < FPT; ++j) {  // reduced_mass_l0 relax.cpp:46-55
-      const int ta = (fab[j] & 0xffff) / 24, hb = (fab[j] >> 16) / 24;
+      const int ta = (fab[j] & 0xffff) / 24, hb = (static_cast<unsigned>(fab[j]) >> 16) / 24;
       if (ta < E.thread_slots) {
         const double ma = E.slot_lump[ta] * scale;
         const double mb = E.slot_lump[hb] * scale;
@@ -345,8 +342,6 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     }
     if (tid == 0) {
       ctl.t = is_base ? P.t[p] : 0.0;
-      ctl.ck_k[0] = 0;
-      ctl.ck_k[1] = -1;
       ctl.ck_t[0] = ctl.t;
       ctl.ck_dt[0] = 0.0;
       ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
@@ -366,7 +361,6 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
     int k = 0;              // force pass the next fiber phase evaluates
     int target = -1;        // pass at which to stop and decide exactly (replay mode)
-    int ck_count = 1;       // passes until the next checkpoint (resume points C, 2C, ...)
     double dt_k = 0;        // dt of iteration k (0 for the initial pass)
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
@@ -399,7 +393,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
           const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-          const double* xb_ = sm_at<double>(X, fab[j] >> 16);
+          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
           dx[j] = xb_[0] - xa_[0];
           dy[j] = xb_[1] - xa_[1];
           dz[j] = xb_[2] - xa_[2];
@@ -425,11 +419,16 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           }
         }
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) {
-          double* gr = sm_at<double>(G, fgo[j]);
-          gr[0] = g[j] * dx[j];
-          gr[1] = g[j] * dy[j];
-          gr[2] = g[j] * dz[j];
+        for (int j = 0; j < FPT; ++j) {  // head record +g*d, tail record (-g)*d == -(g*d)
+          double* gh = sm_at<double>(G, static_cast<unsigned>(fgo[j]) >> 16);
+          double* gt = sm_at<double>(G, fgo[j] & 0xffff);
+          const double ng = -g[j];
+          gh[0] = g[j] * dx[j];
+          gh[1] = g[j] * dy[j];
+          gh[2] = g[j] * dz[j];
+          gt[0] = ng * dx[j];
+          gt[1] = ng * dy[j];
+          gt[2] = ng * dz[j];
         }
         if (collapsed) ctl.collapse = 1;
         if (LAW != 0) {
@@ -447,8 +446,10 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         if ((d & (kDecConv | kDecExact)) || k - 1 == P.max_iterations) {
           // stop at k-1: replay from the newest checkpoint that resumes at or before it
           target = k - 1;
-          const int b = (ctl.ck_k[0] <= target && (ctl.ck_k[1] > target || ctl.ck_k[0] > ctl.ck_k[1])) ? 0 : 1;
-          k = static_cast<int>(ctl.ck_k[b]);
+          // resume points are the multiples of kCkInterval, alternating between buffers;
+          // the newest one <= target is still held (the save at target+1 used the other)
+          k = target / kCkInterval * kCkInterval;
+          const int b = (k / kCkInterval) & 1;
           dt_k = ctl.ck_dt[b];
           const double* ck = ckpt + b * 6 * P.ck_stride;
 #pragma unroll
@@ -492,18 +493,18 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
         double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
-        for (int i = nbeg[j]; i < nend[j]; i += 2) {  // even-length lists
-          const int e0 = cent[i], e1 = cent[i + 1];
-          const double* g0 = sm_at<double>(G, e0 & 0x7fffffff);
-          const double* g1 = sm_at<double>(G, e1 & 0x7fffffff);
+        for (int kp = 0; kp < npair[j]; ++kp) {  // two incidences per step
+          const int2 ep = cent[kp * (NPT * T) + sl];
+          const double* g0 = sm_at<double>(G, ep.x);  // this node's own signed record
+          const double* g1 = sm_at<double>(G, ep.y);
           const double a0 = g0[0], a1 = g0[1], a2 = g0[2];
           const double b0 = g1[0], b1 = g1[1], b2 = g1[2];
-          f0 = f0 + signed_by(a0, e0);
-          f1 = f1 + signed_by(a1, e0);
-          f2 = f2 + signed_by(a2, e0);
-          f0 = f0 + signed_by(b0, e1);
-          f1 = f1 + signed_by(b1, e1);
-          f2 = f2 + signed_by(b2, e1);
+          f0 = f0 + a0;  // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
+          f1 = f1 + a1;
+          f2 = f2 + a2;
+          f0 = f0 + b0;
+          f1 = f1 + b1;
+          f2 = f2 + b2;
         }
         fk[j][0] = f0;
         fk[j][1] = f1;
@@ -523,6 +524,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         }
         __syncthreads();
         if (tid < 8) {
+          const int NFN = E.n_free_nodes, NFIX = E.n_fix_nodes;
           const int base = tid < 4 ? 0 : 3 * NFN;
           const int len = tid < 4 ? 3 * NFN : 3 * NFIX;
           double acc = 0;
@@ -545,13 +547,16 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           // holds f) and, for base solves, to the PackedStates (batch.cpp:169-176).  Doing
           // it here keeps no exit arrays alive across the DR loop.
           double* SX = reinterpret_cast<double*>(G);
-          double* SW = SX + 3 * N;
+          double* SW = SX + 3 * E.n_nodes;
+          const bool base_solve = ctl.q < 0;
+          const long long soff = P.offsets[ctl.point];
+          const double mscale = P.density_scale / E.max_lump;
 #pragma unroll
           for (int j = 0; j < NPT; ++j) {
             const int sl = j * T + tid;
             const int pn = E.slot_pn[sl];
             if (pn < 0) continue;
-            const double m = E.slot_lump[sl] * scale;
+            const double m = E.slot_lump[sl] * mscale;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
               double fd = 0.0, acc = 0.0, vv = 0.0;  // fixed dofs / 0-iteration exit
@@ -562,8 +567,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
               }
               SX[3 * pn + c] = nref[j][c] + u[j][c];
               if (sl < F0) SW[3 * pn + c] = m * (vv * vv);
-              if (is_base) {
-                const long long d = off + 3 * pn + c;
+              if (base_solve) {
+                const long long d = soff + 3 * pn + c;
                 P.u[d] = u[j][c];
                 P.v[d] = vv;
                 P.a[d] = acc;
@@ -589,9 +594,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         dt_next = P.dt_safety * sqrt(mn);
       }
       const double h_n = 0.5 * dt_next;
-      const bool save = target < 0 && --ck_count == 0;
-      const int sb = (ctl.ck_k[0] < ctl.ck_k[1]) ? 0 : 1;  // overwrite the older buffer
-      if (save) ck_count = P.ck_interval;
+      const bool save = target < 0 && ((k + 1) % kCkInterval == 0);
+      const int sb = ((k + 1) / kCkInterval) & 1;
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
@@ -626,8 +630,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       FB_PROF({ const long long t1 = clock64(); pc2 += t1 - tq; tq = t1; })
       __syncthreads();
       FB_PROF({ const long long t1 = clock64(); pc3 += t1 - tq; tq = t1; })
-      if (save && tid == 0) {  // after the barrier: every thread has chosen `sb`
-        ctl.ck_k[sb] = k + 1;
+      if (save && tid == 0) {
         ctl.ck_t[sb] = ctl.t;
         ctl.ck_dt[sb] = dt_next;
       }
@@ -645,6 +648,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       pp[0] += pc0; pp[1] += pc1; pp[2] += pc2; pp[3] += pc3;
     })
     const bool zero_iter = (n_done == 0);
+    const int N = E.n_nodes, M = E.n_fibers, NFN = E.n_free_nodes, NFIX = E.n_fix_nodes;
+    const int s_ = ctl.solve, p_ = ctl.point;
+    const bool base_solve = ctl.q < 0;
     __syncthreads();
     double* SF = reinterpret_cast<double*>(X);                 // f, flat packed order (3N)
     double* SX = reinterpret_cast<double*>(G);                 // x = ref + u (3N)
@@ -655,7 +661,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       for (int j = 0; j < FPT; ++j) {
         const int f = E.fib_id[j * T + tid];
         if (f >= 0) {  // strain_energy relax.cpp:57-72 (reference fiber id order)
-          const int ta = E.slot_pn[(fab[j] & 0xffff) / 24], hb = E.slot_pn[(fab[j] >> 16) / 24];
+          const int ta = E.slot_pn[(fab[j] & 0xffff) / 24];
+          const int hb = E.slot_pn[(static_cast<unsigned>(fab[j]) >> 16) / 24];
           const double dx = SX[3 * hb] - SX[3 * ta];
           const double dy = SX[3 * hb + 1] - SX[3 * ta + 1];
           const double dz = SX[3 * hb + 2] - SX[3 * ta + 2];
@@ -707,17 +714,17 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           for (int i = 0; i < 9; ++i) o.moment[i] = sm[i];
           o.box_volume = E.box_volume;
         } else {
-          o.status = q < 0 ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;
+          o.status = base_solve ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;
         }
       }
-      P.out[s] = o;
-      if (is_base) {
-        P.t[p] = ctl.t;
+      P.out[s_] = o;
+      if (base_solve) {
+        P.t[p_] = ctl.t;
         if (status == FIBRA_OK) {  // a throw leaves iters untouched (relax.cpp:187)
-          P.iters[p] += n_done;
-          P.converged[p] = static_cast<unsigned char>(conv);
+          P.iters[p_] += n_done;
+          P.converged[p_] = static_cast<unsigned char>(conv);
         } else {
-          P.converged[p] = 0;      // apply_affine_bc already cleared it (network.cpp:268)
+          P.converged[p_] = 0;     // apply_affine_bc already cleared it (network.cpp:268)
         }
       }
       atomicAdd(P.counters + 0, static_cast<unsigned long long>(n_done));
@@ -726,12 +733,12 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
                                     (51ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
       atomicAdd(P.counters + 3, 1ull);
     }
-    if (is_base) {
+    if (base_solve) {
       __syncthreads();
       if (tid == 0) {
-        const int ok = (P.out[s].status == FIBRA_OK) ? 1 : 2;
+        const int ok = (P.out[s_].status == FIBRA_OK) ? 1 : 2;
         __threadfence();
-        atomicExch(P.base_flag + p, ok);
+        atomicExch(P.base_flag + p_, ok);
       }
     }
     __syncthreads();

@@ -650,36 +650,43 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
       slot_lump[sl] = P.lump[pn];
     }
-    // g*d records: [real (schedule)] [dummies of empty fiber slots, bank = lane] [zero]
-    std::vector<int> gslot_of_fslot(FS, -1);
-    int dummy_per_lane[16] = {0};
+    // g*d records: [real: tail (-g*d) and head (+g*d) per fiber, schedule colouring]
+    //               [two per dummy fiber slot, bank = lane] [zero record]
+    // (all dummies of one lane share a record pair: their values are never read, and within
+    //  one store instruction the 16 lanes still hit 16 different banks)
+    std::vector<int> dummy_tail(FS, -1), dummy_head(FS, -1);
     for (int fs = 0; fs < FS; ++fs)
-      if (S.fiber_of_fslot[fs] < 0) gslot_of_fslot[fs] = S.gd_slots + 16 * dummy_per_lane[fs % 16]++ + fs % 16;
-    int max_dummy = 0;
-    for (int l = 0; l < 16; ++l) max_dummy = std::max(max_dummy, dummy_per_lane[l]);
-    const int zero_rec = S.gd_slots + 16 * max_dummy;
+      if (S.fiber_of_fslot[fs] < 0) {
+        dummy_tail[fs] = S.gd_slots + fs % 16;
+        dummy_head[fs] = S.gd_slots + 16 + fs % 16;
+      }
+    const int zero_rec = S.gd_slots + 32;
     const int gd_total = zero_rec + 1;
+    if (24 * gd_total >= 65536)
+      return set_err(c, FIBRA_E_ARG, "too many g*d records for 16-bit offsets in entry " + std::to_string(i));
     // CSR by slot, ascending fiber id, padded to even length with the zero record;
-    // entry = g*d record byte offset | (node is the stored tail) << 31
+    // entry = byte offset of the node's own record of that fiber
     std::vector<std::vector<int>> lists(TS);
     for (int f = 0; f < P.M; ++f) {
-      const int g = 24 * S.gslot_of_fiber[f];
-      const int ts = S.slot_of_pn[S.tail_pn[f]], hs = S.slot_of_pn[S.head_pn[f]];
-      lists[ts].push_back(f);
-      lists[hs].push_back(f);
-      (void)g;
+      lists[S.slot_of_pn[S.tail_pn[f]]].push_back(f);
+      lists[S.slot_of_pn[S.head_pn[f]]].push_back(f);
     }
-    std::vector<int> off(TS + 1, 0), ent;
+    int max_pairs = 0;
     for (int sl = 0; sl < TS; ++sl) {
-      auto& L = lists[sl];
-      std::sort(L.begin(), L.end());  // reference accumulation order (network.cpp:298-303)
+      std::sort(lists[sl].begin(), lists[sl].end());  // reference order (network.cpp:298-303)
+      max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
+    }
+    // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step)
+    std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs) * TS, 24 * zero_rec);
+    for (int sl = 0; sl < TS; ++sl) {
+      const auto& L = lists[sl];
       const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
-      for (int f : L) {
-        const int g = 24 * S.gslot_of_fiber[f];
-        ent.push_back(pn == S.tail_pn[f] ? static_cast<int>(g | 0x80000000u) : g);
+      npairs[sl] = static_cast<int>((L.size() + 1) / 2);
+      for (size_t i = 0; i < L.size(); ++i) {
+        const int f = L[i];
+        ent[2 * ((i / 2) * TS + sl) + (i % 2)] =
+            24 * (pn == S.tail_pn[f] ? S.rec_tail[f] : S.rec_head[f]);
       }
-      if (L.size() % 2) ent.push_back(24 * zero_rec);
-      off[sl + 1] = static_cast<int>(ent.size());
     }
     std::vector<int> fab(FS), fg(FS), fid(FS, -1);
     std::vector<double> fl0(FS, 0.5), fea(FS, 1.0);
@@ -687,11 +694,11 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       const int f = S.fiber_of_fslot[fs];
       if (f < 0) {  // dummy: unit segment between the two dummy x records
         fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
-        fg[fs] = 24 * gslot_of_fslot[fs];
+        fg[fs] = (24 * dummy_tail[fs]) | ((24 * dummy_head[fs]) << 16);
         continue;
       }
       fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
-      fg[fs] = 24 * S.gslot_of_fiber[f];
+      fg[fs] = (24 * S.rec_tail[f]) | ((24 * S.rec_head[f]) << 16);
       fid[fs] = f;
       fl0[fs] = P.l0[f];
       fea[fs] = P.ea[f];
@@ -723,8 +730,13 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     if ((rc = up(&E.slot_pn, slot_pn))) return rc;
     if ((rc = up(&E.slot_ref, slot_ref))) return rc;
     if ((rc = up(&E.slot_lump, slot_lump))) return rc;
-    if ((rc = up(&E.csr_off, off))) return rc;
-    if ((rc = up(&E.csr_ent, ent))) return rc;
+    if ((rc = up(&E.csr_npairs, npairs))) return rc;
+    {
+      int* pairs = nullptr;
+      if ((rc = up(&pairs, ent))) return rc;
+      E.csr_pairs = reinterpret_cast<const int2*>(pairs);
+    }
+    E.max_pairs = max_pairs;
     if ((rc = up(&E.fib_ab, fab))) return rc;
     if ((rc = up(&E.fib_g, fg))) return rc;
     if ((rc = up(&E.fib_id, fid))) return rc;

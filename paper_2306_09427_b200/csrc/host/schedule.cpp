@@ -1,7 +1,10 @@
 // Bank-aware placement of an RVE topology onto the DR kernel's CTA (see schedule.hpp).
 #include "schedule.hpp"
 
+#include "fibra_cuda.h"
+
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstdint>
 #include <numeric>
@@ -168,14 +171,15 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
     s.groups_conflicting += conflict;
   }
 
-  // ---- g*d banks: distinct inside each fiber group, min-conflict inside gather steps
-  std::vector<int> beta(M, 0), group_of(M, 0);
+  // ---- g*d records: each fiber writes a tail record (-g*d) and a head record (+g*d), each
+  // read by exactly one gather step.  A record is an edge between its store group (the
+  // half-warp STS instruction that writes it: fiber group x {tail, head}) and its gather
+  // group (half-warp of the reading node x step in that node's list).  Both sides have
+  // degree <= 16, so the bipartite multigraph is 16-edge-colourable (Koenig); colour c
+  // becomes bank 3c mod 16 of the record and every store and gather is conflict-free.
+  std::vector<int> group_of(M, 0);
   for (int g = 0; g < n_groups; ++g)
-    for (int i = 0; i < static_cast<int>(best_groups[g].size()); ++i) {
-      beta[best_groups[g][i]] = i;
-      group_of[best_groups[g][i]] = g;
-    }
-  // incident fibers per node in ascending id -> gather step k of half-warp slot/16
+    for (int f : best_groups[g]) group_of[f] = g;
   std::vector<std::vector<int>> inc_fibers(N);
   for (int f = 0; f < M; ++f) {
     inc_fibers[a_pn[f]].push_back(f);
@@ -184,85 +188,79 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
   int max_deg = 0;
   for (int pn = 0; pn < N; ++pn) max_deg = std::max<int>(max_deg, inc_fibers[pn].size());
   const int n_hw = s.node_slots / kBanks;
-  // gather group id = hw * max_deg + k ; each fiber sits in two of them
-  std::vector<std::array<int, 2>> gg_of(M, {-1, -1});
+  // edges: 2f = tail record, 2f+1 = head record
+  std::vector<int> eL(2 * M), eR(2 * M);
+  for (int f = 0; f < M; ++f) {
+    eL[2 * f] = 2 * group_of[f];
+    eL[2 * f + 1] = 2 * group_of[f] + 1;
+  }
   for (int pn = 0; pn < N; ++pn) {
     const int hw = s.slot_of_pn[pn] / kBanks;
     for (int k = 0; k < static_cast<int>(inc_fibers[pn].size()); ++k) {
       const int f = inc_fibers[pn][k];
-      gg_of[f][gg_of[f][0] < 0 ? 0 : 1] = hw * max_deg + k;
+      eR[2 * f + (pn == s.tail_pn[f] ? 0 : 1)] = hw * max_deg + k;
     }
   }
-  std::vector<std::array<int, kBanks>> cnt(static_cast<size_t>(n_hw) * max_deg);
-  for (auto& c : cnt) c.fill(0);
-  for (int f = 0; f < M; ++f)
-    for (int gg : gg_of[f]) ++cnt[gg][beta[f]];
-  auto move_delta = [&](int f, int to) {  // cost change of moving f's bank to `to`
-    int d = 0;
-    for (int gg : gg_of[f]) d += cnt[gg][to] - (cnt[gg][beta[f]] - 1);
-    if (gg_of[f][0] == gg_of[f][1]) d += 0;  // both endpoints in one step: counted twice
-    return d;
-  };
-  auto apply_move = [&](int f, int to) {
-    for (int gg : gg_of[f]) {
-      --cnt[gg][beta[f]];
-      ++cnt[gg][to];
+  const int nL = 2 * n_groups, nR = n_hw * max_deg;
+  std::vector<std::array<int, kBanks>> atL(nL), atR(nR);  // edge holding colour c, or -1
+  for (auto& x : atL) x.fill(-1);
+  for (auto& x : atR) x.fill(-1);
+  std::vector<int> colour(2 * M, -1);
+  bool perfect = true;
+  for (int e = 0; e < 2 * M; ++e) {
+    const int u = eL[e], v = eR[e];
+    int a = -1, b = -1;
+    for (int c = 0; c < kBanks && a < 0; ++c)
+      if (atL[u][c] < 0) a = c;
+    for (int c = 0; c < kBanks && b < 0; ++c)
+      if (atR[v][c] < 0) b = c;
+    if (a < 0 || b < 0) {  // degree > 16 (cannot happen for <= 16-lane groups)
+      perfect = false;
+      colour[e] = 0;
+      continue;
     }
-    beta[f] = to;
-  };
-  for (int pass = 0; pass < 40; ++pass) {
-    bool improved = false;
-    for (int g = 0; g < n_groups; ++g) {
-      auto& members = best_groups[g];
-      std::array<int, kBanks> owner;
-      owner.fill(-1);
-      for (int f : members) owner[beta[f]] = f;
-      for (int f : members) {
-        int best_to = -1, best_d = 0;
-        for (int to = 0; to < kBanks; ++to) {
-          if (to == beta[f]) continue;
-          int d;
-          const int other = owner[to];
-          if (other < 0) {
-            d = move_delta(f, to);
-          } else {  // swap banks with `other` (keeps the group bank-distinct)
-            const int from = beta[f];
-            d = move_delta(f, to);
-            apply_move(f, to);
-            d += move_delta(other, from);
-            apply_move(f, from);
-          }
-          if (d < best_d) {
-            best_d = d;
-            best_to = to;
-          }
-        }
-        if (best_to >= 0) {
-          const int from = beta[f], other = owner[best_to];
-          apply_move(f, best_to);
-          owner[best_to] = f;
-          owner[from] = other;
-          if (other >= 0) apply_move(other, from);
-          improved = true;
-        }
+    if (atR[v][a] >= 0) {
+      // a is free at u, taken at v; b free at v.  Swap a<->b along the alternating path
+      // that starts at v with colour a; it cannot reach u, after which a is free at v.
+      std::vector<int> path;
+      int node = v, side = 1, c = a;
+      for (;;) {
+        const int pe = side ? atR[node][c] : atL[node][c];
+        if (pe < 0) break;
+        path.push_back(pe);
+        node = side ? eL[pe] : eR[pe];
+        side ^= 1;
+        c = (c == a) ? b : a;
+      }
+      for (int pe : path) {
+        atL[eL[pe]][colour[pe]] = -1;
+        atR[eR[pe]][colour[pe]] = -1;
+      }
+      for (int pe : path) {
+        colour[pe] = (colour[pe] == a) ? b : a;
+        atL[eL[pe]][colour[pe]] = pe;
+        atR[eR[pe]][colour[pe]] = pe;
       }
     }
-    if (!improved) break;
+    colour[e] = a;
+    atL[u][a] = e;
+    atR[v][a] = e;
   }
-  for (const auto& c : cnt) {
-    int mx = 0, tot = 0;
-    for (int v : c) {
-      mx = std::max(mx, v);
-      tot += v;
-    }
-    if (tot) {
-      s.gather_excess += mx - 1;
-      ++s.gather_steps;
-    }
+  s.gather_steps = 0;
+  for (int v = 0; v < nR; ++v) {
+    bool any = false;
+    for (int c = 0; c < kBanks; ++c) any |= atR[v][c] >= 0;
+    s.gather_steps += any;
   }
+  s.gather_excess = perfect ? 0 : -1;
   std::array<int, kBanks> used{};
-  s.gslot_of_fiber.assign(M, -1);
-  for (int f = 0; f < M; ++f) s.gslot_of_fiber[f] = beta[f] + kBanks * used[beta[f]]++;
+  s.rec_tail.assign(M, -1);
+  s.rec_head.assign(M, -1);
+  for (int f = 0; f < M; ++f) {  // record index = colour + 16 * (running count of colour)
+    const int ct = colour[2 * f], ch = colour[2 * f + 1];
+    s.rec_tail[f] = ct + kBanks * used[ct]++;
+    s.rec_head[f] = ch + kBanks * used[ch]++;
+  }
   int mx = 0;
   for (int v : used) mx = std::max(mx, v);
   s.gd_slots = kBanks * std::max(mx, 1);
@@ -270,3 +268,24 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
 }
 
 }  // namespace fibra_b200
+
+// Diagnostics (C-ABI, no GPU needed): schedule quality of one network for a kernel shape.
+extern "C" int fibra_schedule_report(const fibra_net_desc* d, int T, int FPT, int NPT,
+                                     int64_t* out) {
+  const int N = d->n_nodes, M = d->n_fibers;
+  std::vector<int> a(M), b(M);
+  for (int f = 0; f < M; ++f) {
+    a[f] = d->fiber_packed_dofs[6 * f] / 3;
+    b[f] = d->fiber_packed_dofs[6 * f + 3] / 3;
+  }
+  fibra_b200::Schedule s;
+  const bool ok = fibra_b200::build_schedule(N, d->n_free / 3, M, a.data(), b.data(), T, FPT,
+                                             NPT, s);
+  out[0] = ok;
+  out[1] = s.groups_conflicting;
+  out[2] = s.gather_excess;
+  out[3] = s.gather_steps;
+  out[4] = s.gd_slots;
+  out[5] = s.node_slots;
+  return ok ? 0 : 21;
+}

@@ -33,10 +33,10 @@ struct Schedule {
   std::vector<int> slot_of_pn, pn_of_slot;      // node placement (-1 empty)
   std::vector<int> fiber_of_fslot;              // fiber placement (-1 empty)
   std::vector<int> tail_pn, head_pn;            // stored orientation per fiber
-  std::vector<int> gslot_of_fiber;              // g*d record per fiber
+  std::vector<int> rec_tail, rec_head;          // g*d records per fiber (-g*d, +g*d)
   // quality report
   int groups_conflicting = 0;       // fiber groups with a bank conflict on x loads
-  long gather_excess = 0;           // sum over gather steps of (max bank multiplicity - 1)
+  long gather_excess = 0;           // 0 when the record colouring is perfect, -1 otherwise
   long gather_steps = 0;
 };
 
