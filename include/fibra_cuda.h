@@ -115,6 +115,7 @@ typedef struct {          /* RelaxReport relax.hpp:28-36                        
   int64_t iterations;
   double residual, eps_eff, kinetic_fraction, dt;
   int32_t converged;
+  int32_t reserved0;      /* explicit padding, always 0 (records compare bytewise)   */
   double energy_drift;
 } fibra_relax_report;
 
@@ -128,6 +129,7 @@ typedef struct {          /* PointResponse macrofem.hpp:48-51 + Response/Respons
   double stress_asymmetry;
   fibra_relax_report base_report;
   int32_t solves;
+  int32_t reserved1;      /* explicit padding, always 0                              */
   int64_t relax_iterations;
   int32_t failed_probe;
   int32_t status;         /* FIBRA_OK or the point's failure code                    */
@@ -159,6 +161,17 @@ int fibra_cuda_upload_library(fibra_ctx* ctx, const fibra_net_desc* entries, int
  * init_batch (batch.cpp:125-143); offsets are the prefix sums of 3*n_nodes. */
 int fibra_cuda_bind_points(fibra_ctx* ctx, const int32_t* entry_of_point, int32_t n_points);
 int fibra_cuda_reset_states(fibra_ctx* ctx);
+
+/* Order in which the persistent kernel starts base solves (probes always follow base
+ * completion).  Results are independent of it (every solve is computed bit-identically
+ * wherever it runs); only the batch makespan changes.  The reference's WorkerPool takes
+ * points in index order (batch.cpp:160-186), which is FIBRA_SCHED_BATCH.
+ *   FIBRA_SCHED_STRAIN (default): ascending Green-strain norm |F^T F - I|/2 of the base
+ *     point -- small-strain networks are dominated by soft modes and relax longest;
+ *   FIBRA_SCHED_HINT: descending caller cost (e.g. the previous call's relax_iterations
+ *     per point, n_points values, copied); cleared by fibra_cuda_bind_points. */
+enum { FIBRA_SCHED_BATCH = 0, FIBRA_SCHED_STRAIN = 1, FIBRA_SCHED_HINT = 2 };
+int fibra_cuda_set_schedule(fibra_ctx* ctx, int32_t mode, const double* cost_hint);
 /* Warm data host->device: u (total dofs), t, iters, converged (n_points); any may be NULL */
 int fibra_cuda_upload_states(fibra_ctx* ctx, const double* u, const double* t,
                              const int64_t* iters, const uint8_t* converged);

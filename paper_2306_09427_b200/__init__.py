@@ -333,12 +333,15 @@ def _to_result(rec: np.ndarray) -> BatchResult:
         stats.append(ResponseStats(int(r["solves"]), int(r["relax_iterations"]),
                                    int(r["failed_probe"]) if status[p] == 0 else -1))
         br = r["base_report"]
-        reports.append({k: br[k].item() for k in br.dtype.names})
+        reports.append({k: br[k].item() for k in br.dtype.names if not k.startswith("reserved")})
     failed = [int(p) for p in np.nonzero(status)[0]]
     return BatchResult(responses, stats, reports, failed, rec)
 
 
 # ---- device context ---------------------------------------------------------------------
+SCHED_BATCH, SCHED_STRAIN, SCHED_HINT = 0, 1, 2  # fibra_cuda_set_schedule modes
+
+
 class DeviceBatch:
     """A CUDA context holding one RveLibrary in HBM and the PackedStates of one assignment.
 
@@ -370,6 +373,18 @@ class DeviceBatch:
 
     def reset_states(self):
         self._check(self._L.fibra_cuda_reset_states(self._ctx))
+
+    def set_schedule(self, mode: int, cost_hint=None):
+        """Start order of base solves (SCHED_BATCH / SCHED_STRAIN / SCHED_HINT); results do
+        not depend on it, only the makespan does.  ``cost_hint``: one cost per point, larger
+        first (e.g. the previous call's relax_iterations)."""
+        hint = None
+        if mode == SCHED_HINT:
+            hint = np.ascontiguousarray(cost_hint, dtype=np.float64)
+            if hint.shape != (self.n_points,):
+                raise ConfigError("cost_hint needs one value per point")
+        self._check(self._L.fibra_cuda_set_schedule(
+            self._ctx, int(mode), None if hint is None else _ptr(hint, _capi._dp)))
 
     def upload_states(self, st: PackedStates):
         self._check(self._L.fibra_cuda_upload_states(
@@ -497,6 +512,12 @@ class NetworkBatchProvider:
     def respond(self, deformation) -> ProviderResult:
         rec = self._db.solve(deformation, self.law, self.relax_cfg, self.stiff_cfg, True)
         self._dirty = True
+        # the next macro iteration revisits the same points: start the ones that relaxed
+        # longest first (failed relaxations ran to the iteration cap)
+        cost = np.where(rec["status"] == 0, rec["relax_iterations"].astype(np.float64),
+                        np.where(np.isin(rec["status"], (6, 7)),
+                                 7.0 * self.relax_cfg.max_iterations, 0.0))
+        self._db.set_schedule(SCHED_HINT, cost)
         br = _to_result(rec)
         its = int(sum(s.relax_iterations for s in br.stats))
         self.total_solves += int(sum(s.solves for s in br.stats))

@@ -28,6 +28,7 @@ EXPORTS = [
     "fibra_host_last_error", "fibra_assign_random", "fibra_schedule_report",
     "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
+    "fibra_cuda_set_schedule",
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
     "fibra_cuda_solve_device", "fibra_cuda_synchronize", "fibra_cuda_last_stats",
     "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile",
@@ -71,14 +72,15 @@ class StiffCfg(C.Structure):
 class RelaxReport(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("residual", C.c_double), ("eps_eff", C.c_double),
                 ("kinetic_fraction", C.c_double), ("dt", C.c_double),
-                ("converged", C.c_int32), ("energy_drift", C.c_double)]
+                ("converged", C.c_int32), ("reserved0", C.c_int32),
+                ("energy_drift", C.c_double)]
 
 
 class PointResult(C.Structure):
     _fields_ = [("sigma", C.c_double * 6), ("spatial_c", C.c_double * 36),
                 ("pk2", C.c_double * 6), ("material_a", C.c_double * 36),
                 ("stress_asymmetry", C.c_double), ("base_report", RelaxReport),
-                ("solves", C.c_int32), ("relax_iterations", C.c_int64),
+                ("solves", C.c_int32), ("reserved1", C.c_int32), ("relax_iterations", C.c_int64),
                 ("failed_probe", C.c_int32), ("status", C.c_int32)]
 
 
@@ -127,6 +129,7 @@ def load(build_if_missing: bool = True):
         "fibra_cuda_upload_library": (C.c_int, [vp, C.POINTER(NetDesc), C.c_int32]),
         "fibra_cuda_bind_points": (C.c_int, [vp, _ip, C.c_int32]),
         "fibra_cuda_reset_states": (C.c_int, [vp]),
+        "fibra_cuda_set_schedule": (C.c_int, [vp, C.c_int32, _dp]),
         "fibra_cuda_upload_states": (C.c_int, [vp, _dp, _dp, _lp, _bp]),
         "fibra_cuda_download_states": (C.c_int, [vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                                  _lp, _bp]),

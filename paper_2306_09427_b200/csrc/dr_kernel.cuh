@@ -81,7 +81,9 @@ struct DrParams {
   const int* solve_skip;       // nonzero: solve pre-failed by prep (status code)
   SolveOut* out;
   int* base_flag;              // per point: 0 pending, 1 converged, 2 failed
-  int* ticket;
+  const int* order;            // base ticket -> point (longest expected solve first)
+  int* done_list;              // points in base-completion order (-1: not yet)
+  int* ticket;                 // [0] next ticket, [1] done_list fill count
   unsigned long long* counters;  // [0] iterations [1] fiber-iterations [2] pipe ops [3] solves
   double* ckpt;                // [grid][2][6][ck_stride]
   int ck_stride, ck_interval;
@@ -124,6 +126,18 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// a finished base solve publishes its flag, then its point in the completion FIFO from
+// which probe tickets are served
+__device__ __forceinline__ void publish_base(const DrParams& P, int p, int flag) {
+  __threadfence();
+  atomicExch(P.base_flag + p, flag);
+  st_release(P.done_list + atomicAdd(P.ticket + 1, 1), p);
 }
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -206,25 +220,33 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 #define SJ(j) (UEA ? s_uni : fs[j])
 
   for (;;) {
+    // Tickets [0, n) are base solves in P.order; tickets [n, 7n) are probes, served in the
+    // order base solves finish (six per finished base), so a CTA only waits for a base when
+    // every finished base's probes are already taken.  Solve index: base p -> p, probe q of
+    // p -> n + 6p + q (the output layout post_kernel reads).
     if (tid == 0) {
-      const int s = atomicAdd(P.ticket, 1);
-      ctl.solve = s;
-      if (s < P.n_solves) {
-        const int p = s < P.n_points ? s : (s - P.n_points) / 6;
+      const int t = atomicAdd(P.ticket, 1);
+      int s = P.n_solves;
+      if (t < P.n_solves) {
+        int p, q = -1, flag = 1;
+        if (t < P.n_points) {
+          p = P.order[t];
+          s = p;
+        } else {
+          const int k = (t - P.n_points) / 6;
+          q = (t - P.n_points) % 6;
+          while ((p = ld_acquire(P.done_list + k)) < 0) __nanosleep(256);
+          s = P.n_points + 6 * p + q;
+          flag = ld_acquire(P.base_flag + p) == 1;
+        }
+        if (P.solve_skip[s]) flag = 0;
         ctl.point = p;
-        ctl.q = s < P.n_points ? -1 : (s - P.n_points) % 6;
+        ctl.q = q;
         ctl.entry = P.entry_of_point[p];
         ctl.collapse = 0;
-        int flag = 1;
-        if (P.solve_skip[s]) {
-          flag = 0;
-        } else if (ctl.q >= 0) {  // probe: wait for the base solve of its point
-          int f;
-          while ((f = ld_acquire(P.base_flag + p)) == 0) __nanosleep(256);
-          flag = (f == 1);
-        }
         ctl.flag = flag;
       }
+      ctl.solve = s;
     }
     __syncthreads();
     const int s = ctl.solve;
@@ -235,10 +257,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         SolveOut o = {};
         o.status = P.solve_skip[s] ? P.solve_skip[s] : FIBRA_E_NOT_CONVERGED;
         P.out[s] = o;
-        if (q < 0) {
-          __threadfence();
-          atomicExch(P.base_flag + p, 2);
-        }
+        if (q < 0) publish_base(P, p, 2);
       }
       __syncthreads();
       continue;
@@ -734,12 +753,11 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       atomicAdd(P.counters + 3, 1ull);
     }
     if (base_solve) {
+      // every thread wrote part of the converged u its probes warm-start from: each one
+      // fences its own stores before thread 0 publishes
+      __threadfence();
       __syncthreads();
-      if (tid == 0) {
-        const int ok = (P.out[s_].status == FIBRA_OK) ? 1 : 2;
-        __threadfence();
-        atomicExch(P.base_flag + p_, ok);
-      }
+      if (tid == 0) publish_base(P, p_, P.out[s_].status == FIBRA_OK ? 1 : 2);
     }
     __syncthreads();
   }

@@ -26,6 +26,8 @@
 
 namespace fibra_b200 {
 
+static_assert(sizeof(fibra_point_result) == 760, "fibra_point_result ABI layout");
+
 struct PrepOut {
   double R[9];
   double U[6];
@@ -36,13 +38,31 @@ struct PrepOut {
 
 __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangent,
                             double fd_rel_step, PrepOut* prep, double* solve_F, int* solve_skip,
-                            int* base_flag) {
+                            int* base_flag, int* done_list, int sched_mode,
+                            const double* __restrict__ hint, unsigned long long* key) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double f[9];
   for (int i = 0; i < 9; ++i) f[i] = F[9 * p + i];
   PrepOut o = {};
   base_flag[p] = 0;
+  done_list[p] = -1;
+  // schedule key (ascending = started first), unique through the point index in the low word
+  unsigned hi = 0;
+  if (sched_mode == FIBRA_SCHED_STRAIN) {
+    double e2 = 0;  // |F^T F - I|^2, fp64 only for ordering
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double c = f[i] * f[j] + f[3 + i] * f[3 + j] + f[6 + i] * f[6 + j] - (i == j);
+        e2 += c * c;
+      }
+    const float k = static_cast<float>(sqrt(e2));
+    hi = k == k ? __float_as_uint(k) : 0xffffffffu;
+  } else if (sched_mode == FIBRA_SCHED_HINT) {
+    const float k = static_cast<float>(hint[p]);
+    hi = (k == k && k > 0) ? ~__float_as_uint(k) : 0xffffffffu;
+  }
+  key[p] = (static_cast<unsigned long long>(hi) << 32) | static_cast<unsigned>(p);
   if (!polar_decompose(f, o.R, o.U)) {  // KinematicsError -> failed point
     o.status = FIBRA_E_KINEMATICS;
     solve_skip[p] = FIBRA_E_KINEMATICS;
@@ -67,6 +87,23 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
     }
   }
   prep[p] = o;
+}
+
+// order[rank of key[p]] = p (keys are unique): a counting rank, O(n^2 / 256) smem compares,
+// a few microseconds at thousands of points
+__global__ void rank_kernel(int n, const unsigned long long* __restrict__ key, int* order) {
+  __shared__ unsigned long long tile[256];
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long k = p < n ? key[p] : 0;
+  int rank = 0;
+  for (int b = 0; b < n; b += 256) {
+    __syncthreads();
+    if (b + static_cast<int>(threadIdx.x) < n) tile[threadIdx.x] = key[b + threadIdx.x];
+    __syncthreads();
+    const int m = min(256, n - b);
+    for (int j = 0; j < m; ++j) rank += tile[j] < k;
+  }
+  if (p < n) order[rank] = p;
 }
 
 // homogenized_stress (network.cpp:341-372) from the boundary moment sums of a converged
@@ -269,6 +306,8 @@ struct fibra_ctx {
   double* d_state[8] = {};  // u v a f_int f_damp mass inv_mass t
   long long* d_iters = nullptr;
   unsigned char* d_conv = nullptr;
+  int sched_mode = FIBRA_SCHED_STRAIN;
+  double* d_hint = nullptr;  // FIBRA_SCHED_HINT costs (n_points)
   // per-call scratch
   int cap_points = 0;
   double* d_F = nullptr;
@@ -277,6 +316,9 @@ struct fibra_ctx {
   PrepOut* d_prep = nullptr;
   SolveOut* d_out = nullptr;
   int* d_flag = nullptr;
+  int* d_done = nullptr;
+  int* d_order = nullptr;
+  unsigned long long* d_key = nullptr;
   fibra_point_result* d_res = nullptr;
   double* h_F = nullptr;                 // pinned staging
   fibra_point_result* h_res = nullptr;   // pinned staging
@@ -318,6 +360,9 @@ void free_points(fibra_ctx* c) {
   for (auto& p : c->d_state) cudaFree(p), p = nullptr;
   cudaFree(c->d_iters);
   cudaFree(c->d_conv);
+  cudaFree(c->d_hint);
+  c->d_hint = nullptr;
+  if (c->sched_mode == FIBRA_SCHED_HINT) c->sched_mode = FIBRA_SCHED_STRAIN;
   c->d_entry_of_point = nullptr;
   c->d_offsets = nullptr;
   c->d_iters = nullptr;
@@ -332,11 +377,15 @@ void free_scratch(fibra_ctx* c) {
   cudaFree(c->d_prep);
   cudaFree(c->d_out);
   cudaFree(c->d_flag);
+  cudaFree(c->d_done);
+  cudaFree(c->d_order);
+  cudaFree(c->d_key);
   cudaFree(c->d_res);
   cudaFreeHost(c->h_F);
   cudaFreeHost(c->h_res);
   c->d_F = c->d_solveF = nullptr;
-  c->d_skip = c->d_flag = nullptr;
+  c->d_skip = c->d_flag = c->d_done = c->d_order = nullptr;
+  c->d_key = nullptr;
   c->d_prep = nullptr;
   c->d_out = nullptr;
   c->d_res = nullptr;
@@ -365,6 +414,9 @@ int ensure_scratch(fibra_ctx* c, int n) {
   if ((rc = dalloc(c, &c->d_prep, n))) return rc;
   if ((rc = dalloc(c, &c->d_out, ns))) return rc;
   if ((rc = dalloc(c, &c->d_flag, n))) return rc;
+  if ((rc = dalloc(c, &c->d_done, n))) return rc;
+  if ((rc = dalloc(c, &c->d_order, n))) return rc;
+  if ((rc = dalloc(c, &c->d_key, n))) return rc;
   if ((rc = dalloc(c, &c->d_res, n))) return rc;
   FB_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_F), 9 * sizeof(double) * n));
   FB_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res), sizeof(fibra_point_result) * n));
@@ -442,6 +494,8 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.solve_skip = c->d_skip;
   P.out = c->d_out;
   P.base_flag = c->d_flag;
+  P.order = c->d_order;
+  P.done_list = c->d_done;
   P.ticket = c->d_ticket;
   P.counters = c->d_counters;
   P.ckpt = c->d_ckpt;
@@ -476,11 +530,14 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
 
   cudaStream_t st = c->stream;
   FB_CUDA(c, cudaEventRecord(c->ev[0], st));
-  FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, sizeof(int), st));
+  FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(int), st));
   FB_CUDA(c, cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), st));
   const int tb = 128;
   prep_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, sc ? sc->fd_rel_step : 1e-5,
-                                                c->d_prep, c->d_solveF, c->d_skip, c->d_flag);
+                                                c->d_prep, c->d_solveF, c->d_skip, c->d_flag,
+                                                c->d_done, c->sched_mode, c->d_hint, c->d_key);
+  FB_CUDA(c, cudaGetLastError());
+  rank_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c->d_key, c->d_order);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
   fn<<<grid, v->T, smem, st>>>(P);
@@ -491,7 +548,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[3], st));
   c->last_solves = n_solves;
-  c->last_launches = 3;
+  c->last_launches = 4;
   return FIBRA_OK;
 }
 
@@ -558,7 +615,7 @@ int fibra_cuda_open(int device, fibra_ctx** out) {
   c->n_sm = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
-  if (cudaMalloc(&c->d_ticket, sizeof(int)) != cudaSuccess) return bail(FIBRA_E_CUDA);
+  if (cudaMalloc(&c->d_ticket, 2 * sizeof(int)) != cudaSuccess) return bail(FIBRA_E_CUDA);
   if (cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
   for (auto& e : c->ev)
@@ -787,6 +844,27 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   }
   FB_CUDA(c, cudaMemcpy(c->d_offsets, c->offsets.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice));
   return fibra_cuda_reset_states(c);
+}
+
+int fibra_cuda_set_schedule(fibra_ctx* c, int32_t mode, const double* cost_hint) {
+  if (!c) return FIBRA_E_ARG;
+  if (mode != FIBRA_SCHED_BATCH && mode != FIBRA_SCHED_STRAIN && mode != FIBRA_SCHED_HINT)
+    return set_err(c, FIBRA_E_ARG, "unknown schedule mode");
+  if (mode == FIBRA_SCHED_HINT) {
+    if (!cost_hint) return set_err(c, FIBRA_E_ARG, "FIBRA_SCHED_HINT needs cost_hint");
+    if (c->offsets.empty()) return set_err(c, FIBRA_E_ARG, "bind_points first");
+    FB_CUDA(c, cudaSetDevice(c->device));
+    FB_CUDA(c, cudaStreamSynchronize(c->stream));
+    const size_t n = std::max(c->n_points, 1);
+    if (!c->d_hint) {
+      int rc;
+      if ((rc = dalloc(c, &c->d_hint, n))) return rc;
+    }
+    if (c->n_points)
+      FB_CUDA(c, cudaMemcpy(c->d_hint, cost_hint, sizeof(double) * c->n_points, cudaMemcpyHostToDevice));
+  }
+  c->sched_mode = mode;
+  return FIBRA_OK;
 }
 
 int fibra_cuda_reset_states(fibra_ctx* c) {

@@ -95,6 +95,35 @@ def test_batch_tangent_bitwise(small_lib):
     check_states(st, ost)
 
 
+def test_schedule_modes_bitwise(small_lib):
+    """The start order of base solves (and the completion-order probe FIFO) changes nothing:
+    batch order, strain order and a caller hint give identical records and states, with a
+    failed point (collapse) and a kinematics failure mixed in."""
+    pnets, _ = small_lib
+    lib = P.RveLibrary(pnets)
+    n = 40
+    F = batch_F(n)
+    F[5] = np.diag([1e-9, 1e-9, 1e-9])
+    F[17] = np.diag([-1.0, 1.0, 1.0])
+    F[23] = np.eye(3)
+    outs = []
+    for mode, hint in ((P.SCHED_BATCH, None), (P.SCHED_STRAIN, None),
+                       (P.SCHED_HINT, np.arange(n, dtype=np.float64) % 7)):
+        st, assign = P.init_batch(np.zeros(n, np.int32), lib, 3)
+        db = P.DeviceBatch(lib, assign)
+        db.set_schedule(mode, hint)
+        rec = db.solve(F, want_tangent=True)
+        db.download_states(st)
+        db.close()
+        outs.append((rec, st))
+    r0, s0 = outs[0]
+    assert sorted(np.nonzero(r0["status"])[0].tolist()) == [5, 17]
+    for rec, st in outs[1:]:
+        assert rec.tobytes() == r0.tobytes()
+        for k in STATE_KEYS:
+            assert same_bits(getattr(st, k), getattr(s0, k)), k
+
+
 def test_failed_points_reported(small_lib):
     pnets, _ = small_lib
     lib = P.RveLibrary(pnets)
