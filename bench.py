@@ -211,7 +211,7 @@ def main():
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
-    total_ms, dr_ms, iters, pipe_ops, fiber_iters, failed = 0.0, 0.0, 0, 0, 0, 0
+    total_ms, dr_ms, iters, pipe_ops, fiber_iters, failed, launches = 0.0, 0.0, 0, 0, 0, 0, 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.start()
     for _ in range(args.steps):
@@ -230,6 +230,7 @@ def main():
         iters += s["iterations"]
         pipe_ops += s["pipe_ops"]
         fiber_iters += s["fiber_iterations"]
+        launches += s["kernel_launches"]
     clk = clocks.stop()
     rec = np.frombuffer(out_dev.cpu().numpy().tobytes(), dtype=P.RESULT_DTYPE)
     failed = int((rec["status"] != 0).sum())
@@ -290,7 +291,7 @@ def main():
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": launches,
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
