@@ -171,6 +171,12 @@ int fibra_cuda_reset_states(fibra_ctx* ctx);
  *   FIBRA_SCHED_HINT: descending caller cost (e.g. the previous call's relax_iterations
  *     per point, n_points values, copied); cleared by fibra_cuda_bind_points. */
 enum { FIBRA_SCHED_BATCH = 0, FIBRA_SCHED_STRAIN = 1, FIBRA_SCHED_HINT = 2 };
+
+/* Diagnostics: the kernel shape library entry `entry` was assigned by upload_library.
+ * out[4] = {cluster size C (1: resident one-CTA kernel), threads per CTA, fibers per
+ * thread, nodes per thread}.  RVEs beyond one CTA's shared memory (about 1.3k fibers) run
+ * on a thread-block cluster of C = 2..16 CTAs (csrc/dr_cluster.cuh). */
+int fibra_cuda_entry_kernel(const fibra_ctx* ctx, int32_t entry, int32_t* out);
 int fibra_cuda_set_schedule(fibra_ctx* ctx, int32_t mode, const double* cost_hint);
 /* Warm data host->device: u (total dofs), t, iters, converged (n_points); any may be NULL */
 int fibra_cuda_upload_states(fibra_ctx* ctx, const double* u, const double* t,

@@ -374,6 +374,14 @@ class DeviceBatch:
     def reset_states(self):
         self._check(self._L.fibra_cuda_reset_states(self._ctx))
 
+    def entry_kernel(self, entry: int) -> dict:
+        """Kernel shape of a library entry: cluster size (1 = one CTA per RVE) and per-CTA
+        threads / fibers per thread / nodes per thread."""
+        out = np.zeros(4, np.int32)
+        self._check(self._L.fibra_cuda_entry_kernel(self._ctx, int(entry), _ptr(out, _capi._ip)))
+        return {"cluster": int(out[0]), "threads": int(out[1]), "fibers_per_thread": int(out[2]),
+                "nodes_per_thread": int(out[3])}
+
     def set_schedule(self, mode: int, cost_hint=None):
         """Start order of base solves (SCHED_BATCH / SCHED_STRAIN / SCHED_HINT); results do
         not depend on it, only the makespan does.  ``cost_hint``: one cost per point, larger

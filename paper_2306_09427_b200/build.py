@@ -14,6 +14,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -22,12 +23,18 @@ PROF = bool(os.environ.get("FIBRA_PHASE_PROF"))
 LIB = os.path.join(LIB_DIR, "libfibra_b200_prof.so" if PROF else "libfibra_b200.so")
 SOURCES = [
     os.path.join(HERE, "csrc", "fibra_cuda.cu"),
+    os.path.join(HERE, "csrc", "kernels_resident.cu"),
+    os.path.join(HERE, "csrc", "kernels_cluster.cu"),
     os.path.join(HERE, "csrc", "host", "network.cpp"),
     os.path.join(HERE, "csrc", "host", "netgen.cpp"),
     os.path.join(HERE, "csrc", "host", "schedule.cpp"),
+    os.path.join(HERE, "csrc", "host", "cluster_schedule.cpp"),
 ]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "dr_kernel.cuh"),
+    os.path.join(HERE, "csrc", "dr_cluster.cuh"),
+    os.path.join(HERE, "csrc", "variants.hpp"),
+    os.path.join(HERE, "csrc", "host", "cluster_schedule.hpp"),
     os.path.join(HERE, "csrc", "tensor.cuh"),
     os.path.join(HERE, "csrc", "fastmath.cuh"),
     os.path.join(HERE, "csrc", "host", "host_internal.hpp"),
@@ -46,21 +53,36 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object (in parallel), then link the library."""
     if not force and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
-    cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "--fmad=false", "-lineinfo",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
-           *(["-DFIBRA_PHASE_PROF=1"] if PROF else []),
-           "-shared", "-o", LIB + ".tmp", *SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    obj_dir = os.path.join(LIB_DIR, "obj_prof" if PROF else "obj")
+    os.makedirs(obj_dir, exist_ok=True)
+    flags = ["-O3", "-std=c++17", *ARCH, "--fmad=false", "-lineinfo",
+             "-Xptxas", "-v" if verbose else "-O3",
+             "-Xcompiler", "-fPIC,-ffp-contract=off,-O3",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(HERE, "csrc"),
+             *(["-DFIBRA_PHASE_PROF=1"] if PROF else [])]
+    objs = [os.path.join(obj_dir, os.path.basename(src) + ".o") for src in SOURCES]
+
+    def compile_one(args):
+        src, obj = args
+        return subprocess.run([NVCC, *flags, "-c", "-o", obj, src], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, zip(SOURCES, objs)))
+    for r in results:
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc build of libfibra_b200.so failed")
+        if verbose:
+            sys.stderr.write(r.stderr)
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs],
+                       capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libfibra_b200.so failed")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("link of libfibra_b200.so failed")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

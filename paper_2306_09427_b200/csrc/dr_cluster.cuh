@@ -1,0 +1,705 @@
+// Cluster dynamic-relaxation kernel: one thread-block cluster of C CTAs solves one large
+// RVE at a time (RVEs that do not fit one CTA's shared memory; configs 3 and 4).
+//
+// Same reference path and the same bitwise contract as dr_kernel.cuh (relax.cpp:93-191,
+// network.cpp:254-372, kernels_scalar.cpp:7-65).  The RVE is split by
+// host/cluster_schedule.cpp; per DR iteration every CTA runs
+//   fiber phase: its owned fibers read x of their tail (own node) and head (own node or a
+//                halo copy) from local shared memory, store +g*d into their local record
+//                and, if the head lives in another CTA, into that CTA's record
+//                (st.shared::cluster);
+//   barrier.cluster
+//   node phase:  its nodes gather their CSR lists from local records (tail incidences
+//                negated through the entry's sign bit, ascending fiber id), apply the damped
+//                update, write x locally and push it to the halo slots of the CTAs that read
+//                it;
+//   barrier.cluster
+// Cluster-wide quantities stay exact and use no DSMEM atomics (64-bit shared-memory min is a
+// CAS emulation that is not atomic against another CTA's remote access): every warp pushes
+// its CFL minimum into its own slot in every CTA and each warp takes the min over all slots
+// (order independent); the convergence verdict is formed from
+// per-CTA partial sums that every CTA pushes to every CTA, so all CTAs take the identical
+// decision two passes late; at a stop the force vector goes to a per-cluster global
+// scratch in packed order and each CTA evaluates the reference-order 4-lane sums
+// (kernels_scalar.cpp:34-48) itself.  Checkpoint/replay is per CTA as in dr_kernel.cuh.
+#pragma once
+
+#include <cstddef>
+
+#include "dr_kernel.cuh"
+
+namespace fibra_b200 {
+
+struct PartDev {            // one CTA's share of one RVE
+  int f0, node_slots, halo, max_pairs;
+  int max_push, n_records, pad0, pad1;
+  const int* slot_pn;       // [TS] packed node id, -1 empty
+  const double* slot_ref;   // [3 TS]
+  const double* slot_lump;  // [TS]
+  const int* csr_npairs;    // [TS]
+  const int2* csr_pairs;    // [max_pairs][TS] byte offset of a local record | 1u<<31 negate
+  const int* push_n;        // [TS] halo copies of this slot's x
+  const int* push_dst;      // [max_push][TS] rank << 16 | byte offset of the halo x record
+  const int* fib_ab;        // [FS] x byte offsets: tail | head << 16 (own or halo slot)
+  const int* fib_gt;        // [FS] byte offset of the fiber's local record
+  const int* fib_gh;        // [FS] rank << 24 | byte offset of its record in the head's CTA, -1
+  const int* fib_id;        // [FS] reference fiber id, -1 dummy
+  const double* fib_l0;     // [FS]
+  const double* fib_ea;     // [FS]
+  const double* fib_lt;     // [FS] lumping weight of the tail node
+  const double* fib_lh;     // [FS] lumping weight of the head node
+};
+
+struct ClusterEntryDev {
+  int n_nodes, n_fibers, n_free_nodes, n_fix_nodes;
+  double max_lump, max_ea, box_volume, ea0;
+  const PartDev* parts;     // [C]
+  const void* pad;
+};
+
+struct ClusterParams {
+  DrParams d;
+  const ClusterEntryDev* centries;
+  double* scratch;          // per cluster: SF[3N] | SX[3N] | SW[3 NFN] | SE[M]
+  long long scratch_stride;
+  int push_cap;             // push_dst ints staged in shared memory
+  int pad;
+};
+
+struct __align__(16) ClusterCtl {
+  int solve, point, q, entry;
+  int flag, collapse, dec, pad0;
+  double ck_t[2], ck_dt[2];
+  double warp_min[32];
+  double ex[12];
+  double t, force_floor;
+  double part[2][16][2];       // [pass & 1][rank] partial |f|^2 (free, fixed)
+  double wmin[16 * 16];        // [rank * NW + warp] CFL minima of every warp of the cluster
+};
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_id() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ unsigned sh_addr(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ unsigned cl_map(unsigned a, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st_f64(unsigned a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st_s32(unsigned a, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// min over the n cluster-wide warp slots, evaluated by one warp (every lane gets it)
+__device__ __forceinline__ double slots_min(const double* w, int n, int lane) {
+  double m = INFINITY;
+  for (int i = lane; i < n; i += 32) m = smin(m, w[i]);
+  return warp_min(m);
+}
+
+template <int T, int FPT, int NPT, int LAW, bool UEA>
+__global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ ClusterCtl ctl;
+  const DrParams& P = CP.d;
+  constexpr int NW = T / 32;
+  constexpr int TS = NPT * T;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = cl_rank(), C = cl_size();
+
+  // shared layout: [X: own slots | 2 dummy | halo][G: records][SPART][CSR pairs][push list]
+  unsigned char* X = smem;
+  unsigned char* G = smem + P.x_bytes;
+  double* spart = reinterpret_cast<double*>(G + P.g_bytes);
+  int2* cent = reinterpret_cast<int2*>(spart + TS);
+  int* pushd = reinterpret_cast<int*>(cent + P.csr_cap);
+  double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
+  double* scr = CP.scratch + static_cast<size_t>(cl_id()) * CP.scratch_stride;
+  const unsigned X_sh = sh_addr(X), G_sh = sh_addr(G), ctl_sh = sh_addr(&ctl);
+  const unsigned off_solve = offsetof(ClusterCtl, solve), off_collapse = offsetof(ClusterCtl, collapse);
+  const unsigned off_part = offsetof(ClusterCtl, part);
+  const unsigned off_wmin = offsetof(ClusterCtl, wmin) + 8 * (rank * NW + warp);  // my warp's slot
+  // push this warp's CFL minimum into its slot of every CTA (lane r -> CTA r)
+  auto push_wmin = [&](double v) {
+    if (lane < static_cast<int>(C)) cl_st_f64(cl_map(ctl_sh + off_wmin, lane), v);
+  };
+
+  const double B = P.nonlinearity;
+  const int bo = P.law_buckling_off;
+
+  int fab[FPT], fgt[FPT], fgh[FPT];
+  double fl0[FPT], fs[FPT], fmred[FPT];
+  int npair[NPT], npush[NPT];
+  double nref[NPT][3], ninv[NPT], ncm[NPT];
+  int cur_entry = -1;
+  double s_uni = 0;
+#define SJ(j) (UEA ? s_uni : fs[j])
+
+  cl_sync();  // every CTA of the cluster is running before any DSMEM access
+
+  for (;;) {
+    // ---- ticket (rank 0), broadcast into every CTA's control block ----
+    if (rank == 0 && tid == 0) {
+      const int t = atomicAdd(P.ticket, 1);
+      int s = -1, p = 0, q = -1, flag = 0, e = 0;
+      if (t < P.n_solves) {
+        flag = 1;
+        if (t < P.n_class) {
+          p = P.order[t];
+          s = p;
+        } else {
+          const int kk = (t - P.n_class) / 6;
+          q = (t - P.n_class) % 6;
+          while ((p = ld_acquire(P.done_list + kk)) < 0) __nanosleep(256);
+          s = P.n_points + 6 * p + q;
+          flag = ld_acquire(P.base_flag + p) == 1;
+        }
+        if (P.solve_skip[s]) flag = 0;
+        e = P.entry_of_point[p];
+      }
+      for (unsigned r = 0; r < C; ++r) {
+        const unsigned a = cl_map(ctl_sh + off_solve, r);
+        cl_st_s32(a, s);
+        cl_st_s32(a + 4, p);
+        cl_st_s32(a + 8, q);
+        cl_st_s32(a + 12, e);
+        cl_st_s32(a + 16, flag);
+      }
+    }
+    cl_sync();
+    const int s = ctl.solve;
+    if (s < 0) break;
+    const int p = ctl.point, q = ctl.q, e = ctl.entry;
+    if (!ctl.flag) {
+      if (rank == 0 && tid == 0) {
+        SolveOut o = {};
+        o.status = P.solve_skip[s] ? P.solve_skip[s] : FIBRA_E_NOT_CONVERGED;
+        P.out[s] = o;
+        if (q < 0) publish_base(P, p, 2);
+      }
+      cl_sync();
+      continue;
+    }
+
+    const ClusterEntryDev& E = CP.centries[e];
+    const PartDev& Q = E.parts[rank];
+    const double scale = P.density_scale / E.max_lump;  // setup_mass relax.cpp:35-43
+    const int F0 = Q.f0, NSLOT = Q.node_slots;
+    if (e != cur_entry) {
+      cur_entry = e;
+      s_uni = P.ea_scale * E.ea0;
+      for (int i = tid; i < Q.max_pairs * TS; i += T) cent[i] = Q.csr_pairs[i];
+      for (int i = tid; i < Q.max_push * TS; i += T) pushd[i] = Q.push_dst[i];
+      for (int i = tid; i < TS; i += T) spart[i] = 0.0;
+      if (tid < 6) sm_at<double>(X, 24 * TS)[tid] = (tid == 3) ? 1.0 : 0.0;
+      if (tid < 3) sm_at<double>(G, 24 * (Q.n_records - 1))[tid] = 0.0;
+#pragma unroll
+      for (int j = 0; j < FPT; ++j) {
+        const int f = j * T + tid;
+        fab[j] = Q.fib_ab[f];
+        fgt[j] = Q.fib_gt[f];
+        fgh[j] = Q.fib_gh[f];
+        fl0[j] = Q.fib_l0[f];
+        if (!UEA) fs[j] = P.ea_scale * Q.fib_ea[f];
+      }
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int sl = j * T + tid;
+        npair[j] = Q.csr_npairs[sl];
+        npush[j] = Q.push_n[sl];
+        nref[j][0] = Q.slot_ref[3 * sl];
+        nref[j][1] = Q.slot_ref[3 * sl + 1];
+        nref[j][2] = Q.slot_ref[3 * sl + 2];
+      }
+    }
+    auto push_x = [&](int j, int sl, double x0, double x1, double x2) {
+      for (int h = 0; h < npush[j]; ++h) {
+        const int d = pushd[h * TS + sl];
+        const unsigned a = cl_map(X_sh + (d & 0xffff), static_cast<unsigned>(d) >> 16);
+        cl_st_f64(a, x0);
+        cl_st_f64(a + 8, x1);
+        cl_st_f64(a + 16, x2);
+      }
+    };
+
+    // ---- per-solve setup (relax.cpp:95-145) ----
+    double Fm[9];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Fm[i] = P.solve_F[9 * s + i];
+    const long long off = P.offsets[p];
+    const bool is_base = q < 0;
+    double lmin = INFINITY;
+#pragma unroll
+    for (int j = 0; j < FPT; ++j) {  // reduced_mass_l0 relax.cpp:46-55
+      const int ta = (fab[j] & 0xffff) / 24;
+      if (ta < TS) {
+        const double ma = Q.fib_lt[j * T + tid] * scale;
+        const double mb = Q.fib_lh[j * T + tid] * scale;
+        fmred[j] = ma * mb / (ma + mb) * fl0[j];
+      } else {
+        fmred[j] = INFINITY;  // dummy fiber
+      }
+      if (LAW == 0) {
+        const double kt = smax(fabs(law_tangent<0>(SJ(j), 1.0, 0, B)), SJ(j));
+        lmin = smin(lmin, fmred[j] / kt);
+      }
+    }
+    double u[NPT][3], vh[NPT][3];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      const int sl = j * T + tid;
+      const int pn = Q.slot_pn[sl];
+      const double m = Q.slot_lump[sl] * scale;
+      ninv[j] = 1.0 / m;
+      ncm[j] = P.damping * m;
+      if (sl < F0) {
+        if (pn < 0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
+        } else if (is_base) {  // WarmStart::reuse (stiffness.cpp:157)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) u[j][c] = P.u[off + 3 * pn + c];
+        } else if (P.reuse_warm) {  // probe: copy of the converged base u (:100-101)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) u[j][c] = __ldcg(P.u + off + 3 * pn + c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
+        }
+      } else {  // affine BC (network.cpp:254-269), Def3::apply tensor.cpp:58-62
+        const double X0 = nref[j][0], X1 = nref[j][1], X2 = nref[j][2];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double fx = Fm[3 * c] * X0 + Fm[3 * c + 1] * X1 + Fm[3 * c + 2] * X2;
+          u[j][c] = fx - nref[j][c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) vh[j][c] = 0.0;
+      double* xr = sm_at<double>(X, 24 * sl);
+      xr[0] = nref[j][0] + u[j][0];
+      xr[1] = nref[j][1] + u[j][1];
+      xr[2] = nref[j][2] + u[j][2];
+      push_x(j, sl, xr[0], xr[1], xr[2]);
+      if (sl < F0) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          ckpt[c * P.ck_stride + sl] = u[j][c];
+          ckpt[(3 + c) * P.ck_stride + sl] = 0.0;
+        }
+      }
+    }
+    if (tid == 0) {
+      ctl.t = is_base ? P.t[p] : 0.0;
+      ctl.ck_t[0] = ctl.t;
+      ctl.ck_dt[0] = 0.0;
+      ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
+      ctl.collapse = 0;
+    }
+    if (LAW == 0) push_wmin(warp_min(lmin));
+    const bool det_ok = det3(Fm) > 0;
+    cl_sync();  // halo x, CFL minima, control block resets
+    double dt_const = 0;
+    if (LAW == 0) dt_const = P.dt_safety * sqrt(slots_min(ctl.wmin, C * NW, lane));
+    cl_sync();  // wmin consumed before the first fiber phase overwrites it
+
+    int k = 0;
+    int target = -1;
+    int decided = -1;  // last pass whose exact verdict said "continue" (near tie)
+    double dt_k = 0;
+    int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
+    int conv = 0;
+
+    while (status == FIBRA_OK) {
+      // ================= fiber phase (force pass k) =================
+      if (warp == NW - 1) {  // reducer warp: owns no fibers
+        if (LAW != 0) push_wmin(INFINITY);
+        if (target < 0 && k >= 1) {
+          double sf = 0, sfix = 0;  // partials of pass k-1 -> every CTA
+          for (int i = lane; i < F0; i += 32) sf += spart[i];
+          for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
+          sf = warp_sum(sf);
+          sfix = warp_sum(sfix);
+          if (lane < static_cast<int>(C)) {
+            const unsigned a = cl_map(ctl_sh + off_part + ((k - 1) & 1) * 256 + rank * 16, lane);
+            cl_st_f64(a, sf);
+            cl_st_f64(a + 8, sfix);
+          }
+          if (k - 2 > decided && lane == 0) {  // verdict for pass k-2 (rank order, every CTA)
+            double tf = 0, tx = 0;
+            for (unsigned r = 0; r < C; ++r) {
+              tf += ctl.part[(k - 2) & 1][r][0];
+              tx += ctl.part[(k - 2) & 1][r][1];
+            }
+            const double res = sqrt(tf);
+            const double eps = P.tolerance * smax(sqrt(tx), ctl.force_floor);
+            int d = (res <= eps) ? kDecConv : 0;
+            if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
+            else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
+            ctl.dec = d;
+          }
+        }
+      } else {
+        double kmin = INFINITY;
+        bool collapsed = false, fast = true;
+        double dx[FPT], dy[FPT], dz[FPT], g[FPT];
+#pragma unroll
+        for (int j = 0; j < FPT; ++j) {
+          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
+          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+          dx[j] = xb_[0] - xa_[0];
+          dy[j] = xb_[1] - xa_[1];
+          dz[j] = xb_[2] - xa_[2];
+          bool o1, o2, o3 = true;
+          const double len = sqrt_fast(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j], o1);
+          collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
+          const double stretch = div_fast(len, fl0[j], o2);
+          if (LAW == 0) {
+            g[j] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+          } else {
+            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
+            kmin = smin(kmin, fmred[j] / kt);
+          }
+          fast = fast && o1 && o2 && o3;
+        }
+        if (!__all_sync(0xffffffffu, fast)) {
+#pragma unroll
+          for (int j = 0; j < FPT; ++j) {
+            const double len = sqrt(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j]);
+            const double stretch = len / fl0[j];
+            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < FPT; ++j) {  // +g*d: the tail gathers it negated
+          const double g0 = g[j] * dx[j], g1 = g[j] * dy[j], g2 = g[j] * dz[j];
+          double* gt = sm_at<double>(G, fgt[j]);
+          gt[0] = g0;
+          gt[1] = g1;
+          gt[2] = g2;
+          if (fgh[j] >= 0) {
+            const unsigned a = cl_map(G_sh + (fgh[j] & 0xffffff), static_cast<unsigned>(fgh[j]) >> 24);
+            cl_st_f64(a, g0);
+            cl_st_f64(a + 8, g1);
+            cl_st_f64(a + 16, g2);
+          }
+        }
+        if (collapsed)
+          for (unsigned r = 0; r < C; ++r) cl_st_s32(cl_map(ctl_sh + off_collapse, r), 1);
+        if (LAW != 0) push_wmin(warp_min(kmin));
+      }
+      cl_sync();
+
+      // ================= node phase (pass k) =================
+      if (target < 0 && k - 2 > decided) {
+        const int d = ctl.dec;
+        if ((d & (kDecConv | kDecExact)) || k - 2 == P.max_iterations) {
+          target = k - 2;  // replay from the newest checkpoint at or before it
+          k = target / kCkInterval * kCkInterval;
+          const int b = (k / kCkInterval) & 1;
+          dt_k = ctl.ck_dt[b];
+          const double* ck = ckpt + b * 6 * P.ck_stride;
+#pragma unroll
+          for (int j = 0; j < NPT; ++j) {
+            const int sl = j * T + tid;
+            if (sl < F0) {
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                u[j][c] = __ldcg(ck + c * P.ck_stride + sl);
+                vh[j][c] = __ldcg(ck + (3 + c) * P.ck_stride + sl);
+              }
+              double* xr = sm_at<double>(X, 24 * sl);
+              xr[0] = nref[j][0] + u[j][0];
+              xr[1] = nref[j][1] + u[j][1];
+              xr[2] = nref[j][2] + u[j][2];
+              push_x(j, sl, xr[0], xr[1], xr[2]);
+            }
+          }
+          if (tid == 0) {
+            ctl.t = ctl.ck_t[b];
+            ctl.collapse = 0;
+          }
+          cl_sync();
+          continue;
+        }
+      }
+      if (k >= 1) {  // commit iteration k (relax.cpp:150-153)
+        if (!isfinite(dt_k) || !(dt_k > 0)) {
+          status = FIBRA_E_BAD_DT;
+          break;
+        }
+        if (tid == 0) ctl.t += dt_k;
+      }
+      if (ctl.collapse) {
+        status = FIBRA_E_COLLAPSE;
+        break;
+      }
+      const double h_k = 0.5 * dt_k;
+      double fk[NPT][3];
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int sl = j * T + tid;
+        double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
+        for (int kp = 0; kp < npair[j]; ++kp) {
+          const int2 ep = cent[kp * TS + sl];
+          const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);
+          const double* g1 = sm_at<double>(G, ep.y & 0x7fffffff);
+          const double a0 = signed_by(g0[0], ep.x), a1 = signed_by(g0[1], ep.x);
+          const double a2 = signed_by(g0[2], ep.x);
+          const double b0 = signed_by(g1[0], ep.y), b1 = signed_by(g1[1], ep.y);
+          const double b2 = signed_by(g1[2], ep.y);
+          f0 = f0 + a0;  // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
+          f1 = f1 + a1;
+          f2 = f2 + a2;
+          f0 = f0 + b0;
+          f1 = f1 + b1;
+          f2 = f2 + b2;
+        }
+        fk[j][0] = f0;
+        fk[j][1] = f1;
+        fk[j][2] = f2;
+        spart[sl] = f0 * f0 + f1 * f1 + f2 * f2;
+      }
+      if (k == target) {
+        // ---- exact verdict at the target pass: f to the cluster scratch, packed order ----
+        const int NFN = E.n_free_nodes, NFIX = E.n_fix_nodes;
+        double* SF = scr;
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+          const int pn = Q.slot_pn[j * T + tid];
+          if (pn >= 0)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) SF[3 * pn + c] = fk[j][c];
+        }
+        __threadfence();
+        cl_sync();
+        if (tid < 8) {
+          const int base = tid < 4 ? 0 : 3 * NFN;
+          const int len = tid < 4 ? 3 * NFN : 3 * NFIX;
+          double acc = 0;
+          for (int i = tid & 3; i < len; i += 4) {
+            const double v = __ldcg(SF + base + i);
+            acc += v * v;
+          }
+          ctl.ex[tid] = acc;
+        }
+        __syncthreads();
+        const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
+        const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
+        const double eps = P.tolerance * smax(react, ctl.force_floor);
+        __syncthreads();
+        const bool nonfinite = k >= 1 && !isfinite(res);
+        conv = res <= eps;
+        if (nonfinite || conv || k == P.max_iterations) {
+          if (nonfinite) {
+            status = FIBRA_E_DIVERGED;
+            break;
+          }
+          // final state of iteration k -> cluster scratch and (base) PackedStates
+          double* SX = scr + 3 * E.n_nodes;
+          double* SW = SX + 3 * E.n_nodes;
+          const long long soff = P.offsets[ctl.point];
+#pragma unroll
+          for (int j = 0; j < NPT; ++j) {
+            const int sl = j * T + tid;
+            const int pn = Q.slot_pn[sl];
+            if (pn < 0) continue;
+            const double m = Q.slot_lump[sl] * scale;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              double fd = 0.0, acc = 0.0, vv = 0.0;
+              if (sl < F0 && k >= 1) {
+                fd = ncm[j] * vh[j][c];                // kernels_scalar.cpp:15-17
+                acc = -(fk[j][c] + fd) * ninv[j];
+                vv = vh[j][c] + h_k * acc;             // relax.cpp:166
+              }
+              SX[3 * pn + c] = nref[j][c] + u[j][c];
+              if (sl < F0) SW[3 * pn + c] = m * (vv * vv);
+              if (is_base) {
+                const long long dd = soff + 3 * pn + c;
+                P.u[dd] = u[j][c];
+                P.v[dd] = vv;
+                P.a[dd] = acc;
+                P.f_int[dd] = fk[j][c];
+                P.f_damp[dd] = fd;
+                P.mass[dd] = m;
+                P.inv_mass[dd] = ninv[j];
+              }
+            }
+          }
+          break;
+        }
+        decided = target;  // near tie that did not stop: continue normally
+        target = -1;
+      }
+      // ---- damped update + speculative half step / drift of iteration k+1 ----
+      double dt_next;
+      if (LAW == 0) {
+        dt_next = dt_const;
+      } else {
+        dt_next = P.dt_safety * sqrt(slots_min(ctl.wmin, C * NW, lane));
+      }
+      const double h_n = 0.5 * dt_next;
+      const bool save = target < 0 && ((k + 1) % kCkInterval == 0);
+      const int sb = ((k + 1) / kCkInterval) & 1;
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int sl = j * T + tid;
+        if (sl < F0) {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const double fd = ncm[j] * vh[j][c];              // kernels_scalar.cpp:15-17
+            const double acc = -(fk[j][c] + fd) * ninv[j];
+            const double vv = (k >= 1) ? vh[j][c] + h_k * acc : vh[j][c];  // relax.cpp:166
+            vh[j][c] = vv + h_n * acc;                          // relax.cpp:155
+            u[j][c] = u[j][c] + dt_next * vh[j][c];             // relax.cpp:156
+          }
+          double* xr = sm_at<double>(X, 24 * sl);
+          xr[0] = nref[j][0] + u[j][0];
+          xr[1] = nref[j][1] + u[j][1];
+          xr[2] = nref[j][2] + u[j][2];
+          push_x(j, sl, xr[0], xr[1], xr[2]);
+          if (save) {
+            double* ck = ckpt + sb * 6 * P.ck_stride;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              ck[c * P.ck_stride + sl] = u[j][c];
+              ck[(3 + c) * P.ck_stride + sl] = vh[j][c];
+            }
+          }
+        }
+      }
+      cl_sync();
+      if (save && tid == 0) {
+        ctl.ck_t[sb] = ctl.t;
+        ctl.ck_dt[sb] = dt_next;
+      }
+      dt_k = dt_next;
+      ++k;
+    }
+
+    // ================= exit (relax.cpp:181-190, network.cpp:341-372) =================
+    const int n_done = (status == FIBRA_OK) ? k : (k > 0 ? k - 1 : 0);
+    const bool zero_iter = (n_done == 0);
+    const int N = E.n_nodes, M = E.n_fibers, NFN = E.n_free_nodes, NFIX = E.n_fix_nodes;
+    double* SF = scr;
+    double* SX = SF + 3 * N;
+    double* SW = SX + 3 * N;
+    double* SE = SW + 3 * NFN;
+    if (status == FIBRA_OK && !zero_iter) {
+#pragma unroll
+      for (int j = 0; j < FPT; ++j) {
+        const int f = Q.fib_id[j * T + tid];
+        if (f >= 0) {  // strain_energy relax.cpp:57-72, from the final x records
+          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
+          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+          const double dx = xb_[0] - xa_[0];
+          const double dy = xb_[1] - xa_[1];
+          const double dz = xb_[2] - xa_[2];
+          const double len = sqrt(dx * dx + dy * dy + dz * dz);
+          SE[f] = law_energy<LAW>(SJ(j), len / fl0[j], fl0[j], bo, B);
+        }
+      }
+    }
+    __threadfence();
+    cl_sync();
+    if (rank == 0) {
+      if (status == FIBRA_OK && tid < 12) {  // reference-order reductions (4 partials)
+        const int r = tid & 3, which = tid >> 2;
+        const double* src = which == 0 ? SF : (which == 1 ? SF + 3 * NFN : SW);
+        const int len = which == 1 ? 3 * NFIX : 3 * NFN;
+        double acc = 0;
+        if (which < 2)
+          for (int i = r; i < len; i += 4) {
+            const double v = __ldcg(src + i);
+            acc += v * v;
+          }
+        else
+          for (int i = r; i < len; i += 4) acc += __ldcg(src + i);
+        ctl.ex[tid] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        SolveOut o = {};
+        o.iterations = n_done;
+        o.status = status;
+        if (status == FIBRA_OK) {
+          const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
+          const double react = sqrt((ctl.ex[4] + ctl.ex[5]) + (ctl.ex[6] + ctl.ex[7]));
+          o.residual = res;
+          o.eps_eff = P.tolerance * smax(react, ctl.force_floor);
+          o.dt = zero_iter ? 0.0 : dt_k;
+          o.converged = conv;
+          if (!zero_iter) {
+            const double ke = 0.5 * ((ctl.ex[8] + ctl.ex[9]) + (ctl.ex[10] + ctl.ex[11]));
+            double se = 0;
+            for (int f = 0; f < M; ++f) se += __ldcg(SE + f);
+            o.kinetic_fraction = (ke + se) > 0 ? ke / (ke + se) : 0.0;
+          }
+          if (conv) {  // homogenized_stress moment sums, boundary nodes ascending
+            double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            for (int pn = NFN; pn < N; ++pn) {
+              const double r0 = __ldcg(SF + 3 * pn), r1 = __ldcg(SF + 3 * pn + 1);
+              const double r2 = __ldcg(SF + 3 * pn + 2);
+              const double x0 = __ldcg(SX + 3 * pn), x1 = __ldcg(SX + 3 * pn + 1);
+              const double x2 = __ldcg(SX + 3 * pn + 2);
+              sm[0] += r0 * x0; sm[1] += r0 * x1; sm[2] += r0 * x2;
+              sm[3] += r1 * x0; sm[4] += r1 * x1; sm[5] += r1 * x2;
+              sm[6] += r2 * x0; sm[7] += r2 * x1; sm[8] += r2 * x2;
+            }
+            for (int i = 0; i < 9; ++i) o.moment[i] = sm[i];
+            o.box_volume = E.box_volume;
+          } else {
+            o.status = is_base ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;
+          }
+        }
+        P.out[s] = o;
+        if (is_base) {
+          P.t[p] = ctl.t;
+          if (status == FIBRA_OK) {
+            P.iters[p] += n_done;
+            P.converged[p] = static_cast<unsigned char>(conv);
+          } else {
+            P.converged[p] = 0;
+          }
+        }
+        atomicAdd(P.counters + 0, static_cast<unsigned long long>(n_done));
+        atomicAdd(P.counters + 1, static_cast<unsigned long long>(n_done) * M);
+        atomicAdd(P.counters + 2, static_cast<unsigned long long>(n_done) *
+                                      (51ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
+        atomicAdd(P.counters + 3, 1ull);
+      }
+    }
+    if (is_base) {  // every CTA wrote part of the base state its probes warm-start from
+      __threadfence();
+      cl_sync();
+      if (rank == 0 && tid == 0) publish_base(P, p, P.out[s].status == FIBRA_OK ? 1 : 2);
+    }
+    cl_sync();
+  }
+#undef SJ
+}
+
+}  // namespace fibra_b200

@@ -87,7 +87,8 @@ struct DrParams {
   unsigned long long* counters;  // [0] iterations [1] fiber-iterations [2] pipe ops [3] solves
   double* ckpt;                // [grid][2][6][ck_stride]
   int ck_stride, ck_interval;
-  int n_points, n_solves;
+  int n_points;                // all bound points (solve index layout)
+  int n_class, n_solves;       // this launch: points of its kernel class, their solves
   int x_bytes, g_bytes, part_slots, csr_cap;  // shared-memory layout capacities
   int reuse_warm;
   int law_buckling_off;
@@ -220,21 +221,22 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 #define SJ(j) (UEA ? s_uni : fs[j])
 
   for (;;) {
-    // Tickets [0, n) are base solves in P.order; tickets [n, 7n) are probes, served in the
-    // order base solves finish (six per finished base), so a CTA only waits for a base when
-    // every finished base's probes are already taken.  Solve index: base p -> p, probe q of
-    // p -> n + 6p + q (the output layout post_kernel reads).
+    // Tickets [0, nc) are the base solves of this kernel class in P.order; tickets
+    // [nc, 7nc) are probes, served in the order base solves finish (six per finished base),
+    // so a CTA only waits for a base when every finished base's probes are already taken.
+    // Solve index: base p -> p, probe q of p -> n + 6p + q (the layout post_kernel reads);
+    // -1 = queue drained.
     if (tid == 0) {
       const int t = atomicAdd(P.ticket, 1);
-      int s = P.n_solves;
+      int s = -1;
       if (t < P.n_solves) {
         int p, q = -1, flag = 1;
-        if (t < P.n_points) {
+        if (t < P.n_class) {
           p = P.order[t];
           s = p;
         } else {
-          const int k = (t - P.n_points) / 6;
-          q = (t - P.n_points) % 6;
+          const int k = (t - P.n_class) / 6;
+          q = (t - P.n_class) % 6;
           while ((p = ld_acquire(P.done_list + k)) < 0) __nanosleep(256);
           s = P.n_points + 6 * p + q;
           flag = ld_acquire(P.base_flag + p) == 1;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     }
     __syncthreads();
     const int s = ctl.solve;
-    if (s >= P.n_solves) break;
+    if (s < 0) break;
     const int p = ctl.point, q = ctl.q, e = ctl.entry;
     if (!ctl.flag) {  // pre-failed (prep) or base failed: nothing to solve
       if (tid == 0) {
@@ -380,6 +382,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
     int k = 0;              // force pass the next fiber phase evaluates
     int target = -1;        // pass at which to stop and decide exactly (replay mode)
+    int decided = -1;       // last pass whose exact verdict said "continue" (near tie)
     double dt_k = 0;        // dt of iteration k (0 for the initial pass)
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
       FB_PROF(tq = clock64());
-      if (target < 0 && k >= 1 && warp == NW - 1) {  // verdict for pass k-1, tree order
+      if (target < 0 && k - 1 > decided && warp == NW - 1) {  // verdict for pass k-1
         double sf = 0, sfix = 0;
         for (int i = lane; i < F0; i += 32) sf += spart[i];
         for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       FB_PROF({ const long long t1 = clock64(); pc1 += t1 - tq; tq = t1; })
 
       // ================= node phase (pass k) =================
-      if (target < 0 && k >= 1) {
+      if (target < 0 && k - 1 > decided) {
         const int d = ctl.dec;
         if ((d & (kDecConv | kDecExact)) || k - 1 == P.max_iterations) {
           // stop at k-1: replay from the newest checkpoint that resumes at or before it
@@ -600,7 +603,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           }
           break;
         }
-        target = -1;  // near tie that did not stop: continue normally
+        decided = target;  // near tie that did not stop: continue normally
+        target = -1;
         rewrite_fixed = true;
       }
       // ---- damped update + speculative half step / drift of iteration k+1 ----

@@ -19,10 +19,13 @@
 #include <type_traits>
 #include <vector>
 
+#include "dr_cluster.cuh"
 #include "dr_kernel.cuh"
+#include "host/cluster_schedule.hpp"
 #include "host/schedule.hpp"
 #include "fibra_cuda.h"
 #include "tensor.cuh"
+#include "variants.hpp"
 
 namespace fibra_b200 {
 
@@ -39,7 +42,8 @@ struct PrepOut {
 __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangent,
                             double fd_rel_step, PrepOut* prep, double* solve_F, int* solve_skip,
                             int* base_flag, int* done_list, int sched_mode,
-                            const double* __restrict__ hint, unsigned long long* key) {
+                            const double* __restrict__ hint, const int* __restrict__ cls,
+                            unsigned long long* key) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double f[9];
@@ -62,7 +66,9 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
     const float k = static_cast<float>(hint[p]);
     hi = (k == k && k > 0) ? ~__float_as_uint(k) : 0xffffffffu;
   }
-  key[p] = (static_cast<unsigned long long>(hi) << 32) | static_cast<unsigned>(p);
+  // [kernel class : 3][cost : 29][point : 32] -- the order is grouped by class
+  key[p] = (static_cast<unsigned long long>(cls[p]) << 61) |
+           (static_cast<unsigned long long>(hi >> 3) << 32) | static_cast<unsigned>(p);
   if (!polar_decompose(f, o.R, o.U)) {  // KinematicsError -> failed point
     o.status = FIBRA_E_KINEMATICS;
     solve_skip[p] = FIBRA_E_KINEMATICS;
@@ -248,38 +254,44 @@ __global__ void fp64_peak_kernel(double* sink, int iters, double c) {
 }
 
 // ---------------------------------------------------------------------------------
-// kernel variants: T threads, FPT fibers and NPT nodes per thread, force law
+// kernel classes (shapes in variants.hpp, instantiated in kernels_*.cu)
 // ---------------------------------------------------------------------------------
-using KernelFn = void (*)(DrParams);
-
-struct Variant {
-  int T, FPT, NPT, MINB;
-  KernelFn fn[2][2];  // [law: linear, exponential][uniform EA]
-};
-
-// Ordered by preference: the first variant whose capacity covers every library entry wins.
-// MINB = 2 keeps two CTAs (two RVEs) per SM so one CTA's barrier wait is covered by the
-// other's work.
-#define FB_V(T, F, N, B)                                                                 \
-  {T, F, N, B,                                                                             \
-   {{&dr_persistent_kernel<T, F, N, 0, B, false>, &dr_persistent_kernel<T, F, N, 0, B, true>}, \
-    {&dr_persistent_kernel<T, F, N, 1, B, false>, &dr_persistent_kernel<T, F, N, 1, B, true>}}}
-static const Variant kVariants[] = {
-    FB_V(256, 3, 1, 2),  // <= 256 node slots, <= 768 fibers
-    FB_V(384, 3, 1, 2),  // <= 384 node slots, <= 1152 fibers (config 1/2 networks)
-    FB_V(512, 2, 1, 2),  // <= 512 node slots, <= 1024 fibers
-    FB_V(512, 4, 1, 1),  // <= 512 node slots, <= 2048 fibers
-    FB_V(512, 6, 2, 1),  // <= 1024 node slots, <= 3072 fibers
-    FB_V(768, 7, 2, 1),  // <= 1536 node slots, <= 5376 fibers (ragged config-3 tail)
-};
-#undef FB_V
+constexpr int kMaxClasses = 8;
 
 struct DeviceEntry {
-  EntryDev dev;
+  EntryDev dev;           // resident-kernel entry
+  ClusterEntryDev cdev;   // cluster-kernel entry
   Schedule sched;
   std::vector<void*> allocs;
+  int cls = -1;           // kernel class
+  int n_nodes = 0;
   bool config_ok = true;
   std::string config_err;
+};
+
+// A kernel class: one kernel shape (resident variant, or cluster variant x cluster size)
+// and the library entries it solves.  Each class runs its own persistent launch with its
+// own ticket queue; classes of one call run concurrently on forked streams.
+struct KClass {
+  bool cluster = false;
+  int vi = 0, C = 1;
+  int x_bytes = 0, g_bytes = 0, ts = 0, csr_cap = 0, push_cap = 0, ck_stride = 0;
+  long long scratch_stride = 0;
+  bool uniform_ea = true;
+  EntryDev* d_entries = nullptr;          // [n_entries] (resident)
+  ClusterEntryDev* d_centries = nullptr;  // [n_entries] (cluster)
+  int n_points = 0, point_off = 0;        // bound points of the class, offset in the order
+  cudaStream_t stream = nullptr;
+  cudaEvent_t done = nullptr;
+  double* d_ckpt = nullptr;
+  size_t ckpt_cap = 0;
+  double* d_scratch = nullptr;
+  size_t scratch_cap = 0;
+  size_t smem() const {
+    if (cluster)
+      return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 8ull * csr_cap + 4ull * push_cap;
+    return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 4ull * (ts + 1) + 4ull * csr_cap;
+  }
 };
 
 }  // namespace fibra_b200
@@ -289,19 +301,18 @@ using namespace fibra_b200;
 struct fibra_ctx {
   int device = 0;
   int n_sm = 0;
+  int max_smem = 0;  // opt-in dynamic shared memory per block
   cudaStream_t stream = nullptr;
   bool own_stream = true;
   std::string err;
   std::vector<DeviceEntry> entries;
-  EntryDev* d_entries = nullptr;
-  const Variant* variant = nullptr;
-  bool uniform_ea = false;  // every entry has a single area*modulus over its fibers
-  int x_bytes = 0, g_bytes = 0, part_slots = 0, csr_cap = 0, ck_stride = 0;
+  std::vector<KClass> classes;
   // points
   int n_points = 0;
   std::vector<int32_t> entry_of_point;
   std::vector<long long> offsets;
   int* d_entry_of_point = nullptr;
+  int* d_class_of_point = nullptr;
   long long* d_offsets = nullptr;
   double* d_state[8] = {};  // u v a f_int f_damp mass inv_mass t
   long long* d_iters = nullptr;
@@ -322,11 +333,10 @@ struct fibra_ctx {
   fibra_point_result* d_res = nullptr;
   double* h_F = nullptr;                 // pinned staging
   fibra_point_result* h_res = nullptr;   // pinned staging
-  double* d_ckpt = nullptr;
-  size_t ckpt_cap = 0;
-  int* d_ticket = nullptr;
+  int* d_ticket = nullptr;               // [kMaxClasses][2]
   unsigned long long* d_counters = nullptr;
   cudaEvent_t ev[4] = {};
+  cudaEvent_t ev_fork = nullptr;
   int last_solves = 0;
   int last_launches = 0;
   unsigned long long* phase_prof = nullptr;
@@ -356,6 +366,8 @@ int dalloc(fibra_ctx* c, T** p, size_t n) {
 
 void free_points(fibra_ctx* c) {
   cudaFree(c->d_entry_of_point);
+  cudaFree(c->d_class_of_point);
+  c->d_class_of_point = nullptr;
   cudaFree(c->d_offsets);
   for (auto& p : c->d_state) cudaFree(p), p = nullptr;
   cudaFree(c->d_iters);
@@ -398,9 +410,15 @@ void free_library(fibra_ctx* c) {
   for (auto& e : c->entries)
     for (void* p : e.allocs) cudaFree(p);
   c->entries.clear();
-  cudaFree(c->d_entries);
-  c->d_entries = nullptr;
-  c->variant = nullptr;
+  for (auto& k : c->classes) {
+    cudaFree(k.d_entries);
+    cudaFree(k.d_centries);
+    cudaFree(k.d_ckpt);
+    cudaFree(k.d_scratch);
+    if (k.stream) cudaStreamDestroy(k.stream);
+    if (k.done) cudaEventDestroy(k.done);
+  }
+  c->classes.clear();
 }
 
 int ensure_scratch(fibra_ctx* c, int n) {
@@ -426,16 +444,22 @@ int ensure_scratch(fibra_ctx* c, int n) {
 
 size_t align16(size_t b) { return (b + 15) & ~static_cast<size_t>(15); }
 
-size_t smem_bytes(const fibra_ctx* c) {
-  return static_cast<size_t>(c->x_bytes) + c->g_bytes + 8ull * c->part_slots +
-         4ull * (c->part_slots + 1) + 4ull * c->csr_cap;
+template <class Tp>
+int grow(fibra_ctx* c, Tp** p, size_t& cap, size_t need) {
+  if (need <= cap) return FIBRA_OK;
+  cudaFree(*p);
+  *p = nullptr;
+  cap = 0;
+  FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(p), need * sizeof(Tp)));
+  cap = need;
+  return FIBRA_OK;
 }
 
 int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
                  const fibra_relax_cfg* rc, const fibra_stiff_cfg* sc, int want_tangent,
                  fibra_point_result* dres) {
   const int n = c->n_points;
-  if (!c->d_entries || !c->variant)
+  if (c->classes.empty() || c->offsets.empty())
     return set_err(c, FIBRA_E_ARG, "upload_library and bind_points must precede solve");
   // configuration validation (ConfigError propagates: relax.cpp:12-19, network.cpp:55-59,
   // stiffness.cpp:10-13)
@@ -457,27 +481,9 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   if (n == 0) return FIBRA_OK;
   int r;
   if ((r = ensure_scratch(c, n))) return r;
-  const Variant* v = c->variant;
-  KernelFn fn = v->fn[law->kind][c->uniform_ea ? 1 : 0];
-  const size_t smem = smem_bytes(c);
-  FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
-  int per_sm = 0;
-  FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v->T, smem));
-  if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "DR kernel does not fit on an SM");
-  const int n_solves = want_tangent ? 7 * n : n;
-  const int grid = std::min(n_solves, per_sm * c->n_sm);
-  const size_t ck = static_cast<size_t>(grid) * 12 * c->ck_stride;
-  if (ck > c->ckpt_cap) {
-    cudaFree(c->d_ckpt);
-    c->d_ckpt = nullptr;
-    c->ckpt_cap = 0;
-    FB_CUDA(c, cudaMalloc(&c->d_ckpt, ck * sizeof(double)));
-    c->ckpt_cap = ck;
-  }
 
   DrParams P;
-  P.entries = c->d_entries;
+  P.entries = nullptr;
   P.entry_of_point = c->d_entry_of_point;
   P.offsets = c->d_offsets;
   P.u = c->d_state[0];
@@ -494,19 +500,9 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.solve_skip = c->d_skip;
   P.out = c->d_out;
   P.base_flag = c->d_flag;
-  P.order = c->d_order;
-  P.done_list = c->d_done;
-  P.ticket = c->d_ticket;
   P.counters = c->d_counters;
-  P.ckpt = c->d_ckpt;
-  P.ck_stride = c->ck_stride;
-  P.ck_interval = 8;
+  P.ck_interval = kCkInterval;
   P.n_points = n;
-  P.n_solves = n_solves;
-  P.x_bytes = c->x_bytes;
-  P.g_bytes = c->g_bytes;
-  P.part_slots = c->part_slots;
-  P.csr_cap = c->csr_cap;
   P.reuse_warm = sc ? sc->reuse_warm : 1;
   P.law_buckling_off = law->buckling_off;
   P.ea_scale = law->ea_scale;
@@ -517,38 +513,126 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.density_scale = rc->density_scale;
   P.max_iterations = rc->max_iterations;
   P.phase_prof = nullptr;
-  if (getenv("FIBRA_PHASE_PROF")) {  // diagnostics: per-warp phase cycle accumulators
-    static unsigned long long* buf = nullptr;
-    static size_t cap = 0;
-    const size_t need = static_cast<size_t>(grid) * (v->T / 32) * 4;
-    if (need > cap) { cudaFree(buf); cudaMalloc(&buf, need * 8); cap = need; }
-    cudaMemsetAsync(buf, 0, need * 8, c->stream);
-    P.phase_prof = buf;
-    c->phase_prof = buf;
-    c->phase_prof_n = need;
-  }
 
   cudaStream_t st = c->stream;
   FB_CUDA(c, cudaEventRecord(c->ev[0], st));
-  FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(int), st));
+  FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, 2 * kMaxClasses * sizeof(int), st));
   FB_CUDA(c, cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), st));
   const int tb = 128;
   prep_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, sc ? sc->fd_rel_step : 1e-5,
                                                 c->d_prep, c->d_solveF, c->d_skip, c->d_flag,
-                                                c->d_done, c->sched_mode, c->d_hint, c->d_key);
+                                                c->d_done, c->sched_mode, c->d_hint,
+                                                c->d_class_of_point, c->d_key);
   FB_CUDA(c, cudaGetLastError());
   rank_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c->d_key, c->d_order);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
-  fn<<<grid, v->T, smem, st>>>(P);
-  FB_CUDA(c, cudaGetLastError());
+  FB_CUDA(c, cudaEventRecord(c->ev_fork, st));
+
+  // classes run concurrently; cluster classes (largest RVEs) are launched first
+  std::vector<int> launch_order;
+  for (int k = 0; k < static_cast<int>(c->classes.size()); ++k)
+    if (c->classes[k].n_points) launch_order.push_back(k);
+  std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
+    return c->classes[a].C > c->classes[b].C;
+  });
+  int launches = 3;  // prep, rank, post
+  bool prof_used = false;
+  for (int ci : launch_order) {
+    KClass& K = c->classes[ci];
+    const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
+    P.n_class = K.n_points;
+    P.n_solves = n_solves;
+    P.order = c->d_order + K.point_off;
+    P.done_list = c->d_done + K.point_off;
+    P.ticket = c->d_ticket + 2 * ci;
+    P.x_bytes = K.x_bytes;
+    P.g_bytes = K.g_bytes;
+    P.part_slots = K.ts;
+    P.csr_cap = K.csr_cap;
+    P.ck_stride = K.ck_stride;
+    const size_t smem = K.smem();
+    FB_CUDA(c, cudaStreamWaitEvent(K.stream, c->ev_fork, 0));
+    if (!K.cluster) {
+      const Variant& v = kVariants[K.vi];
+      KernelFn fn = v.fn[law->kind][K.uniform_ea ? 1 : 0];
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      int per_sm = 0;
+      FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.T, smem));
+      if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "DR kernel does not fit on an SM");
+      const int grid = std::min(n_solves, per_sm * c->n_sm);
+      if ((r = grow(c, &K.d_ckpt, K.ckpt_cap, static_cast<size_t>(grid) * 12 * K.ck_stride)))
+        return r;
+      P.entries = K.d_entries;
+      P.ckpt = K.d_ckpt;
+      P.phase_prof = nullptr;
+      if (getenv("FIBRA_PHASE_PROF") && !prof_used) {  // diagnostics: per-warp phase cycles
+        static unsigned long long* buf = nullptr;
+        static size_t cap = 0;
+        const size_t need = static_cast<size_t>(grid) * (v.T / 32) * 4;
+        if (need > cap) { cudaFree(buf); cudaMalloc(&buf, need * 8); cap = need; }
+        cudaMemsetAsync(buf, 0, need * 8, K.stream);
+        P.phase_prof = buf;
+        c->phase_prof = buf;
+        c->phase_prof_n = need;
+        prof_used = true;
+      }
+      fn<<<grid, v.T, smem, K.stream>>>(P);
+    } else {
+      const ClusterVariant& v = kClusterVariants[K.vi];
+      ClusterFn fn = v.fn[law->kind][K.uniform_ea ? 1 : 0];
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      if (K.C > 8)
+        FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = K.C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(K.C);
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = K.stream;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int max_clusters = 0;
+      FB_CUDA(c, cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg));
+      if (max_clusters < 1)
+        return set_err(c, FIBRA_E_ARG, "cluster DR kernel cannot be co-scheduled on this device");
+      const int nclu = std::min(n_solves, max_clusters);
+      cfg.gridDim = dim3(nclu * K.C);
+      if ((r = grow(c, &K.d_ckpt, K.ckpt_cap,
+                    static_cast<size_t>(nclu) * K.C * 12 * K.ck_stride)))
+        return r;
+      if ((r = grow(c, &K.d_scratch, K.scratch_cap, static_cast<size_t>(nclu) * K.scratch_stride)))
+        return r;
+      ClusterParams CP;
+      CP.d = P;
+      CP.d.entries = nullptr;
+      CP.d.ckpt = K.d_ckpt;
+      CP.d.phase_prof = nullptr;
+      CP.centries = K.d_centries;
+      CP.scratch = K.d_scratch;
+      CP.scratch_stride = K.scratch_stride;
+      CP.push_cap = K.push_cap;
+      CP.pad = 0;
+      FB_CUDA(c, cudaLaunchKernelEx(&cfg, fn, CP));
+    }
+    FB_CUDA(c, cudaGetLastError());
+    FB_CUDA(c, cudaEventRecord(K.done, K.stream));
+    FB_CUDA(c, cudaStreamWaitEvent(st, K.done, 0));
+    ++launches;
+  }
   FB_CUDA(c, cudaEventRecord(c->ev[2], st));
   post_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, c->d_prep, c->d_out,
                                                 c->d_solveF, dres);
   FB_CUDA(c, cudaGetLastError());
   FB_CUDA(c, cudaEventRecord(c->ev[3], st));
-  c->last_solves = n_solves;
-  c->last_launches = 4;
+  c->last_solves = want_tangent ? 7 * n : n;
+  c->last_launches = launches;
   return FIBRA_OK;
 }
 
@@ -592,6 +676,301 @@ PackedNet pack(const fibra_net_desc& d) {
   return P;
 }
 
+// largest CSR list of a network in entry pairs (incident fibers per node, padded to even)
+int max_pairs_of(const PackedNet& P) {
+  std::vector<int> deg(P.N, 0);
+  for (int f = 0; f < P.M; ++f) {
+    ++deg[P.a[f]];
+    ++deg[P.b[f]];
+  }
+  int m = 0;
+  for (int pn = 0; pn < P.N; ++pn) m = std::max(m, (deg[pn] + 1) / 2);
+  return m;
+}
+
+bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int max_pairs,
+                   Schedule& S) {
+  if (!build_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.FPT, v.NPT, S))
+    return false;
+  const int TS = v.NPT * v.T;
+  const int gd_total = S.gd_slots + 33;
+  if (S.node_slots * 24 >= 65536 || 24 * gd_total >= 65536) return false;  // 16-bit offsets
+  const size_t smem = align16(24 * static_cast<size_t>(TS + 2)) +
+                      align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
+                      8ull * TS + 4ull * (TS + 1) + 8ull * max_pairs * TS;
+  return smem <= static_cast<size_t>(c->max_smem);
+}
+
+bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& v, int C,
+                  int max_pairs, ClusterPlan& plan) {
+  if (!build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
+                          v.NPT, plan))
+    return false;
+  const int TS = v.NPT * v.T;
+  if (24 * (TS + 2 + plan.max_halo) >= 65536) return false;  // 16-bit x offsets
+  const size_t smem = align16(24ull * (TS + 2 + plan.max_halo)) +
+                      align16(24ull * (plan.max_records + 17)) + 8ull * TS +
+                      8ull * max_pairs * TS + 4ull * plan.max_push * TS;
+  return smem <= static_cast<size_t>(c->max_smem);
+}
+
+template <class Vec, class Tp>
+int upload_vec(fibra_ctx* c, DeviceEntry& de, Tp** dst, const Vec& vec) {
+  using Ep = typename Vec::value_type;
+  Ep* p = nullptr;
+  FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(vec.size(), 1) * sizeof(Ep)));
+  de.allocs.push_back(p);
+  if (!vec.empty())
+    FB_CUDA(c, cudaMemcpy(p, vec.data(), vec.size() * sizeof(Ep), cudaMemcpyHostToDevice));
+  *dst = reinterpret_cast<Tp*>(p);
+  return FIBRA_OK;
+}
+
+// resident-kernel entry: slot arrays, g*d record colouring, step-major CSR pairs
+int upload_resident_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
+                          const fibra_net_desc& d, const Variant& v, KClass& K) {
+  const Schedule& S = de.sched;
+  const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS, TS+1
+  const int FS = S.fiber_slots;
+  std::vector<int> slot_pn(TS, -1);
+  std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
+  for (int sl = 0; sl < S.node_slots; ++sl) {
+    const int pn = S.pn_of_slot[sl];
+    slot_pn[sl] = pn;
+    if (pn < 0) continue;
+    for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
+    slot_lump[sl] = P.lump[pn];
+  }
+  // g*d records: [real: tail (-g*d) and head (+g*d) per fiber, schedule colouring]
+  //               [two per dummy fiber slot, bank = lane] [zero record]
+  // (all dummies of one lane share a record pair: their values are never read, and within
+  //  one store instruction the 16 lanes still hit 16 different banks)
+  std::vector<int> dummy_tail(FS, -1), dummy_head(FS, -1);
+  for (int fs = 0; fs < FS; ++fs)
+    if (S.fiber_of_fslot[fs] < 0) {
+      dummy_tail[fs] = S.gd_slots + fs % 16;
+      dummy_head[fs] = S.gd_slots + 16 + fs % 16;
+    }
+  const int zero_rec = S.gd_slots + 32;
+  const int gd_total = zero_rec + 1;
+  // CSR by slot, ascending fiber id, padded to even length with the zero record;
+  // entry = byte offset of the node's own record of that fiber
+  std::vector<std::vector<int>> lists(TS);
+  for (int f = 0; f < P.M; ++f) {
+    lists[S.slot_of_pn[S.tail_pn[f]]].push_back(f);
+    lists[S.slot_of_pn[S.head_pn[f]]].push_back(f);
+  }
+  int max_pairs = 0;
+  for (int sl = 0; sl < TS; ++sl) {
+    std::sort(lists[sl].begin(), lists[sl].end());  // reference order (network.cpp:298-303)
+    max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
+  }
+  // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step)
+  std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs) * TS, 24 * zero_rec);
+  for (int sl = 0; sl < TS; ++sl) {
+    const auto& L = lists[sl];
+    const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
+    npairs[sl] = static_cast<int>((L.size() + 1) / 2);
+    for (size_t i = 0; i < L.size(); ++i) {
+      const int f = L[i];
+      ent[2 * ((i / 2) * TS + sl) + (i % 2)] =
+          24 * (pn == S.tail_pn[f] ? S.rec_tail[f] : S.rec_head[f]);
+    }
+  }
+  std::vector<int> fab(FS), fg(FS), fid(FS, -1);
+  std::vector<double> fl0(FS, 0.5), fea(FS, P.M > 0 ? P.ea[0] : 1.0);
+  for (int fs = 0; fs < FS; ++fs) {
+    const int f = S.fiber_of_fslot[fs];
+    if (f < 0) {  // dummy: unit segment between the two dummy x records
+      fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
+      fg[fs] = (24 * dummy_tail[fs]) | ((24 * dummy_head[fs]) << 16);
+      continue;
+    }
+    fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
+    fg[fs] = (24 * S.rec_tail[f]) | ((24 * S.rec_head[f]) << 16);
+    fid[fs] = f;
+    fl0[fs] = P.l0[f];
+    fea[fs] = P.ea[f];
+  }
+  EntryDev& E = de.dev;
+  E = EntryDev{};
+  E.n_nodes = P.N;
+  E.n_fibers = P.M;
+  E.n_free_nodes = P.NFN;
+  E.n_fix_nodes = P.N - P.NFN;
+  E.f0 = S.f0;
+  E.node_slots = S.node_slots;
+  E.fiber_slots = FS;
+  E.gd_slots = gd_total;
+  E.thread_slots = TS;
+  E.max_pairs = max_pairs;
+  E.max_lump = P.max_lump;
+  E.max_ea = d.max_ea;
+  E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
+  int rc;
+  if ((rc = upload_vec(c, de, &E.slot_pn, slot_pn))) return rc;
+  if ((rc = upload_vec(c, de, &E.slot_ref, slot_ref))) return rc;
+  if ((rc = upload_vec(c, de, &E.slot_lump, slot_lump))) return rc;
+  if ((rc = upload_vec(c, de, &E.csr_npairs, npairs))) return rc;
+  if ((rc = upload_vec(c, de, &E.csr_pairs, ent))) return rc;
+  if ((rc = upload_vec(c, de, &E.fib_ab, fab))) return rc;
+  if ((rc = upload_vec(c, de, &E.fib_g, fg))) return rc;
+  if ((rc = upload_vec(c, de, &E.fib_id, fid))) return rc;
+  if ((rc = upload_vec(c, de, &E.fib_l0, fl0))) return rc;
+  if ((rc = upload_vec(c, de, &E.fib_ea, fea))) return rc;
+  K.ts = TS;
+  K.ck_stride = TS;
+  K.x_bytes = std::max(K.x_bytes, static_cast<int>(align16(24 * static_cast<size_t>(TS + 2))));
+  const size_t gb = std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M));
+  K.g_bytes = std::max(K.g_bytes, static_cast<int>(align16(gb)));
+  K.csr_cap = std::max(K.csr_cap, static_cast<int>(ent.size()));
+  return FIBRA_OK;
+}
+
+// cluster-kernel entry: one PartDev per CTA (host/cluster_schedule.hpp)
+int upload_cluster_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
+                         const fibra_net_desc& d, const ClusterPlan& plan,
+                         const ClusterVariant& v, KClass& K) {
+  const int C = plan.C, T = v.T, TS = v.NPT * v.T, FS = v.FPT * v.T, FT = T - 32;
+  std::vector<std::vector<int>> inc(P.N);  // incident fibers per node, ascending id
+  for (int f = 0; f < P.M; ++f) {
+    inc[P.a[f]].push_back(f);
+    if (P.b[f] != P.a[f]) inc[P.b[f]].push_back(f);
+  }
+  std::vector<int> own_k(P.M, -1), hrec(P.M, -1);
+  for (int q = 0; q < C; ++q) {
+    const ClusterPart& Q = plan.parts[q];
+    for (size_t k = 0; k < Q.fibers.size(); ++k) own_k[Q.fibers[k]] = static_cast<int>(k);
+    for (size_t h = 0; h < Q.h_fiber.size(); ++h) hrec[Q.h_fiber[h]] = static_cast<int>(h);
+  }
+  // halo slot of a remote node in part q, and the push lists of the owners
+  std::vector<std::vector<int>> halo_of(C, std::vector<int>());
+  std::vector<std::vector<std::vector<int>>> push(C, std::vector<std::vector<int>>(TS));
+  for (int q = 0; q < C; ++q) {
+    const ClusterPart& Q = plan.parts[q];
+    halo_of[q].assign(P.N, -1);
+    for (size_t h = 0; h < Q.halo_pn.size(); ++h) {
+      const int pn = Q.halo_pn[h];
+      halo_of[q][pn] = static_cast<int>(h);
+      const int o = plan.part_of_pn[pn];
+      push[o][plan.slot_of_pn[pn]].push_back((q << 16) | (24 * (TS + 2 + static_cast<int>(h))));
+    }
+  }
+  std::vector<PartDev> parts(C);
+  int max_pairs_all = 0, max_push_all = 0, max_rec = 0;
+  for (int q = 0; q < C; ++q) {
+    const ClusterPart& Q = plan.parts[q];
+    PartDev& D = parts[q];
+    D = PartDev{};
+    const int n_own = static_cast<int>(Q.fibers.size());
+    const int n_h = static_cast<int>(Q.h_fiber.size());
+    const int zero_rec = n_own + n_h + 16;
+    std::vector<int> slot_pn(TS, -1);
+    std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
+    for (int sl = 0; sl < Q.node_slots; ++sl) {
+      const int pn = Q.pn_of_slot[sl];
+      slot_pn[sl] = pn;
+      if (pn < 0) continue;
+      for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
+      slot_lump[sl] = P.lump[pn];
+    }
+    // CSR: ascending fiber id; the owned fiber's record (negated for its tail) or the copy
+    // of a remote fiber's record (this node is its head)
+    int max_pairs = 0, max_push = 0;
+    std::vector<std::vector<int>> lists(TS);
+    for (int sl = 0; sl < Q.node_slots; ++sl) {
+      const int pn = Q.pn_of_slot[sl];
+      if (pn < 0) continue;
+      for (int f : inc[pn]) {
+        int e;
+        if (plan.owner_of_fiber[f] == q) {
+          const int k = own_k[f];
+          e = 24 * k;
+          if (Q.tail_pn[k] == pn) e |= static_cast<int>(0x80000000u);
+        } else {
+          e = 24 * (n_own + hrec[f]);
+        }
+        lists[sl].push_back(e);
+      }
+      max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
+      max_push = std::max(max_push, static_cast<int>(push[q][sl].size()));
+    }
+    std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs) * TS, 24 * zero_rec);
+    std::vector<int> npush(TS, 0), pdst(static_cast<size_t>(max_push) * TS, 0);
+    for (int sl = 0; sl < TS; ++sl) {
+      const auto& L = lists[sl];
+      npairs[sl] = static_cast<int>((L.size() + 1) / 2);
+      for (size_t i = 0; i < L.size(); ++i) ent[2 * ((i / 2) * TS + sl) + (i % 2)] = L[i];
+      npush[sl] = static_cast<int>(push[q][sl].size());
+      for (int h = 0; h < npush[sl]; ++h) pdst[static_cast<size_t>(h) * TS + sl] = push[q][sl][h];
+    }
+    std::vector<int> fab(FS, (24 * TS) | ((24 * (TS + 1)) << 16)), fgt(FS), fgh(FS, -1), fid(FS, -1);
+    std::vector<double> fl0(FS, 0.5), fea(FS, P.M > 0 ? P.ea[0] : 1.0), flt(FS, 1.0), flh(FS, 1.0);
+    for (int fs = 0; fs < FS; ++fs) fgt[fs] = 24 * (n_own + n_h + fs % 16);
+    for (int k = 0; k < n_own; ++k) {
+      const int fs = (k / FT) * T + k % FT;
+      const int f = Q.fibers[k], tl = Q.tail_pn[k], hd = Q.head_pn[k];
+      const int ph = plan.part_of_pn[hd];
+      const int xh = ph == q ? 24 * plan.slot_of_pn[hd] : 24 * (TS + 2 + halo_of[q][hd]);
+      fab[fs] = (24 * plan.slot_of_pn[tl]) | (xh << 16);
+      fgt[fs] = 24 * k;
+      if (ph != q)
+        fgh[fs] = (ph << 24) |
+                  (24 * (static_cast<int>(plan.parts[ph].fibers.size()) + hrec[f]));
+      fid[fs] = f;
+      fl0[fs] = P.l0[f];
+      fea[fs] = P.ea[f];
+      flt[fs] = P.lump[tl];
+      flh[fs] = P.lump[hd];
+    }
+    D.f0 = Q.f0;
+    D.node_slots = Q.node_slots;
+    D.halo = static_cast<int>(Q.halo_pn.size());
+    D.max_pairs = max_pairs;
+    D.max_push = max_push;
+    D.n_records = zero_rec + 1;
+    int rc;
+    if ((rc = upload_vec(c, de, &D.slot_pn, slot_pn))) return rc;
+    if ((rc = upload_vec(c, de, &D.slot_ref, slot_ref))) return rc;
+    if ((rc = upload_vec(c, de, &D.slot_lump, slot_lump))) return rc;
+    if ((rc = upload_vec(c, de, &D.csr_npairs, npairs))) return rc;
+    if ((rc = upload_vec(c, de, &D.csr_pairs, ent))) return rc;
+    if ((rc = upload_vec(c, de, &D.push_n, npush))) return rc;
+    if ((rc = upload_vec(c, de, &D.push_dst, pdst))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_ab, fab))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_gt, fgt))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_gh, fgh))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_id, fid))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_l0, fl0))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_ea, fea))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_lt, flt))) return rc;
+    if ((rc = upload_vec(c, de, &D.fib_lh, flh))) return rc;
+    max_pairs_all = std::max(max_pairs_all, max_pairs);
+    max_push_all = std::max(max_push_all, max_push);
+    max_rec = std::max(max_rec, D.n_records);
+  }
+  ClusterEntryDev& E = de.cdev;
+  E = ClusterEntryDev{};
+  E.n_nodes = P.N;
+  E.n_fibers = P.M;
+  E.n_free_nodes = P.NFN;
+  E.n_fix_nodes = P.N - P.NFN;
+  E.max_lump = P.max_lump;
+  E.max_ea = d.max_ea;
+  E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
+  E.ea0 = P.M > 0 ? P.ea[0] : 1.0;
+  int rc;
+  if ((rc = upload_vec(c, de, &E.parts, parts))) return rc;
+  K.ts = TS;
+  K.ck_stride = TS;
+  K.x_bytes = std::max(K.x_bytes, static_cast<int>(align16(24ull * (TS + 2 + plan.max_halo))));
+  K.g_bytes = std::max(K.g_bytes, static_cast<int>(align16(24ull * max_rec)));
+  K.csr_cap = std::max(K.csr_cap, max_pairs_all * TS);
+  K.push_cap = std::max(K.push_cap, max_push_all * TS);
+  K.scratch_stride = std::max<long long>(K.scratch_stride, 6LL * P.N + 3LL * P.NFN + P.M);
+  return FIBRA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -615,7 +994,12 @@ int fibra_cuda_open(int device, fibra_ctx** out) {
   c->n_sm = prop.multiProcessorCount;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
-  if (cudaMalloc(&c->d_ticket, 2 * sizeof(int)) != cudaSuccess) return bail(FIBRA_E_CUDA);
+  if (cudaMalloc(&c->d_ticket, 2 * kMaxClasses * sizeof(int)) != cudaSuccess) return bail(FIBRA_E_CUDA);
+  if (cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
+    return bail(FIBRA_E_CUDA);
+  c->max_smem -= 4096;  // the kernels' static control blocks (ClusterCtl ~3 KB)
+  if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+    return bail(FIBRA_E_CUDA);
   if (cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
   for (auto& e : c->ev)
@@ -631,10 +1015,10 @@ int fibra_cuda_close(fibra_ctx* c) {
   free_points(c);
   free_scratch(c);
   free_library(c);
-  cudaFree(c->d_ckpt);
   cudaFree(c->d_ticket);
   cudaFree(c->d_counters);
   for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaEventDestroy(c->ev_fork);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return FIBRA_OK;
@@ -668,150 +1052,76 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       return set_err(c, FIBRA_E_ARG, "malformed library entry " + std::to_string(i));
     nets.push_back(pack(d));
   }
-  // one kernel variant for the whole library: the first whose capacity covers every entry
+  // kernel class per entry: the first resident shape that holds it, else the smallest
+  // cluster (fewest CTAs) that does
   c->entries.resize(n);
-  for (const Variant& v : kVariants) {
-    bool ok = true;
-    for (int i = 0; i < n && ok; ++i) {
-      const PackedNet& P = nets[i];
-      ok = build_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.FPT, v.NPT,
-                          c->entries[i].sched) &&
-           c->entries[i].sched.node_slots * 24 < 65536;
-    }
-    if (ok) {
-      c->variant = &v;
-      break;
-    }
-  }
-  if (!c->variant)
-    return set_err(c, FIBRA_E_ARG, "RVE too large for the resident kernel variants");
-  c->uniform_ea = true;
-  for (const PackedNet& P : nets)
-    for (int f = 1; f < P.M && c->uniform_ea; ++f) c->uniform_ea = (P.ea[f] == P.ea[0]);
-  std::vector<EntryDev> host(n);
-  int max_ts = 0, max_gbytes = 0, max_ent = 0;
+  std::vector<ClusterPlan> plans(n);
   for (int i = 0; i < n; ++i) {
     const PackedNet& P = nets[i];
     DeviceEntry& de = c->entries[i];
-    const Schedule& S = de.sched;
     de.config_ok = P.ok;
     de.config_err = P.err;
-    const int TS = c->variant->NPT * c->variant->T;  // thread slots; dummy x records at TS, TS+1
-    const int FS = S.fiber_slots;
-    std::vector<int> slot_pn(TS, -1);
-    std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
-    for (int sl = 0; sl < S.node_slots; ++sl) {
-      const int pn = S.pn_of_slot[sl];
-      slot_pn[sl] = pn;
-      if (pn < 0) continue;
-      for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
-      slot_lump[sl] = P.lump[pn];
+    de.n_nodes = P.N;
+    const int mp = max_pairs_of(P);
+    bool cl = false;
+    int vi = -1, C = 1;
+    for (int v = 0; v < kNumVariants && vi < 0; ++v)
+      if (resident_fits(c, P, kVariants[v], mp, de.sched)) vi = v;
+    for (int cc = 2; cc <= 16 && vi < 0; cc *= 2)
+      for (int v = 0; v < kNumClusterVariants && vi < 0; ++v)
+        if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
+          vi = v;
+          C = cc;
+          cl = true;
+        }
+    if (vi < 0)
+      return set_err(c, FIBRA_E_ARG, "RVE library entry " + std::to_string(i) + " (" +
+                                         std::to_string(P.M) + " fibers, " +
+                                         std::to_string(P.N) + " nodes) exceeds a 16-CTA cluster");
+    int k = 0;
+    const int nk = static_cast<int>(c->classes.size());
+    while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].vi == vi && c->classes[k].C == C)) ++k;
+    if (k == nk) {
+      if (nk == kMaxClasses) return set_err(c, FIBRA_E_ARG, "too many kernel classes in one library");
+      KClass K;
+      K.cluster = cl;
+      K.vi = vi;
+      K.C = C;
+      c->classes.push_back(K);
     }
-    // g*d records: [real: tail (-g*d) and head (+g*d) per fiber, schedule colouring]
-    //               [two per dummy fiber slot, bank = lane] [zero record]
-    // (all dummies of one lane share a record pair: their values are never read, and within
-    //  one store instruction the 16 lanes still hit 16 different banks)
-    std::vector<int> dummy_tail(FS, -1), dummy_head(FS, -1);
-    for (int fs = 0; fs < FS; ++fs)
-      if (S.fiber_of_fslot[fs] < 0) {
-        dummy_tail[fs] = S.gd_slots + fs % 16;
-        dummy_head[fs] = S.gd_slots + 16 + fs % 16;
-      }
-    const int zero_rec = S.gd_slots + 32;
-    const int gd_total = zero_rec + 1;
-    if (24 * gd_total >= 65536)
-      return set_err(c, FIBRA_E_ARG, "too many g*d records for 16-bit offsets in entry " + std::to_string(i));
-    // CSR by slot, ascending fiber id, padded to even length with the zero record;
-    // entry = byte offset of the node's own record of that fiber
-    std::vector<std::vector<int>> lists(TS);
-    for (int f = 0; f < P.M; ++f) {
-      lists[S.slot_of_pn[S.tail_pn[f]]].push_back(f);
-      lists[S.slot_of_pn[S.head_pn[f]]].push_back(f);
-    }
-    int max_pairs = 0;
-    for (int sl = 0; sl < TS; ++sl) {
-      std::sort(lists[sl].begin(), lists[sl].end());  // reference order (network.cpp:298-303)
-      max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
-    }
-    // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step)
-    std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs) * TS, 24 * zero_rec);
-    for (int sl = 0; sl < TS; ++sl) {
-      const auto& L = lists[sl];
-      const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
-      npairs[sl] = static_cast<int>((L.size() + 1) / 2);
-      for (size_t i = 0; i < L.size(); ++i) {
-        const int f = L[i];
-        ent[2 * ((i / 2) * TS + sl) + (i % 2)] =
-            24 * (pn == S.tail_pn[f] ? S.rec_tail[f] : S.rec_head[f]);
-      }
-    }
-    std::vector<int> fab(FS), fg(FS), fid(FS, -1);
-    std::vector<double> fl0(FS, 0.5), fea(FS, 1.0);
-    for (int fs = 0; fs < FS; ++fs) {
-      const int f = S.fiber_of_fslot[fs];
-      if (f < 0) {  // dummy: unit segment between the two dummy x records
-        fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
-        fg[fs] = (24 * dummy_tail[fs]) | ((24 * dummy_head[fs]) << 16);
-        continue;
-      }
-      fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
-      fg[fs] = (24 * S.rec_tail[f]) | ((24 * S.rec_head[f]) << 16);
-      fid[fs] = f;
-      fl0[fs] = P.l0[f];
-      fea[fs] = P.ea[f];
-    }
-    EntryDev& E = host[i];
-    E.n_nodes = P.N;
-    E.n_fibers = P.M;
-    E.n_free_nodes = P.NFN;
-    E.n_fix_nodes = P.N - P.NFN;
-    E.f0 = S.f0;
-    E.node_slots = S.node_slots;
-    E.fiber_slots = FS;
-    E.gd_slots = gd_total;
-    E.thread_slots = TS;
-    E.max_lump = P.max_lump;
-    E.max_ea = entries[i].max_ea;
-    E.box_volume = 8.0 * entries[i].box_half * entries[i].box_half * entries[i].box_half;
-    auto up = [&](auto** dst, const auto& vec) -> int {
-      using Tp = typename std::decay_t<decltype(vec)>::value_type;
-      Tp* p = nullptr;
-      FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(vec.size(), 1) * sizeof(Tp)));
-      de.allocs.push_back(p);
-      if (!vec.empty())
-        FB_CUDA(c, cudaMemcpy(p, vec.data(), vec.size() * sizeof(Tp), cudaMemcpyHostToDevice));
-      *dst = p;
-      return FIBRA_OK;
-    };
-    int rc;
-    if ((rc = up(&E.slot_pn, slot_pn))) return rc;
-    if ((rc = up(&E.slot_ref, slot_ref))) return rc;
-    if ((rc = up(&E.slot_lump, slot_lump))) return rc;
-    if ((rc = up(&E.csr_npairs, npairs))) return rc;
-    {
-      int* pairs = nullptr;
-      if ((rc = up(&pairs, ent))) return rc;
-      E.csr_pairs = reinterpret_cast<const int2*>(pairs);
-    }
-    E.max_pairs = max_pairs;
-    if ((rc = up(&E.fib_ab, fab))) return rc;
-    if ((rc = up(&E.fib_g, fg))) return rc;
-    if ((rc = up(&E.fib_id, fid))) return rc;
-    if ((rc = up(&E.fib_l0, fl0))) return rc;
-    if ((rc = up(&E.fib_ea, fea))) return rc;
-    de.dev = E;
-    max_ts = std::max(max_ts, TS);
-    max_ent = std::max(max_ent, static_cast<int>(ent.size()));
-    const int gb = std::max(24 * gd_total, 8 * (3 * P.N + 3 * P.NFN + P.M));
-    max_gbytes = std::max(max_gbytes, gb);
+    de.cls = k;
+    KClass& K = c->classes[k];
+    for (int f = 1; f < P.M && K.uniform_ea; ++f) K.uniform_ea = (P.ea[f] == P.ea[0]);
   }
-  c->x_bytes = static_cast<int>(align16(24 * static_cast<size_t>(max_ts + 2)));
-  c->g_bytes = static_cast<int>(align16(max_gbytes));
-  c->part_slots = max_ts;
-  c->csr_cap = max_ent;
-  c->ck_stride = max_ts;
-  FB_CUDA(c, cudaMalloc(&c->d_entries, sizeof(EntryDev) * n));
-  FB_CUDA(c, cudaMemcpy(c->d_entries, host.data(), sizeof(EntryDev) * n, cudaMemcpyHostToDevice));
+  for (int i = 0; i < n; ++i) {
+    DeviceEntry& de = c->entries[i];
+    KClass& K = c->classes[de.cls];
+    const int rc = K.cluster
+                       ? upload_cluster_entry(c, de, nets[i], entries[i], plans[i],
+                                              kClusterVariants[K.vi], K)
+                       : upload_resident_entry(c, de, nets[i], entries[i], kVariants[K.vi], K);
+    if (rc) return rc;
+  }
+  for (KClass& K : c->classes) {
+    if (K.smem() > static_cast<size_t>(c->max_smem))
+      return set_err(c, FIBRA_E_ARG, "library shared-memory footprint exceeds the device limit");
+    if (K.cluster) {
+      std::vector<ClusterEntryDev> host(n, ClusterEntryDev{});
+      for (int i = 0; i < n; ++i)
+        if (&c->classes[c->entries[i].cls] == &K) host[i] = c->entries[i].cdev;
+      FB_CUDA(c, cudaMalloc(&K.d_centries, sizeof(ClusterEntryDev) * n));
+      FB_CUDA(c, cudaMemcpy(K.d_centries, host.data(), sizeof(ClusterEntryDev) * n,
+                            cudaMemcpyHostToDevice));
+    } else {
+      std::vector<EntryDev> host(n, EntryDev{});
+      for (int i = 0; i < n; ++i)
+        if (&c->classes[c->entries[i].cls] == &K) host[i] = c->entries[i].dev;
+      FB_CUDA(c, cudaMalloc(&K.d_entries, sizeof(EntryDev) * n));
+      FB_CUDA(c, cudaMemcpy(K.d_entries, host.data(), sizeof(EntryDev) * n, cudaMemcpyHostToDevice));
+    }
+    FB_CUDA(c, cudaStreamCreateWithFlags(&K.stream, cudaStreamNonBlocking));
+    FB_CUDA(c, cudaEventCreateWithFlags(&K.done, cudaEventDisableTiming));
+  }
   return FIBRA_OK;
 }
 
@@ -823,16 +1133,26 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   free_points(c);
   c->entry_of_point.assign(entry_of_point, entry_of_point + n);
   c->offsets.assign(n + 1, 0);
+  std::vector<int> cls(n);
+  for (auto& K : c->classes) K.n_points = 0;
   for (int p = 0; p < n; ++p) {
     const int e = entry_of_point[p];
     if (e < 0 || e >= static_cast<int>(c->entries.size()))
       return set_err(c, FIBRA_E_CONFIG, "assignment entry out of range");
-    c->offsets[p + 1] = c->offsets[p] + 3LL * c->entries[e].dev.n_nodes;
+    c->offsets[p + 1] = c->offsets[p] + 3LL * c->entries[e].n_nodes;
+    cls[p] = c->entries[e].cls;
+    ++c->classes[cls[p]].n_points;
+  }
+  int off = 0;  // the schedule order groups points by class (rank_kernel keys)
+  for (auto& K : c->classes) {
+    K.point_off = off;
+    off += K.n_points;
   }
   c->n_points = n;
   const size_t tot = static_cast<size_t>(c->offsets[n]);
   int rc;
   if ((rc = dalloc(c, &c->d_entry_of_point, n))) return rc;
+  if ((rc = dalloc(c, &c->d_class_of_point, n))) return rc;
   if ((rc = dalloc(c, &c->d_offsets, n + 1))) return rc;
   for (int k = 0; k < 7; ++k)
     if ((rc = dalloc(c, &c->d_state[k], tot))) return rc;
@@ -841,9 +1161,23 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   if ((rc = dalloc(c, &c->d_conv, n))) return rc;
   if (n) {
     FB_CUDA(c, cudaMemcpy(c->d_entry_of_point, entry_of_point, sizeof(int) * n, cudaMemcpyHostToDevice));
+    FB_CUDA(c, cudaMemcpy(c->d_class_of_point, cls.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
   }
   FB_CUDA(c, cudaMemcpy(c->d_offsets, c->offsets.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice));
   return fibra_cuda_reset_states(c);
+}
+
+int fibra_cuda_entry_kernel(const fibra_ctx* c, int32_t entry, int32_t* out) {
+  if (!c || !out || entry < 0 || entry >= static_cast<int>(c->entries.size())) return FIBRA_E_ARG;
+  const KClass& K = c->classes[c->entries[entry].cls];
+  if (K.cluster) {
+    const ClusterVariant& v = kClusterVariants[K.vi];
+    out[0] = K.C, out[1] = v.T, out[2] = v.FPT, out[3] = v.NPT;
+  } else {
+    const Variant& v = kVariants[K.vi];
+    out[0] = 1, out[1] = v.T, out[2] = v.FPT, out[3] = v.NPT;
+  }
+  return FIBRA_OK;
 }
 
 int fibra_cuda_set_schedule(fibra_ctx* c, int32_t mode, const double* cost_hint) {

@@ -111,10 +111,12 @@ bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
       P.parts[ph].h_fiber.push_back(f);
     }
   }
+  std::vector<int> copies(N, 0);
   for (int c = 0; c < C; ++c) {
     ClusterPart& Q = P.parts[c];
     std::sort(Q.halo_pn.begin(), Q.halo_pn.end());
     Q.halo_pn.erase(std::unique(Q.halo_pn.begin(), Q.halo_pn.end()), Q.halo_pn.end());
+    for (int pn : Q.halo_pn) P.max_push = std::max(P.max_push, ++copies[pn]);
     if (static_cast<int>(Q.fibers.size()) > fiber_cap) return false;
     P.max_halo = std::max(P.max_halo, static_cast<int>(Q.halo_pn.size()));
     P.max_records = std::max(P.max_records, static_cast<int>(Q.fibers.size() + Q.h_fiber.size()));

@@ -39,6 +39,7 @@ struct ClusterPlan {
   std::vector<int> owner_of_fiber;  // [M]
   std::vector<ClusterPart> parts;   // [C]
   int max_halo = 0, max_records = 0, max_fibers = 0, max_node_slots = 0;
+  int max_push = 0;                 // most halo copies of one node
 };
 
 // ref: packed reference coordinates (3N); nodes [0, NFN) are free.  Returns false when a

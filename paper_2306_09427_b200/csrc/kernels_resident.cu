@@ -1,0 +1,23 @@
+// Resident DR kernel instances (dr_kernel.cuh), by preference: an entry takes the first
+// shape whose capacity covers it.  MINB = 2 keeps two CTAs (two RVEs) per SM so one CTA's
+// barrier wait is covered by the other's work.
+#include "variants.hpp"
+
+namespace fibra_b200 {
+
+#define FB_V(T, F, N, B)                                                                 \
+  {T, F, N, B,                                                                             \
+   {{&dr_persistent_kernel<T, F, N, 0, B, false>, &dr_persistent_kernel<T, F, N, 0, B, true>}, \
+    {&dr_persistent_kernel<T, F, N, 1, B, false>, &dr_persistent_kernel<T, F, N, 1, B, true>}}}
+const Variant kVariants[] = {
+    FB_V(256, 3, 1, 2),  // <= 256 node slots, <= 672 fibers
+    FB_V(384, 3, 1, 2),  // <= 384 node slots, <= 1056 fibers (config 1/2 networks)
+    FB_V(512, 2, 1, 2),  // <= 512 node slots, <= 960 fibers
+    FB_V(512, 4, 1, 1),  // <= 512 node slots; 16-bit record offsets cap fibers at ~1.3k
+    FB_V(512, 6, 2, 1),  // <= 1024 node slots (node-heavy segments networks)
+    FB_V(768, 7, 2, 1),  // <= 1536 node slots
+};
+#undef FB_V
+const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+}  // namespace fibra_b200

@@ -1,0 +1,28 @@
+// Kernel shapes compiled into the library (instantiated in kernels_resident.cu and
+// kernels_cluster.cu so nvcc builds them as separate translation units).
+#pragma once
+
+#include "dr_cluster.cuh"
+#include "dr_kernel.cuh"
+
+namespace fibra_b200 {
+
+using KernelFn = void (*)(DrParams);
+using ClusterFn = void (*)(ClusterParams);
+
+struct Variant {     // resident kernel: one CTA per RVE
+  int T, FPT, NPT, MINB;
+  KernelFn fn[2][2];  // [law: linear, exponential][uniform EA]
+};
+
+struct ClusterVariant {  // cluster kernel: one cluster of C CTAs per RVE (per-CTA shape)
+  int T, FPT, NPT;
+  ClusterFn fn[2][2];
+};
+
+extern const Variant kVariants[];
+extern const int kNumVariants;
+extern const ClusterVariant kClusterVariants[];
+extern const int kNumClusterVariants;
+
+}  // namespace fibra_b200

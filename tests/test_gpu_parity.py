@@ -124,6 +124,21 @@ def test_schedule_modes_bitwise(small_lib):
             assert same_bits(getattr(st, k), getattr(s0, k)), k
 
 
+def test_exponential_law_tolerance(oracle_lib):
+    """Exponential law on the resident kernel: libm vs CUDA expm1/exp differ by ulps, so
+    sigma to 1e-12 and the tangent to 1e-8 (test_gpu_cluster.check_exponential)."""
+    from test_gpu_cluster import check_exponential
+    pn, on = knn(375, 1000, 1)
+    F = batch_F(4)
+    lib = P.RveLibrary([pn])
+    st, assign = P.init_batch(np.zeros(4, np.int32), lib, 0)
+    br = P.batch_response(lib, assign, st, P.FiberLaw(kind="exponential", nonlinearity=1.2), F,
+                          P.RelaxConfig(), P.StiffnessConfig())
+    resp, status, _ = oracle_batch([on], [0] * 4, F, tangent=True,
+                                   law=O.Law(kind=1, nonlinearity=1.2))
+    check_exponential(br, resp, status)
+
+
 def test_failed_points_reported(small_lib):
     pnets, _ = small_lib
     lib = P.RveLibrary(pnets)
