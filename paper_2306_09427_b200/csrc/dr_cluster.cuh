@@ -68,7 +68,7 @@ struct ClusterParams {
 
 struct __align__(16) ClusterCtl {
   int solve, point, q, entry;
-  int flag, collapse, dec, pad0;
+  int flag, collapse, dec, skip;  // skip: last pass whose exact verdict said "continue"
   double ck_t[2], ck_dt[2];
   double warp_min[32];
   double ex[12];
@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       ctl.ck_dt[0] = 0.0;
       ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
       ctl.collapse = 0;
+      ctl.skip = -1;
     }
     if (LAW == 0) push_wmin(warp_min(lmin));
     const bool det_ok = det3(Fm) > 0;
@@ -326,7 +327,6 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
 
     int k = 0;
     int target = -1;
-    int decided = -1;  // last pass whose exact verdict said "continue" (near tie)
     double dt_k = 0;
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
             cl_st_f64(a, sf);
             cl_st_f64(a + 8, sfix);
           }
-          if (k - 2 > decided && lane == 0) {  // verdict for pass k-2 (rank order, every CTA)
+          if (k >= 2 && lane == 0) {  // verdict for pass k-2 (rank order, every CTA)
             double tf = 0, tx = 0;
             for (unsigned r = 0; r < C; ++r) {
               tf += ctl.part[(k - 2) & 1][r][0];
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
             int d = (res <= eps) ? kDecConv : 0;
             if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
             else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
-            ctl.dec = d;
+            ctl.dec = (k - 2 > ctl.skip) ? d : 0;  // decided passes are not re-decided
           }
         }
       } else {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       cl_sync();
 
       // ================= node phase (pass k) =================
-      if (target < 0 && k - 2 > decided) {
+      if (target < 0 && k >= 2) {
         const int d = ctl.dec;
         if ((d & (kDecConv | kDecExact)) || k - 2 == P.max_iterations) {
           target = k - 2;  // replay from the newest checkpoint at or before it
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
           }
           break;
         }
-        decided = target;  // near tie that did not stop: continue normally
+        if (tid == 0) ctl.skip = target;  // near tie that did not stop: continue normally
         target = -1;
       }
       // ---- damped update + speculative half step / drift of iteration k+1 ----

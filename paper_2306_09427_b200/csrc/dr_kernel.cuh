@@ -115,7 +115,7 @@ constexpr int kCkInterval = 8;
 
 struct __align__(16) DrCtl {
   int solve, point, q, entry;
-  int flag, collapse, dec, pad0;
+  int flag, collapse, dec, skip;  // skip: last pass whose exact verdict said "continue"
   double ck_t[2], ck_dt[2];  // checkpoint buffers: t after, dt of, the resume pass
   double warp_min[32];
   double ex[12];
@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       ctl.ck_t[0] = ctl.t;
       ctl.ck_dt[0] = 0.0;
       ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
+      ctl.skip = -1;
     }
     if (LAW == 0) {
       lmin = warp_min(lmin);
@@ -382,7 +383,6 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
     int k = 0;              // force pass the next fiber phase evaluates
     int target = -1;        // pass at which to stop and decide exactly (replay mode)
-    int decided = -1;       // last pass whose exact verdict said "continue" (near tie)
     double dt_k = 0;        // dt of iteration k (0 for the initial pass)
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
@@ -392,7 +392,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
       FB_PROF(tq = clock64());
-      if (target < 0 && k - 1 > decided && warp == NW - 1) {  // verdict for pass k-1
+      if (target < 0 && k >= 1 && warp == NW - 1) {  // verdict for pass k-1, tree order
+        // a pass already decided exactly ("continue" at a near tie) is not re-decided
         double sf = 0, sfix = 0;
         for (int i = lane; i < F0; i += 32) sf += spart[i];
         for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           int d = (res <= eps) ? kDecConv : 0;
           if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
           else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
-          ctl.dec = d;
+          ctl.dec = (k - 1 > ctl.skip) ? d : 0;
         }
       }
       if (LAW != 0 && warp == NW - 1 && lane == 0) ctl.warp_min[warp] = INFINITY;
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       FB_PROF({ const long long t1 = clock64(); pc1 += t1 - tq; tq = t1; })
 
       // ================= node phase (pass k) =================
-      if (target < 0 && k - 1 > decided) {
+      if (target < 0 && k >= 1) {
         const int d = ctl.dec;
         if ((d & (kDecConv | kDecExact)) || k - 1 == P.max_iterations) {
           // stop at k-1: replay from the newest checkpoint that resumes at or before it
@@ -603,7 +604,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           }
           break;
         }
-        decided = target;  // near tie that did not stop: continue normally
+        if (tid == 0) ctl.skip = target;  // near tie that did not stop: continue normally
         target = -1;
         rewrite_fixed = true;
       }
