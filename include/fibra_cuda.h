@@ -77,6 +77,13 @@ int fibra_network_create(const double* coords, int32_t n_nodes, const int32_t* f
                          double box_half, double tol_bnd, fibra_network** out);
 int fibra_network_generate(const fibra_netgen_spec* spec, uint64_t seed, fibra_network** out);
 int fibra_network_read(const char* path, double box_half, double tol_bnd, fibra_network** out);
+/* Builder-side jittered lattice (no reference generator exists for config-4 sizes, SURVEY
+ * 8d): n_side^3 nodes, face nodes exactly on the box faces, every axis bond plus seeded face
+ * diagonals up to `fibers`; constructed like a file read (write it with
+ * fibra_network_write to obtain the reference file format). */
+int fibra_network_generate_lattice(int32_t n_side, int32_t fibers, double jitter, double area,
+                                   double modulus, double box_half, double tol_bnd,
+                                   uint64_t seed, fibra_network** out);
 int fibra_network_write(const fibra_network* net, const char* path);
 int fibra_network_describe(const fibra_network* net, fibra_net_desc* out);
 void fibra_network_free(fibra_network* net);
@@ -88,6 +95,10 @@ int fibra_assign_random(uint64_t seed, int32_t n_points, int32_t n_entries, int3
  * out[6] = {fits, conflicting fiber groups, gather excess wavefronts, gather steps,
  *           g*d records, node slots}. */
 int fibra_schedule_report(const fibra_net_desc* net, int T, int FPT, int NPT, int64_t* out);
+/* Diagnostics: the cluster partition (csrc/host/cluster_schedule.cpp) of one network over C
+ * CTAs of shape (T, FPT, NPT).  out[8] = {fits, max fibers per CTA, min fibers per CTA, max
+ * node slots, max halo nodes, max records, max halo copies of a node, cross-CTA fibers}. */
+int fibra_cluster_report(const fibra_net_desc* net, int C, int T, int FPT, int NPT, int64_t* out);
 
 /* ---- solver configuration records ------------------------------------------------- */
 typedef struct {          /* FiberLaw network.hpp:27-38                              */

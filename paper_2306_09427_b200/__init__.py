@@ -205,6 +205,19 @@ def generate_network(spec: NetGenSpec, seed: int) -> FiberNetwork:
     return FiberNetwork(h)
 
 
+def generate_lattice_network(n_side: int, fibers: int, seed: int, jitter: float = 0.25,
+                             fiber_area: float = 1.0, fiber_modulus: float = 1.0,
+                             box_half: float = 0.5, tol_bnd: float = 1e-6) -> FiberNetwork:
+    """Builder-side jittered lattice for config-4 sized RVEs (~50k fibers; the reference's
+    knn generator fails there).  n_side^3 nodes, face nodes exactly on the box,
+    every axis bond plus seeded face diagonals up to `fibers`."""
+    h = C.c_void_p()
+    FiberNetwork._check(_capi.load().fibra_network_generate_lattice(
+        int(n_side), int(fibers), float(jitter), float(fiber_area), float(fiber_modulus),
+        float(box_half), float(tol_bnd), int(seed), C.byref(h)))
+    return FiberNetwork(h)
+
+
 # ---- library / assignment / packed states (batch.hpp:20-61) -----------------------------
 @dataclass
 class RveLibrary:

@@ -23,9 +23,11 @@ STATUS_NAMES = {0: "ok", 1: "config", 2: "kinematics", 3: "collapse", 4: "bad_dt
 
 # every symbol include/fibra_cuda.h declares (checked by tests/test_capi.py)
 EXPORTS = [
-    "fibra_network_create", "fibra_network_generate", "fibra_network_read",
+    "fibra_network_create", "fibra_network_generate", "fibra_network_generate_lattice",
+    "fibra_network_read",
     "fibra_network_write", "fibra_network_describe", "fibra_network_free",
     "fibra_host_last_error", "fibra_assign_random", "fibra_schedule_report",
+    "fibra_cluster_report",
     "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
     "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel",
@@ -116,12 +118,17 @@ def load(build_if_missing: bool = True):
                                            C.c_double, pp]),
         "fibra_network_generate": (C.c_int, [C.POINTER(NetgenSpec), C.c_uint64, pp]),
         "fibra_network_read": (C.c_int, [C.c_char_p, C.c_double, C.c_double, pp]),
+        "fibra_network_generate_lattice": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                                     C.c_double, C.c_double, C.c_double,
+                                                     C.c_uint64, pp]),
         "fibra_network_write": (C.c_int, [vp, C.c_char_p]),
         "fibra_network_describe": (C.c_int, [vp, C.POINTER(NetDesc)]),
         "fibra_network_free": (None, [vp]),
         "fibra_host_last_error": (C.c_char_p, []),
         "fibra_assign_random": (C.c_int, [C.c_uint64, C.c_int32, C.c_int32, _ip]),
         "fibra_schedule_report": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, _lp]),
+        "fibra_cluster_report": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, C.c_int,
+                                           _lp]),
         "fibra_cuda_open": (C.c_int, [C.c_int, pp]),
         "fibra_cuda_close": (C.c_int, [vp]),
         "fibra_cuda_last_error": (C.c_char_p, [vp]),

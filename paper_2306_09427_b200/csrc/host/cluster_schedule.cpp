@@ -2,7 +2,10 @@
 #include "host/cluster_schedule.hpp"
 
 #include <algorithm>
+#include <cstdint>
 #include <numeric>
+
+#include "fibra_cuda.h"
 
 namespace fibra_b200 {
 namespace {
@@ -127,3 +130,29 @@ bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
 }
 
 }  // namespace fibra_b200
+
+// Diagnostics (C-ABI, no GPU needed): the cluster partition of one network.
+extern "C" int fibra_cluster_report(const fibra_net_desc* d, int C, int T, int FPT, int NPT,
+                                    int64_t* out) {
+  const int N = d->n_nodes, M = d->n_fibers;
+  std::vector<int> a(M), b(M);
+  for (int f = 0; f < M; ++f) {
+    a[f] = d->fiber_packed_dofs[6 * f] / 3;
+    b[f] = d->fiber_packed_dofs[6 * f + 3] / 3;
+  }
+  fibra_b200::ClusterPlan plan;
+  const bool ok = fibra_b200::build_cluster_plan(N, d->n_free / 3, M, a.data(), b.data(),
+                                                 d->packed_ref, C, T, FPT, NPT, plan);
+  int min_fibers = M, cross = 0;
+  for (const auto& q : plan.parts) min_fibers = std::min(min_fibers, static_cast<int>(q.fibers.size()));
+  for (const auto& q : plan.parts) cross += static_cast<int>(q.h_fiber.size());
+  out[0] = ok;
+  out[1] = plan.max_fibers;
+  out[2] = plan.parts.empty() ? 0 : min_fibers;
+  out[3] = plan.max_node_slots;
+  out[4] = plan.max_halo;
+  out[5] = plan.max_records;
+  out[6] = plan.max_push;
+  out[7] = cross;
+  return ok ? 0 : 21;
+}

@@ -33,6 +33,8 @@ int build_network(std::vector<double> coords, std::vector<int32_t> fiber_nodes,
 int read_network(const std::string& path, double box_half, double tol_bnd, Network& net);
 int write_network(const Network& net, const std::string& path);
 int generate_network(const fibra_netgen_spec& spec, uint64_t seed, Network& net);
+int generate_lattice(int n, int fibers, double jitter, double area, double modulus,
+                     double box_half, double tol_bnd, uint64_t seed, Network& net);
 void describe(const Network& net, fibra_net_desc* d);
 
 }  // namespace fibra_b200

@@ -326,6 +326,79 @@ int knn(const fibra_netgen_spec& s, uint64_t seed, Network& net) {
 
 }  // namespace
 
+// Builder-side jittered lattice for config-4 sized RVEs (the reference knn
+// generator fails beyond ~6k nodes).  n^3 nodes on a cube lattice spanning the box; face
+// nodes sit exactly on their face (so FiberNetwork's boundary test, network.cpp:110-117,
+// finds them) and are jittered only tangentially; interior nodes are jittered by up to
+// `jitter` lattice spacings per axis.  Fibers: every axis bond, then face diagonals drawn
+// without replacement (mt19937_64(seed) shuffle) up to `fibers`.  The result goes through
+// the same construction as a file read (build_network), so it can be written in the
+// reference format and re-read there.
+int generate_lattice(int n, int fibers, double jitter, double area, double modulus,
+                     double box_half, double tol_bnd, uint64_t seed, Network& net) {
+  if (n < 2 || !(jitter >= 0 && jitter < 0.5) || !(box_half > 0) || !(area > 0) ||
+      !(modulus > 0))
+    return fail(FIBRA_E_CONFIG, "lattice: need n >= 2, 0 <= jitter < 0.5, positive box/area/modulus");
+  std::mt19937_64 rng(seed);
+  const double a = 2.0 * box_half / (n - 1);
+  auto id = [n](int i, int j, int k) { return (i * n + j) * n + k; };
+  std::vector<double> coords(3 * static_cast<size_t>(n) * n * n);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) {
+        const int idx[3] = {i, j, k};
+        for (int ax = 0; ax < 3; ++ax) {
+          double x = -box_half + idx[ax] * a;
+          if (idx[ax] == 0) x = -box_half;
+          else if (idx[ax] == n - 1) x = box_half;
+          else x += jitter * a * (2.0 * u01(rng) - 1.0);
+          coords[3 * static_cast<size_t>(id(i, j, k)) + ax] = x;
+        }
+      }
+  std::vector<int32_t> fn;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) {
+        const int v = id(i, j, k);
+        if (i + 1 < n) fn.insert(fn.end(), {v, id(i + 1, j, k)});
+        if (j + 1 < n) fn.insert(fn.end(), {v, id(i, j + 1, k)});
+        if (k + 1 < n) fn.insert(fn.end(), {v, id(i, j, k + 1)});
+      }
+  const int axis_bonds = static_cast<int>(fn.size() / 2);
+  if (fibers < axis_bonds)
+    return fail(FIBRA_E_CONFIG, "lattice: fibers below the " + std::to_string(axis_bonds) +
+                                    " axis bonds of an n^3 lattice");
+  std::vector<std::pair<int32_t, int32_t>> diag;  // both diagonals of every lattice square
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) {
+        if (i + 1 < n && j + 1 < n) {
+          diag.push_back({id(i, j, k), id(i + 1, j + 1, k)});
+          diag.push_back({id(i + 1, j, k), id(i, j + 1, k)});
+        }
+        if (j + 1 < n && k + 1 < n) {
+          diag.push_back({id(i, j, k), id(i, j + 1, k + 1)});
+          diag.push_back({id(i, j + 1, k), id(i, j, k + 1)});
+        }
+        if (i + 1 < n && k + 1 < n) {
+          diag.push_back({id(i, j, k), id(i + 1, j, k + 1)});
+          diag.push_back({id(i + 1, j, k), id(i, j, k + 1)});
+        }
+      }
+  const size_t extra = static_cast<size_t>(fibers - axis_bonds);
+  if (extra > diag.size())
+    return fail(FIBRA_E_CONFIG, "lattice: more fibers than axis bonds plus face diagonals");
+  for (size_t i = 0; i < extra; ++i) {  // partial Fisher-Yates
+    const size_t r = i + static_cast<size_t>(rng() % (diag.size() - i));
+    std::swap(diag[i], diag[r]);
+  }
+  std::sort(diag.begin(), diag.begin() + static_cast<long>(extra));
+  for (size_t i = 0; i < extra; ++i) fn.insert(fn.end(), {diag[i].first, diag[i].second});
+  const size_t m = fn.size() / 2;
+  return build_network(std::move(coords), std::move(fn), std::vector<double>(m, area),
+                       std::vector<double>(m, modulus), box_half, tol_bnd, net);
+}
+
 int generate_network(const fibra_netgen_spec& spec, uint64_t seed, Network& net) {
   const int rc = validate(spec);
   if (rc) return rc;

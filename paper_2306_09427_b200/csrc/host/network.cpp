@@ -227,6 +227,21 @@ int fibra_network_generate(const fibra_netgen_spec* spec, uint64_t seed, fibra_n
   return FIBRA_OK;
 }
 
+int fibra_network_generate_lattice(int32_t n_side, int32_t fibers, double jitter, double area,
+                                   double modulus, double box_half, double tol_bnd,
+                                   uint64_t seed, fibra_network** out) {
+  if (!out) return fibra_b200::fail(FIBRA_E_ARG, "bad arguments");
+  auto* h = new fibra_network;
+  const int rc = fibra_b200::generate_lattice(n_side, fibers, jitter, area, modulus, box_half,
+                                              tol_bnd, seed, h->net);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return FIBRA_OK;
+}
+
 int fibra_network_read(const char* path, double box_half, double tol_bnd, fibra_network** out) {
   auto* h = new fibra_network;
   const int rc = fibra_b200::read_network(path, box_half, tol_bnd, h->net);

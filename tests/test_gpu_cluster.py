@@ -140,3 +140,35 @@ def test_cluster_identity_and_collapse(mid_net):
     assert br.records[1]["status"] == 3 and status[1] == 3
     check_records(br, resp, status, tangent=False)
     check_states(st, ost, points=[0, 2])
+
+
+def lattice_pair(n, m, seed):
+    pn = P.generate_lattice_network(n, m, seed)
+    on = O.Network(pn.coords, pn.fiber_nodes[:, 0], pn.fiber_nodes[:, 1], pn.fiber_area,
+                   pn.fiber_modulus, pn.box_half)
+    return pn, on
+
+
+def test_cluster_config4_lattice_capped(oracle_lib):
+    """A config-4 sized RVE (50k fibers, 12.2k nodes) on a 16-CTA cluster: the full state
+    after an iteration cap, bitwise."""
+    pn, on = lattice_pair(23, 50000, 1)
+    F = batch_F(2)
+    relax = P.RelaxConfig(max_iterations=300)
+    br, st, shapes = run([pn], [0, 0], F, tangent=False, relax=relax)
+    assert shapes[0]["cluster"] == 16
+    resp, status, ost = oracle_batch([on], [0, 0], F, tangent=False,
+                                     relax=O.RelaxConfig(max_iterations=300))
+    assert list(status) == [6, 6] and br.failed == [0, 1]
+    check_states(st, ost)
+
+
+def test_cluster_lattice_converged(oracle_lib):
+    """A mid-size lattice relaxed to convergence, stress and tangent bitwise."""
+    pn, on = lattice_pair(12, 6000, 5)
+    F = batch_F(2)
+    br, st, shapes = run([pn], [0, 0], F, tangent=True)
+    assert shapes[0]["cluster"] >= 2
+    resp, status, ost = oracle_batch([on], [0, 0], F, tangent=True)
+    check_records(br, resp, status, tangent=True)
+    check_states(st, ost)

@@ -98,6 +98,53 @@ def test_file_roundtrip_and_reference_reader(tmp_path):
         assert np.array_equal(rn.packed_ref.view(np.uint64), pn.packed_ref_coords.view(np.uint64))
 
 
+def test_lattice_generator_config4(tmp_path):
+    """Builder-side lattice for config-4 sizes: deterministic, face nodes on the
+    box (boundary set = all lattice face nodes), written in the reference format and re-read
+    (by the reference's own reader when oracle/_ref is built) with identical packing."""
+    n, m = 23, 50000
+    a = P.generate_lattice_network(n, m, 1)
+    b = P.generate_lattice_network(n, m, 1)
+    assert np.array_equal(a.coords.view(np.uint64), b.coords.view(np.uint64))
+    assert np.array_equal(a.fiber_nodes, b.fiber_nodes)
+    assert len(a.coords) == n ** 3 and len(a.fiber_nodes) == m
+    assert len(a.boundary_nodes) == n ** 3 - (n - 2) ** 3
+    on_face = (np.abs(np.abs(a.coords) - 0.5) == 0).any(axis=1)
+    assert np.array_equal(np.nonzero(on_face)[0], np.sort(a.boundary_nodes))
+    assert not np.array_equal(P.generate_lattice_network(n, m, 2).coords, a.coords)
+    small = P.generate_lattice_network(6, 700, 4)
+    path = tmp_path / "lattice.txt"
+    small.write_file(path)
+    back = P.FiberNetwork.read_file(path)
+    assert np.array_equal(back.packed_ref_coords.view(np.uint64), small.packed_ref_coords.view(np.uint64))
+    if O.ref_available():
+        rn = O.ref_read(path)
+        assert np.array_equal(rn.packed_of_dof, small.packed_of_dof)
+    with pytest.raises(P.ConfigError, match="axis bonds"):
+        P.generate_lattice_network(6, 100, 1)
+
+
+def cluster_report(net, C, T, FPT, NPT):
+    out = np.zeros(8, np.int64)
+    d = net.desc()
+    _capi.load().fibra_cluster_report(d, C, T, FPT, NPT, out.ctypes.data_as(_capi._lp))
+    return out
+
+
+def test_cluster_partition_capacities():
+    """Config-3/4 networks fit the cluster kernel shapes: a 5k-fiber knn RVE on 2 CTAs of
+    (512, 7, 2), the 50k-fiber lattice on 16; parts balanced to a few percent."""
+    knn5k = P.generate_network(P.NetGenSpec(style="knn", nodes=1250, fibers=5000, neighbors=10), 3)
+    r = cluster_report(knn5k, 2, 512, 7, 2)
+    assert r[0] == 1 and r[1] <= 7 * 480 and r[1] - r[2] <= 0.05 * r[1]
+    assert cluster_report(knn5k, 4, 384, 3, 1)[0] == 0  # 1.25k fibers per CTA > 3 x 352
+    lat = P.generate_lattice_network(23, 50000, 1)
+    r = cluster_report(lat, 16, 512, 7, 2)
+    assert r[0] == 1 and r[1] <= 7 * 480 and r[3] <= 1024
+    assert 24 * (1024 + 2 + r[4]) < 65536  # 16-bit x-record offsets
+    assert cluster_report(lat, 8, 512, 7, 2)[0] == 0
+
+
 def test_network_errors_follow_reference_taxonomy(tmp_path):
     with pytest.raises(P.ConfigError, match="duplicate fiber"):
         P.FiberNetwork.from_arrays([[-0.5, 0, 0], [0.5, 0, 0]], [[0, 1], [1, 0]])
