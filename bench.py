@@ -2,14 +2,20 @@
 """Benchmark of the B200 batched RVE solver (BASELINE.json metric, config 2).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--tangent]
+                  [--config 2|3|4|5]
 
-A step = one batch_response over one shard of synthetic RVEs: 1,024 same-topology
+Default (the headline, BASELINE configs[1]): a step = one batch_response over one shard of
+synthetic RVEs: 1,024 same-topology
 ~1k-fiber knn RVEs (375 nodes / 1000 fibers, seed 1 = the config-1 network) with distinct
 deformation gradients (mt19937_64(55) recipe of test_batch.cpp:149-157), each relaxed to
 convergence by DR followed by homogenized stress ("stress only", BASELINE configs[1]).
 With --tangent every point also runs the 6 warm-started probes and the tangent (config 5).
 Under torchrun each rank solves its own 1,024 points (weak scaling) and the result
 records are gathered with one NCCL all-gather.
+--config 3|4|5 (strong scaling, the fixed batch is cut into fiber-weighted
+contiguous shards): 3 = 16,384 heterogeneous knn RVEs of 500-5k fibers (one network per
+point), 4 = 64 jittered-lattice RVEs of 50k fibers (16-CTA clusters), 5 = the first 4,096
+config-3 RVEs with base + 6 probes + tangent.
 
 Headline line (rank 0, one JSON line):
   value    RVE-solves/s over all ranks with F resident in HBM (device-timed, CUDA events,
@@ -38,6 +44,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "RVE solves/s (DR to convergence + homogenized stress), config 2"
+METRICS = {2: METRIC,
+           3: "RVE solves/s (DR to convergence + homogenized stress), config 3",
+           4: "RVE solves/s (DR to convergence + homogenized stress), config 4",
+           5: "RVE responses/s (base + 6 probes, stress + tangent), config 5"}
+DEFAULT_POINTS = {2: 1024, 3: 16384, 4: 64, 5: 4096}
 UNIT = "RVE-solves/s"
 POINTS = 1024
 NET_SEED = 1
@@ -49,51 +60,88 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--points", type=int, default=POINTS)
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5])
+    ap.add_argument("--points", type=int, default=None,
+                    help="config 2: points per GPU; configs 3-5: points in the whole batch")
     ap.add_argument("--tangent", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.points is None:
+        a.points = DEFAULT_POINTS[a.config]
+    if a.config == 5:
+        a.tangent = True
+    return a
 
 
-def workload(points, world, rank, tangent):
+def workload(args, world, rank):
+    """(networks, entry_of_point, F (n, 9), description, global point count, scaling) of
+    this rank's shard."""
     import paper_2306_09427_b200 as P
-    from paper_2306_09427_b200.synth import batch_F, config1_spec
-    net = P.generate_network(config1_spec(), NET_SEED)
-    F_all = batch_F(points * world)
-    F = np.ascontiguousarray(F_all[rank * points:(rank + 1) * points]).reshape(points, 9)
-    desc = (f"config{5 if tangent else 2}: {points} same-topology knn RVEs per GPU "
-            f"(375 nodes/1000 fibers, seed {NET_SEED}, n_free {net.n_free}), distinct F "
-            f"(mt19937_64(55) recipe), {'base + 6 probes + tangent' if tangent else 'stress only'}")
-    return net, F, desc
+    from paper_2306_09427_b200 import synth
+    from paper_2306_09427_b200.shard import shard_ranges
+    tangent = args.tangent
+    if args.config == 2:
+        points = args.points
+        net = P.generate_network(synth.config1_spec(), NET_SEED)
+        F_all = synth.batch_F(points * world)
+        F = np.ascontiguousarray(F_all[rank * points:(rank + 1) * points]).reshape(points, 9)
+        desc = (f"config{5 if tangent else 2}: {points} same-topology knn RVEs per GPU "
+                f"(375 nodes/1000 fibers, seed {NET_SEED}, n_free {net.n_free}), distinct F "
+                f"(mt19937_64(55) recipe), {'base + 6 probes + tangent' if tangent else 'stress only'}")
+        return [net], np.zeros(points, np.int32), F, desc, points * world, "weak"
+    total = args.points
+    if args.config == 4:
+        sizes = np.full(total, 50000)
+        make = synth.config4_network
+    else:
+        sizes = np.array([synth.config3_size(p)[0] for p in range(total)])
+        make = synth.config3_network
+    lo, hi = shard_ranges(sizes, world)[rank]
+    nets = synth.parallel_networks(make, range(lo, hi))
+    F = np.ascontiguousarray(synth.batch_F(total)[lo:hi]).reshape(hi - lo, 9)
+    kind = {3: "heterogeneous knn RVEs of 500-5k fibers (SURVEY 8d recipe, one network per point)",
+            4: "jittered-lattice RVEs of 50k fibers / 12,167 nodes (16-CTA clusters)",
+            5: "config-3 RVEs (first 4,096), base + 6 warm probes + tangent"}[args.config]
+    desc = (f"config{args.config}: {total} {kind}, distinct F (mt19937_64(55) recipe), "
+            f"fiber-weighted contiguous shards")
+    return nets, np.arange(hi - lo, dtype=np.int32), F, desc, total, "strong"
 
 
-def cpu_sample_rate(F, n_workers, sample, tangent):
-    """Reference CPU implementation on the host cores: oracle/_ref (reference TUs) when
-    built, else the oracle restatement.  Returns (rve_solves_per_s, kind, seconds)."""
+def sample_points(n, sample):
+    """Bounded CPU sample: evenly spaced points of the shard (all of them when small)."""
+    return np.unique(np.linspace(0, n - 1, min(n, sample)).astype(int))
+
+
+def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
+    """Reference CPU implementation on the host cores over a bounded sample of the workload:
+    oracle/_ref (the reference's own translation units) for the headline config 2, else the
+    oracle restatement.  Returns (rve_solves_per_s, kind, seconds, iterations, n_sampled)."""
     import oracle as O
     from paper_2306_09427_b200.synth import config1_spec
-    Fs = F[:sample]
-    spec = config1_spec()
-    if O.ref_available() and not tangent:
+    if args.config == 2 and O.ref_available() and not args.tangent:
+        Fs = F[:sample]
+        spec = config1_spec()
         rnet = O.ref_generate("knn", nodes=spec.nodes, fibers=spec.fibers,
                               neighbors=spec.neighbors, merge_radius=spec.merge_radius,
                               seed=NET_SEED)
         t0 = time.perf_counter()
         sig, iters, status = O.ref_batch_stress(rnet, Fs, workers=n_workers)
         dt = time.perf_counter() - t0
-        return len(Fs) / dt, "reference", dt, int(iters.sum())
+        return len(Fs) / dt, "reference", dt, int(iters.sum()), len(Fs)
     O.build(ref=False)
-    import paper_2306_09427_b200 as P
-    pn = P.generate_network(spec, NET_SEED)
-    on = O.Network(pn.coords, pn.fiber_nodes[:, 0], pn.fiber_nodes[:, 1], pn.fiber_area,
-                   pn.fiber_modulus)
-    st = O.PackedStates.fresh([on], [0] * len(Fs))
+    idx = np.arange(min(sample, len(F))) if args.config == 2 else sample_points(len(F), sample)
+    used = sorted({int(eop[i]) for i in idx})
+    remap = {e: k for k, e in enumerate(used)}
+    onets = [O.Network(nets[e].coords, nets[e].fiber_nodes[:, 0], nets[e].fiber_nodes[:, 1],
+                       nets[e].fiber_area, nets[e].fiber_modulus, nets[e].box_half) for e in used]
+    seop = [remap[int(eop[i])] for i in idx]
+    st = O.PackedStates.fresh(onets, seop)
     t0 = time.perf_counter()
-    resp, status = O.batch_response([on], [0] * len(Fs), st, Fs, want_tangent=tangent,
+    resp, status = O.batch_response(onets, seop, st, F[idx], want_tangent=args.tangent,
                                     n_threads=n_workers)
     dt = time.perf_counter() - t0
-    return len(Fs) / dt, "port", dt, int(sum(r["relax_iterations"] for r in resp))
+    return len(idx) / dt, "port", dt, int(sum(r["relax_iterations"] for r in resp)), len(idx)
 
 
 def run_reference(args, rank, world):
@@ -101,27 +149,28 @@ def run_reference(args, rank, world):
         return
     n_workers = os.cpu_count() or 1
     import paper_2306_09427_b200  # noqa: F401  (network generator only; no GPU use)
-    _, F, desc = workload(args.points, 1, 0, args.tangent)
+    nets, eop, F, desc, total, scaling = workload(args, 1, 0)
     sample = max(8, 2 * n_workers)
     for _ in range(max(1, min(args.warmup, 1))):
-        cpu_sample_rate(F, n_workers, min(sample, n_workers), args.tangent)
-    rates, secs, iters = [], 0.0, 0
+        cpu_sample_rate(args, nets, eop, F, n_workers, min(sample, n_workers))
+    secs, iters, done = 0.0, 0, 0
     kind = "port"
     for _ in range(args.steps):
-        r, kind, dt, its = cpu_sample_rate(F, n_workers, sample, args.tangent)
-        rates.append(r)
+        r, kind, dt, its, k = cpu_sample_rate(args, nets, eop, F, n_workers, sample)
         secs += dt
         iters += its
-    value = args.steps * sample / secs
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": desc, "sample_points_per_step": sample},
+        done += k
+    value = done / secs
+    which = "first" if args.config == 2 else "evenly spaced"
+    line = {"impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "sample_points_per_step": done // args.steps},
             "dr_iter_rve_per_s": iters / secs,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_workers, "kind": kind,
-                             "sample": f"first {sample} points of the workload per step, "
-                                       f"{n_workers} WorkerPool threads"},
+                             "sample": f"{which} {done // args.steps} points of the workload per "
+                                       f"step, {n_workers} WorkerPool threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -185,18 +234,23 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    net, F, desc = workload(args.points, world, rank, args.tangent)
+    nets, eop, F, desc, total, scaling = workload(args, world, rank)
     n = len(F)
-    lib = P.RveLibrary([net])
-    assign = P.BatchAssignment(np.zeros(n, np.int32))
+    lib = P.RveLibrary(nets, policy="explicit", explicit_assignment=[int(e) for e in eop])
+    assign = P.BatchAssignment(eop)
     stream = torch.cuda.Stream(device=local)  # explicit stream shared by torch and the solver
     torch.cuda.set_stream(stream)
     db = P.DeviceBatch(lib, assign, device=local, stream=stream.cuda_stream)
     peak = db.fp64_peak()  # FP64-pipe roofline denominator, measured while the GPU is idle
     rec_bytes = P.RESULT_DTYPE.itemsize
     F_dev = torch.from_numpy(F).to(f"cuda:{local}")
-    out_dev = torch.empty(n * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
-    gathered = torch.empty(world * n * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
+    # the all-gather moves equal-size buffers: shards are padded to the largest one
+    counts = torch.tensor([n], dtype=torch.int64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.MAX)
+    n_pad = int(counts.item())
+    out_dev = torch.zeros(n_pad * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
+    gathered = torch.empty(world * n_pad * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
     law, rcfg, scfg = P.FiberLaw(), P.RelaxConfig(), P.StiffnessConfig()
 
@@ -232,8 +286,11 @@ def main():
         fiber_iters += s["fiber_iterations"]
         launches += s["kernel_launches"]
     clk = clocks.stop()
-    rec = np.frombuffer(out_dev.cpu().numpy().tobytes(), dtype=P.RESULT_DTYPE)
-    failed = int((rec["status"] != 0).sum())
+    rec = np.frombuffer(out_dev.cpu().numpy().tobytes(), dtype=P.RESULT_DTYPE)[:n]
+    failed_t = torch.tensor([int((rec["status"] != 0).sum())], device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(failed_t)
+    failed = int(failed_t.item())
 
     t = torch.tensor([total_ms, dr_ms], dtype=torch.float64, device=f"cuda:{local}")
     tot_iters = torch.tensor([iters, pipe_ops, fiber_iters], dtype=torch.float64,
@@ -243,10 +300,10 @@ def main():
         dist.all_reduce(tot_iters, op=dist.ReduceOp.SUM)
     max_total_ms, max_dr_ms = t.tolist()
     all_iters, all_pipe, all_fib = tot_iters.tolist()
-    value = world * n * args.steps / (max_total_ms * 1e-3)
+    value = total * args.steps / (max_total_ms * 1e-3)
 
     # ---- end to end through the public API with host buffers ----
-    st_host, _ = P.init_batch(np.zeros(n, np.int32), lib, 0)
+    st_host, _ = P.init_batch(np.zeros(n, np.int32), lib, 0)  # explicit policy -> eop
     st_host.offsets = st_host.offsets  # fresh zero-filled PackedStates (init_batch)
     e2e_s = 0.0
     for i in range(args.e2e_steps + 1):
@@ -258,7 +315,8 @@ def main():
         br = P.batch_response(lib, assign, st_host, law, F, rcfg, scfg,
                               want_tangent=args.tangent, device=local)
         if world > 1:
-            g = torch.from_numpy(br.records.view(np.uint8).copy()).to(f"cuda:{local}")
+            g = torch.zeros(n_pad * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
+            g[:n * rec_bytes] = torch.from_numpy(br.records.view(np.uint8).copy()).to(f"cuda:{local}")
             dist.all_gather_into_tensor(gathered, g)
             torch.cuda.synchronize()
         dt = time.perf_counter() - t0
@@ -267,7 +325,7 @@ def main():
     et = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_val = world * n * args.e2e_steps / et.item()
+    e2e_val = total * args.e2e_steps / et.item()
     tot = int(st_host.total_dofs())
     h2d = n * 72 + tot * 8 + n * (8 + 8 + 1)
     d2h = n * rec_bytes + 7 * tot * 8 + n * (8 + 8 + 1)
@@ -275,11 +333,11 @@ def main():
     if rank == 0:
         achieved = all_pipe / world / (max_dr_ms * 1e-3)  # per-GPU FP64-pipe lane-ops/s
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "points_per_gpu": n, "global_points": world * n,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "points_per_gpu": n, "global_points": total,
                        "l2": "flushed between timed steps (256 MiB device write)",
                        "parallelism": f"dp{world} (independent RVE shards, 1 NCCL all-gather "
                                       "of result records per step)"},
@@ -299,9 +357,10 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             nw = os.cpu_count() or 1
             sample = max(8, nw)
-            r, kind, secs, its = cpu_sample_rate(F, nw, sample, args.tangent)
+            r, kind, secs, its, k = cpu_sample_rate(args, nets, eop, F, nw, sample)
+            which = "first" if args.config == 2 else "evenly spaced"
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": nw, "kind": kind,
-                                    "sample": f"first {sample} points of this workload on "
+                                    "sample": f"{which} {k} points of this workload on "
                                               f"{nw} host threads ({secs:.1f} s, {its} DR "
                                               "iterations)"}
         print(json.dumps(line), flush=True)

@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -714,21 +717,44 @@ bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& 
   return smem <= static_cast<size_t>(c->max_smem);
 }
 
-template <class Vec, class Tp>
-int upload_vec(fibra_ctx* c, DeviceEntry& de, Tp** dst, const Vec& vec) {
-  using Ep = typename Vec::value_type;
-  Ep* p = nullptr;
-  FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&p), std::max<size_t>(vec.size(), 1) * sizeof(Ep)));
-  de.allocs.push_back(p);
-  if (!vec.empty())
-    FB_CUDA(c, cudaMemcpy(p, vec.data(), vec.size() * sizeof(Ep), cudaMemcpyHostToDevice));
-  *dst = reinterpret_cast<Tp*>(p);
-  return FIBRA_OK;
+// Host image of one library entry's device arrays: built without CUDA calls (so entries
+// are built in parallel), then committed with one allocation and one copy.
+struct Arena {
+  std::vector<unsigned char> host;
+  std::vector<std::pair<void*, size_t>> fixes;  // device pointer fields -> arena offsets
+  size_t reserve(size_t bytes) {
+    const size_t off = (host.size() + 15) & ~static_cast<size_t>(15);
+    host.resize(off + std::max<size_t>(bytes, 16));
+    return off;
+  }
+  template <class Vec, class Tp>
+  void add(Tp** dst, const Vec& vec) {
+    using Ep = typename Vec::value_type;
+    const size_t off = reserve(vec.size() * sizeof(Ep));
+    if (!vec.empty()) std::memcpy(host.data() + off, vec.data(), vec.size() * sizeof(Ep));
+    fixes.push_back({static_cast<void*>(dst), off});
+  }
+};
+
+// kernel-class capacities one entry needs (merged into its KClass after the parallel build)
+struct Caps {
+  int ts = 0, x_bytes = 0, g_bytes = 0, csr_cap = 0, push_cap = 0;
+  long long scratch_stride = 0;
+};
+
+void merge_caps(KClass& K, const Caps& e) {
+  K.ts = e.ts;
+  K.ck_stride = e.ts;
+  K.x_bytes = std::max(K.x_bytes, e.x_bytes);
+  K.g_bytes = std::max(K.g_bytes, e.g_bytes);
+  K.csr_cap = std::max(K.csr_cap, e.csr_cap);
+  K.push_cap = std::max(K.push_cap, e.push_cap);
+  K.scratch_stride = std::max(K.scratch_stride, e.scratch_stride);
 }
 
 // resident-kernel entry: slot arrays, g*d record colouring, step-major CSR pairs
-int upload_resident_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
-                          const fibra_net_desc& d, const Variant& v, KClass& K) {
+void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc& d,
+                          const Variant& v, Arena& A, Caps& K) {
   const Schedule& S = de.sched;
   const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS, TS+1
   const int FS = S.fiber_slots;
@@ -807,30 +833,27 @@ int upload_resident_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
   E.max_lump = P.max_lump;
   E.max_ea = d.max_ea;
   E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
-  int rc;
-  if ((rc = upload_vec(c, de, &E.slot_pn, slot_pn))) return rc;
-  if ((rc = upload_vec(c, de, &E.slot_ref, slot_ref))) return rc;
-  if ((rc = upload_vec(c, de, &E.slot_lump, slot_lump))) return rc;
-  if ((rc = upload_vec(c, de, &E.csr_npairs, npairs))) return rc;
-  if ((rc = upload_vec(c, de, &E.csr_pairs, ent))) return rc;
-  if ((rc = upload_vec(c, de, &E.fib_ab, fab))) return rc;
-  if ((rc = upload_vec(c, de, &E.fib_g, fg))) return rc;
-  if ((rc = upload_vec(c, de, &E.fib_id, fid))) return rc;
-  if ((rc = upload_vec(c, de, &E.fib_l0, fl0))) return rc;
-  if ((rc = upload_vec(c, de, &E.fib_ea, fea))) return rc;
+  A.add(&E.slot_pn, slot_pn);
+  A.add(&E.slot_ref, slot_ref);
+  A.add(&E.slot_lump, slot_lump);
+  A.add(&E.csr_npairs, npairs);
+  A.add(&E.csr_pairs, ent);
+  A.add(&E.fib_ab, fab);
+  A.add(&E.fib_g, fg);
+  A.add(&E.fib_id, fid);
+  A.add(&E.fib_l0, fl0);
+  A.add(&E.fib_ea, fea);
   K.ts = TS;
-  K.ck_stride = TS;
-  K.x_bytes = std::max(K.x_bytes, static_cast<int>(align16(24 * static_cast<size_t>(TS + 2))));
+  K.x_bytes = static_cast<int>(align16(24 * static_cast<size_t>(TS + 2)));
   const size_t gb = std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M));
-  K.g_bytes = std::max(K.g_bytes, static_cast<int>(align16(gb)));
-  K.csr_cap = std::max(K.csr_cap, static_cast<int>(ent.size()));
-  return FIBRA_OK;
+  K.g_bytes = static_cast<int>(align16(gb));
+  K.csr_cap = static_cast<int>(ent.size());
 }
 
 // cluster-kernel entry: one PartDev per CTA (host/cluster_schedule.hpp)
-int upload_cluster_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
-                         const fibra_net_desc& d, const ClusterPlan& plan,
-                         const ClusterVariant& v, KClass& K) {
+void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc& d,
+                         const ClusterPlan& plan, const ClusterVariant& v, Arena& A,
+                         std::vector<PartDev>& parts, size_t& parts_off, Caps& K) {
   const int C = plan.C, T = v.T, TS = v.NPT * v.T, FS = v.FPT * v.T, FT = T - 32;
   std::vector<std::vector<int>> inc(P.N);  // incident fibers per node, ascending id
   for (int f = 0; f < P.M; ++f) {
@@ -856,7 +879,7 @@ int upload_cluster_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
       push[o][plan.slot_of_pn[pn]].push_back((q << 16) | (24 * (TS + 2 + static_cast<int>(h))));
     }
   }
-  std::vector<PartDev> parts(C);
+  parts.assign(C, PartDev{});
   int max_pairs_all = 0, max_push_all = 0, max_rec = 0;
   for (int q = 0; q < C; ++q) {
     const ClusterPart& Q = plan.parts[q];
@@ -929,22 +952,21 @@ int upload_cluster_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
     D.max_pairs = max_pairs;
     D.max_push = max_push;
     D.n_records = zero_rec + 1;
-    int rc;
-    if ((rc = upload_vec(c, de, &D.slot_pn, slot_pn))) return rc;
-    if ((rc = upload_vec(c, de, &D.slot_ref, slot_ref))) return rc;
-    if ((rc = upload_vec(c, de, &D.slot_lump, slot_lump))) return rc;
-    if ((rc = upload_vec(c, de, &D.csr_npairs, npairs))) return rc;
-    if ((rc = upload_vec(c, de, &D.csr_pairs, ent))) return rc;
-    if ((rc = upload_vec(c, de, &D.push_n, npush))) return rc;
-    if ((rc = upload_vec(c, de, &D.push_dst, pdst))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_ab, fab))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_gt, fgt))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_gh, fgh))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_id, fid))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_l0, fl0))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_ea, fea))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_lt, flt))) return rc;
-    if ((rc = upload_vec(c, de, &D.fib_lh, flh))) return rc;
+    A.add(&D.slot_pn, slot_pn);
+    A.add(&D.slot_ref, slot_ref);
+    A.add(&D.slot_lump, slot_lump);
+    A.add(&D.csr_npairs, npairs);
+    A.add(&D.csr_pairs, ent);
+    A.add(&D.push_n, npush);
+    A.add(&D.push_dst, pdst);
+    A.add(&D.fib_ab, fab);
+    A.add(&D.fib_gt, fgt);
+    A.add(&D.fib_gh, fgh);
+    A.add(&D.fib_id, fid);
+    A.add(&D.fib_l0, fl0);
+    A.add(&D.fib_ea, fea);
+    A.add(&D.fib_lt, flt);
+    A.add(&D.fib_lh, flh);
     max_pairs_all = std::max(max_pairs_all, max_pairs);
     max_push_all = std::max(max_push_all, max_push);
     max_rec = std::max(max_rec, D.n_records);
@@ -959,15 +981,31 @@ int upload_cluster_entry(fibra_ctx* c, DeviceEntry& de, const PackedNet& P,
   E.max_ea = d.max_ea;
   E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
   E.ea0 = P.M > 0 ? P.ea[0] : 1.0;
-  int rc;
-  if ((rc = upload_vec(c, de, &E.parts, parts))) return rc;
+  parts_off = A.reserve(sizeof(PartDev) * C);  // filled at commit, once pointers are known
   K.ts = TS;
-  K.ck_stride = TS;
-  K.x_bytes = std::max(K.x_bytes, static_cast<int>(align16(24ull * (TS + 2 + plan.max_halo))));
-  K.g_bytes = std::max(K.g_bytes, static_cast<int>(align16(24ull * max_rec)));
-  K.csr_cap = std::max(K.csr_cap, max_pairs_all * TS);
-  K.push_cap = std::max(K.push_cap, max_push_all * TS);
-  K.scratch_stride = std::max<long long>(K.scratch_stride, 6LL * P.N + 3LL * P.NFN + P.M);
+  K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + plan.max_halo)));
+  K.g_bytes = static_cast<int>(align16(24ull * max_rec));
+  K.csr_cap = max_pairs_all * TS;
+  K.push_cap = max_push_all * TS;
+  K.scratch_stride = 6LL * P.N + 3LL * P.NFN + P.M;
+}
+
+// one allocation and one copy for an entry's arrays (and, for cluster entries, its PartDev
+// table, whose pointer fields are resolved first)
+int commit_entry(fibra_ctx* c, DeviceEntry& de, Arena& A, std::vector<PartDev>& parts,
+                 size_t parts_off) {
+  unsigned char* base = nullptr;
+  FB_CUDA(c, cudaMalloc(reinterpret_cast<void**>(&base), A.host.size()));
+  de.allocs.push_back(base);
+  for (auto& f : A.fixes) {  // store the device address into the (const T*) field
+    const void* addr = base + f.second;
+    std::memcpy(f.first, &addr, sizeof addr);
+  }
+  if (!parts.empty()) {
+    std::memcpy(A.host.data() + parts_off, parts.data(), sizeof(PartDev) * parts.size());
+    de.cdev.parts = reinterpret_cast<const PartDev*>(base + parts_off);
+  }
+  FB_CUDA(c, cudaMemcpy(base, A.host.data(), A.host.size(), cudaMemcpyHostToDevice));
   return FIBRA_OK;
 }
 
@@ -1044,63 +1082,96 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   free_library(c);
-  std::vector<PackedNet> nets;
-  nets.reserve(n);
   for (int i = 0; i < n; ++i) {
     const fibra_net_desc& d = entries[i];
     if (d.n_nodes <= 0 || d.n_fibers < 0 || d.n_free % 3 != 0)
       return set_err(c, FIBRA_E_ARG, "malformed library entry " + std::to_string(i));
-    nets.push_back(pack(d));
   }
-  // kernel class per entry: the first resident shape that holds it, else the smallest
+  // host work per entry (packing, shape selection, schedules) runs on all host cores
+  const int workers = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+  auto parallel_for = [&](int lo, int hi, const std::function<void(int)>& fn) {
+    std::atomic<int> next(lo);
+    std::vector<std::thread> pool;
+    for (int w = 0; w < std::min(workers, hi - lo); ++w)
+      pool.emplace_back([&] {
+        for (int i; (i = next.fetch_add(1)) < hi;) fn(i);
+      });
+    for (auto& t : pool) t.join();
+  };
+  // kernel shape per entry: the first resident shape that holds it, else the smallest
   // cluster (fewest CTAs) that does
   c->entries.resize(n);
+  std::vector<PackedNet> nets(n);
   std::vector<ClusterPlan> plans(n);
-  for (int i = 0; i < n; ++i) {
+  std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1);
+  parallel_for(0, n, [&](int i) {
+    nets[i] = pack(entries[i]);
     const PackedNet& P = nets[i];
     DeviceEntry& de = c->entries[i];
     de.config_ok = P.ok;
     de.config_err = P.err;
     de.n_nodes = P.N;
     const int mp = max_pairs_of(P);
-    bool cl = false;
-    int vi = -1, C = 1;
-    for (int v = 0; v < kNumVariants && vi < 0; ++v)
-      if (resident_fits(c, P, kVariants[v], mp, de.sched)) vi = v;
-    for (int cc = 2; cc <= 16 && vi < 0; cc *= 2)
-      for (int v = 0; v < kNumClusterVariants && vi < 0; ++v)
+    for (int v = 0; v < kNumVariants && kind_vi[i] < 0; ++v)
+      if (resident_fits(c, P, kVariants[v], mp, de.sched)) kind_vi[i] = v;
+    for (int cc = 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
+      for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v)
         if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
-          vi = v;
-          C = cc;
-          cl = true;
+          kind_vi[i] = v;
+          kind_C[i] = cc;
+          kind_cl[i] = 1;
         }
-    if (vi < 0)
+  });
+  for (int i = 0; i < n; ++i) {
+    if (kind_vi[i] < 0)
       return set_err(c, FIBRA_E_ARG, "RVE library entry " + std::to_string(i) + " (" +
-                                         std::to_string(P.M) + " fibers, " +
-                                         std::to_string(P.N) + " nodes) exceeds a 16-CTA cluster");
+                                         std::to_string(nets[i].M) + " fibers, " +
+                                         std::to_string(nets[i].N) +
+                                         " nodes) exceeds a 16-CTA cluster");
+    const bool cl = kind_cl[i] != 0;
     int k = 0;
     const int nk = static_cast<int>(c->classes.size());
-    while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].vi == vi && c->classes[k].C == C)) ++k;
+    while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].vi == kind_vi[i] &&
+                       c->classes[k].C == kind_C[i]))
+      ++k;
     if (k == nk) {
       if (nk == kMaxClasses) return set_err(c, FIBRA_E_ARG, "too many kernel classes in one library");
       KClass K;
       K.cluster = cl;
-      K.vi = vi;
-      K.C = C;
+      K.vi = kind_vi[i];
+      K.C = kind_C[i];
       c->classes.push_back(K);
     }
-    de.cls = k;
+    c->entries[i].cls = k;
     KClass& K = c->classes[k];
+    const PackedNet& P = nets[i];
     for (int f = 1; f < P.M && K.uniform_ea; ++f) K.uniform_ea = (P.ea[f] == P.ea[0]);
   }
-  for (int i = 0; i < n; ++i) {
-    DeviceEntry& de = c->entries[i];
-    KClass& K = c->classes[de.cls];
-    const int rc = K.cluster
-                       ? upload_cluster_entry(c, de, nets[i], entries[i], plans[i],
-                                              kClusterVariants[K.vi], K)
-                       : upload_resident_entry(c, de, nets[i], entries[i], kVariants[K.vi], K);
-    if (rc) return rc;
+  // device arrays: built in parallel batches (bounded host memory), committed in order
+  const int batch = 256;
+  for (int lo = 0; lo < n; lo += batch) {
+    const int hi = std::min(n, lo + batch);
+    std::vector<Arena> arenas(hi - lo);
+    std::vector<std::vector<PartDev>> parts(hi - lo);
+    std::vector<size_t> parts_off(hi - lo, 0);
+    std::vector<Caps> caps(hi - lo);
+    parallel_for(lo, hi, [&](int i) {
+      DeviceEntry& de = c->entries[i];
+      const KClass& K = c->classes[de.cls];
+      if (K.cluster)
+        build_cluster_entry(de, nets[i], entries[i], plans[i], kClusterVariants[K.vi],
+                            arenas[i - lo], parts[i - lo], parts_off[i - lo], caps[i - lo]);
+      else
+        build_resident_entry(de, nets[i], entries[i], kVariants[K.vi], arenas[i - lo],
+                             caps[i - lo]);
+    });
+    for (int i = lo; i < hi; ++i) {
+      const int rc = commit_entry(c, c->entries[i], arenas[i - lo], parts[i - lo], parts_off[i - lo]);
+      if (rc) return rc;
+      merge_caps(c->classes[c->entries[i].cls], caps[i - lo]);
+      nets[i] = PackedNet();
+      plans[i] = ClusterPlan();
+    }
   }
   for (KClass& K : c->classes) {
     if (K.smem() > static_cast<size_t>(c->max_smem))

@@ -66,3 +66,53 @@ def config1_spec():
     """Config-1 network: knn 375 nodes / 1000 fibers, neighbors 10."""
     from . import NetGenSpec
     return NetGenSpec(style="knn", nodes=375, fibers=1000, neighbors=10, merge_radius=0.05)
+
+
+def splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+CONFIG3_POINTS = 16384
+
+
+def config3_size(p: int):
+    """Config-3 RVE p: M = 500 + hash(p) mod 4501 fibers, N = round(M / r) nodes
+    with r = 2.67 up to 1,500 fibers and 4 above (denser networks pass the reference's
+    attachment check at 5k fibers)."""
+    m = 500 + splitmix64(p) % 4501
+    r = 2.67 if m <= 1500 else 4.0
+    return m, int(round(m / r))
+
+
+def config3_network(p: int):
+    """knn network of config-3 RVE p, seed p + 1; on ConfigError the seed advances by the
+    batch size."""
+    from . import ConfigError, NetGenSpec, generate_network
+    m, n = config3_size(p)
+    seed = p + 1
+    for _ in range(64):
+        try:
+            return generate_network(NetGenSpec(style="knn", nodes=n, fibers=m, neighbors=10,
+                                               merge_radius=0.05), seed)
+        except ConfigError:
+            seed += CONFIG3_POINTS
+    raise ConfigError(f"config-3 RVE {p}: no valid seed")
+
+
+def config4_network(p: int):
+    """Config-4 RVE p: a ~50k-fiber jittered lattice (23^3 nodes), seed p + 1 (the reference
+    knn generator cannot build this size)."""
+    from . import generate_lattice_network
+    return generate_lattice_network(23, 50000, p + 1)
+
+
+def parallel_networks(make, points, threads=None):
+    """Build networks for `points` with `make` on a thread pool (the C generator releases
+    the GIL through ctypes)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=threads or os.cpu_count() or 1) as ex:
+        return list(ex.map(make, points))
