@@ -25,6 +25,7 @@
 #pragma once
 
 #include <cstddef>
+#include <type_traits>
 
 #include "dr_kernel.cuh"
 
@@ -41,7 +42,7 @@ struct PartDev {            // one CTA's share of one RVE
   const int* push_n;        // [TS] halo copies of this slot's x
   const int* push_dst;      // [max_push][TS] rank << 16 | byte offset of the halo x record
   const int* fib_ab;        // [FS] x byte offsets: tail | head << 16 (own or halo slot)
-  const int* fib_gt;        // [FS] byte offset of the fiber's local record
+  const int* fib_gt;        // [FS] byte offset of the fiber's local record (= 24*(j*(T-32)+tid))
   const int* fib_gh;        // [FS] rank << 24 | byte offset of its record in the head's CTA, -1
   const int* fib_id;        // [FS] reference fiber id, -1 dummy
   const double* fib_l0;     // [FS]
@@ -92,6 +93,8 @@ __device__ __forceinline__ unsigned cl_id() {
   asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
   return r;
 }
+// barrier.cluster with release/acquire (SASS: MEMBAR.ALL.GPU + UCGABAR_ARV/WAIT + CCTL.IVALL);
+// a relaxed arrive would save ~0.2 us per barrier but gives DSMEM stores no ordering
 __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
                ::: "memory");
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   const double B = P.nonlinearity;
   const int bo = P.law_buckling_off;
 
-  int fab[FPT], fgt[FPT], fgh[FPT];
+  int fab[FPT], fgh[FPT];
   double fl0[FPT], fs[FPT], fmred[FPT];
   int npair[NPT], npush[NPT];
   double nref[NPT][3], ninv[NPT], ncm[NPT];
@@ -218,7 +221,6 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       for (int j = 0; j < FPT; ++j) {
         const int f = j * T + tid;
         fab[j] = Q.fib_ab[f];
-        fgt[j] = Q.fib_gt[f];
         fgh[j] = Q.fib_gh[f];
         fl0[j] = Q.fib_l0[f];
         if (!UEA) fs[j] = P.ea_scale * Q.fib_ea[f];
@@ -362,50 +364,63 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         }
       } else {
         double kmin = INFINITY;
-        bool collapsed = false, fast = true;
-        double dx[FPT], dy[FPT], dz[FPT], g[FPT];
+        bool collapsed = false;
+        // fibers in blocks of <= 4 so one block's temporaries are live at a time (FPT = 7
+        // shapes otherwise spill); each fiber's local record sits at compact slot j*(T-32)+tid
+        auto fiber_block = [&](auto j0c, auto j1c) {
+          constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
+          bool fast = true;
+          double dx[J1 - J0], dy[J1 - J0], dz[J1 - J0], g[J1 - J0];
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) {
-          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
-          dx[j] = xb_[0] - xa_[0];
-          dy[j] = xb_[1] - xa_[1];
-          dz[j] = xb_[2] - xa_[2];
-          bool o1, o2, o3 = true;
-          const double len = sqrt_fast(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j], o1);
-          collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
-          const double stretch = div_fast(len, fl0[j], o2);
-          if (LAW == 0) {
-            g[j] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
-          } else {
-            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
-            const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
-            kmin = smin(kmin, fmred[j] / kt);
+          for (int jj = 0; jj < J1 - J0; ++jj) {
+            const int j = J0 + jj;
+            const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
+            const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+            dx[jj] = xb_[0] - xa_[0];
+            dy[jj] = xb_[1] - xa_[1];
+            dz[jj] = xb_[2] - xa_[2];
+            bool o1, o2, o3 = true;
+            const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
+            collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
+            const double stretch = div_fast(len, fl0[j], o2);
+            if (LAW == 0) {
+              g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+            } else {
+              g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+              const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
+              kmin = smin(kmin, fmred[j] / kt);
+            }
+            fast = fast && o1 && o2 && o3;
           }
-          fast = fast && o1 && o2 && o3;
-        }
-        if (!__all_sync(0xffffffffu, fast)) {
+          if (!__all_sync(0xffffffffu, fast)) {  // rare: special operands -> built-in ops
 #pragma unroll
-          for (int j = 0; j < FPT; ++j) {
-            const double len = sqrt(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j]);
-            const double stretch = len / fl0[j];
-            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            for (int jj = 0; jj < J1 - J0; ++jj) {
+              const int j = J0 + jj;
+              const double len = sqrt(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj]);
+              const double stretch = len / fl0[j];
+              g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            }
           }
-        }
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) {  // +g*d: the tail gathers it negated
-          const double g0 = g[j] * dx[j], g1 = g[j] * dy[j], g2 = g[j] * dz[j];
-          double* gt = sm_at<double>(G, fgt[j]);
-          gt[0] = g0;
-          gt[1] = g1;
-          gt[2] = g2;
-          if (fgh[j] >= 0) {
-            const unsigned a = cl_map(G_sh + (fgh[j] & 0xffffff), static_cast<unsigned>(fgh[j]) >> 24);
-            cl_st_f64(a, g0);
-            cl_st_f64(a + 8, g1);
-            cl_st_f64(a + 16, g2);
+          for (int jj = 0; jj < J1 - J0; ++jj) {  // +g*d: the tail gathers it negated
+            const int j = J0 + jj;
+            const double g0 = g[jj] * dx[jj], g1 = g[jj] * dy[jj], g2 = g[jj] * dz[jj];
+            double* gt = sm_at<double>(G, 24 * (j * (T - 32) + tid));
+            gt[0] = g0;
+            gt[1] = g1;
+            gt[2] = g2;
+            if (fgh[j] >= 0) {
+              const unsigned a = cl_map(G_sh + (fgh[j] & 0xffffff), static_cast<unsigned>(fgh[j]) >> 24);
+              cl_st_f64(a, g0);
+              cl_st_f64(a + 8, g1);
+              cl_st_f64(a + 16, g2);
+            }
           }
-        }
+        };
+        constexpr int B1 = FPT < 4 ? FPT : (FPT + 1) / 2;
+        fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, B1>());
+        if constexpr (B1 < FPT)
+          fiber_block(std::integral_constant<int, B1>(), std::integral_constant<int, FPT>());
         if (collapsed)
           for (unsigned r = 0; r < C; ++r) cl_st_s32(cl_map(ctl_sh + off_collapse, r), 1);
         if (LAW != 0) push_wmin(warp_min(kmin));

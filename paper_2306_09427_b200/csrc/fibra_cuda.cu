@@ -711,8 +711,10 @@ bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& 
     return false;
   const int TS = v.NPT * v.T;
   if (24 * (TS + 2 + plan.max_halo) >= 65536) return false;  // 16-bit x offsets
+  size_t max_h = 0;
+  for (const ClusterPart& q : plan.parts) max_h = std::max(max_h, q.h_fiber.size());
   const size_t smem = align16(24ull * (TS + 2 + plan.max_halo)) +
-                      align16(24ull * (plan.max_records + 17)) + 8ull * TS +
+                      align16(24ull * (v.FPT * (v.T - 32) + max_h + 1)) + 8ull * TS +
                       8ull * max_pairs * TS + 4ull * plan.max_push * TS;
   return smem <= static_cast<size_t>(c->max_smem);
 }
@@ -887,7 +889,11 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     D = PartDev{};
     const int n_own = static_cast<int>(Q.fibers.size());
     const int n_h = static_cast<int>(Q.h_fiber.size());
-    const int zero_rec = n_own + n_h + 16;
+    // records: [one per fiber slot of the fiber threads, compact index k = j*FT + tid (dummy
+    // slots included, so the kernel derives the offset)][copies of remote fibers (heads
+    // here)][zero record]
+    const int own_slots = v.FPT * FT;
+    const int zero_rec = own_slots + n_h;
     std::vector<int> slot_pn(TS, -1);
     std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
     for (int sl = 0; sl < Q.node_slots; ++sl) {
@@ -911,7 +917,7 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
           e = 24 * k;
           if (Q.tail_pn[k] == pn) e |= static_cast<int>(0x80000000u);
         } else {
-          e = 24 * (n_own + hrec[f]);
+          e = 24 * (own_slots + hrec[f]);
         }
         lists[sl].push_back(e);
       }
@@ -929,7 +935,7 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     }
     std::vector<int> fab(FS, (24 * TS) | ((24 * (TS + 1)) << 16)), fgt(FS), fgh(FS, -1), fid(FS, -1);
     std::vector<double> fl0(FS, 0.5), fea(FS, P.M > 0 ? P.ea[0] : 1.0), flt(FS, 1.0), flh(FS, 1.0);
-    for (int fs = 0; fs < FS; ++fs) fgt[fs] = 24 * (n_own + n_h + fs % 16);
+    for (int fs = 0; fs < FS; ++fs) fgt[fs] = 24 * ((fs / T) * FT + fs % T);  // (reducer: unused)
     for (int k = 0; k < n_own; ++k) {
       const int fs = (k / FT) * T + k % FT;
       const int f = Q.fibers[k], tl = Q.tail_pn[k], hd = Q.head_pn[k];
@@ -939,7 +945,7 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
       fgt[fs] = 24 * k;
       if (ph != q)
         fgh[fs] = (ph << 24) |
-                  (24 * (static_cast<int>(plan.parts[ph].fibers.size()) + hrec[f]));
+                  (24 * (own_slots + hrec[f]));
       fid[fs] = f;
       fl0[fs] = P.l0[f];
       fea[fs] = P.ea[f];
@@ -1104,6 +1110,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   std::vector<PackedNet> nets(n);
   std::vector<ClusterPlan> plans(n);
   std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1);
+  // diagnostics: FIBRA_FORCE_CLUSTER=C places every entry on a C-CTA cluster (kernel timing)
+  const char* force_env = getenv("FIBRA_FORCE_CLUSTER");
+  const int force_c = force_env ? atoi(force_env) : 0;
   parallel_for(0, n, [&](int i) {
     nets[i] = pack(entries[i]);
     const PackedNet& P = nets[i];
@@ -1112,9 +1121,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     de.config_err = P.err;
     de.n_nodes = P.N;
     const int mp = max_pairs_of(P);
-    for (int v = 0; v < kNumVariants && kind_vi[i] < 0; ++v)
+    for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
       if (resident_fits(c, P, kVariants[v], mp, de.sched)) kind_vi[i] = v;
-    for (int cc = 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
+    for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
       for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v)
         if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
           kind_vi[i] = v;
