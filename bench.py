@@ -176,6 +176,16 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def measured_traffic(args, n_steps):
+    """DRAM bytes per DR launch from the committed ncu --set full capture of this exact
+    workload (profiles/r01_dr_traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "r01_dr_traffic.json")
+    if args.config != 2 or args.tangent or args.points != DEFAULT_POINTS[2] or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)["dram_bytes_per_launch"]
+
+
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -345,7 +355,8 @@ def main():
             "failed_points": failed,
             "roofline": {"bound": "fp64_pipe", "achieved": achieved / 1e9, "peak": peak / 1e9,
                          "unit": "Gop/s (FP64-pipe lane ops)", "frac": achieved / peak,
-                         "traffic": None,
+                         "traffic": measured_traffic(args, args.steps),
+                         "traffic_unit": "DRAM bytes per DR launch (ncu, profiles/r01_dr_traffic.json)",
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
