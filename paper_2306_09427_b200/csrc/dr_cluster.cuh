@@ -120,8 +120,11 @@ __device__ __forceinline__ double slots_min(const double* w, int n, int lane) {
   return warp_min(m);
 }
 
-template <int T, int FPT, int NPT, int LAW, bool UEA>
+template <int T, int FPT, int NPT, int LAWBO, bool UEA>
 __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
+  // LAWBO = law (0 linear, 1 exponential) + 2 * buckling_off: compile-time law flavour
+  constexpr int LAW = LAWBO & 1;
+  constexpr int bo = LAWBO >> 1;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ ClusterCtl ctl;
   const DrParams& P = CP.d;
@@ -149,7 +152,6 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   };
 
   const double B = P.nonlinearity;
-  const int bo = P.law_buckling_off;
 
   int fab[FPT], fgh[FPT];
   double fl0[FPT], fs[FPT], fmred[FPT];

@@ -192,8 +192,11 @@ __device__ __forceinline__ double law_energy(double s, double stretch, double rl
 
 // UEA: every fiber of the library has the same area*modulus (true for generated
 // networks), so the axial stiffness s = ea_scale*EA is one scalar instead of FPT registers.
-template <int T, int FPT, int NPT, int LAW, int MINB, bool UEA>
+template <int T, int FPT, int NPT, int LAWBO, int MINB, bool UEA>
 __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
+  // LAWBO = law (0 linear, 1 exponential) + 2 * buckling_off: compile-time law flavour
+  constexpr int LAW = LAWBO & 1;
+  constexpr int bo = LAWBO >> 1;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ DrCtl ctl;
   constexpr int NW = T / 32;
@@ -209,7 +212,6 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
 
   const double B = P.nonlinearity;
-  const int bo = P.law_buckling_off;
 
   // register-resident topology of the loaded entry
   int fab[FPT], fgo[FPT];

@@ -558,7 +558,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     FB_CUDA(c, cudaStreamWaitEvent(K.stream, c->ev_fork, 0));
     if (!K.cluster) {
       const Variant& v = kVariants[K.vi];
-      KernelFn fn = v.fn[law->kind][K.uniform_ea ? 1 : 0];
+      KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
       int per_sm = 0;
@@ -584,7 +584,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       fn<<<grid, v.T, smem, K.stream>>>(P);
     } else {
       const ClusterVariant& v = kClusterVariants[K.vi];
-      ClusterFn fn = v.fn[law->kind][K.uniform_ea ? 1 : 0];
+      ClusterFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
       if (K.C > 8)

@@ -5,10 +5,11 @@
 
 namespace fibra_b200 {
 
+#define FB_L(T, F, N, L, B) \
+  {&dr_persistent_kernel<T, F, N, L, B, false>, &dr_persistent_kernel<T, F, N, L, B, true>}
 #define FB_V(T, F, N, B)                                                                 \
   {T, F, N, B,                                                                             \
-   {{&dr_persistent_kernel<T, F, N, 0, B, false>, &dr_persistent_kernel<T, F, N, 0, B, true>}, \
-    {&dr_persistent_kernel<T, F, N, 1, B, false>, &dr_persistent_kernel<T, F, N, 1, B, true>}}}
+   {FB_L(T, F, N, 0, B), FB_L(T, F, N, 1, B), FB_L(T, F, N, 2, B), FB_L(T, F, N, 3, B)}}
 const Variant kVariants[] = {
     FB_V(256, 3, 1, 2),  // <= 256 node slots, <= 672 fibers
     FB_V(384, 3, 1, 2),  // <= 384 node slots, <= 1056 fibers (config 1/2 networks)
@@ -18,6 +19,7 @@ const Variant kVariants[] = {
     FB_V(768, 7, 2, 1),  // <= 1536 node slots
 };
 #undef FB_V
+#undef FB_L
 const int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 }  // namespace fibra_b200

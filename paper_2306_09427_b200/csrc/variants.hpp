@@ -12,12 +12,12 @@ using ClusterFn = void (*)(ClusterParams);
 
 struct Variant {     // resident kernel: one CTA per RVE
   int T, FPT, NPT, MINB;
-  KernelFn fn[2][2];  // [law: linear, exponential][uniform EA]
+  KernelFn fn[4][2];  // [law + 2 * buckling_off][uniform EA]
 };
 
 struct ClusterVariant {  // cluster kernel: one cluster of C CTAs per RVE (per-CTA shape)
   int T, FPT, NPT;
-  ClusterFn fn[2][2];
+  ClusterFn fn[4][2];
 };
 
 extern const Variant kVariants[];

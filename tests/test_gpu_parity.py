@@ -139,6 +139,29 @@ def test_exponential_law_tolerance(oracle_lib):
     check_exponential(br, resp, status)
 
 
+def test_buckling_off_bitwise(oracle_lib):
+    """FiberLaw.buckling_off (compressed fibers carry no force, network.cpp:16-38): a
+    compressive load on the resident and the cluster kernels, bitwise vs the oracle."""
+    for args in ((375, 1000, 1), (712, 1900, 7)):
+        pn, on = knn(*args)
+        F = np.stack([np.diag([0.97, 1.01, 1.0]), np.diag([1.03, 0.96, 0.98])])
+        law = P.FiberLaw(buckling_off=True)
+        lib = P.RveLibrary([pn])
+        st, assign = P.init_batch(np.zeros(2, np.int32), lib, 0)
+        br = P.batch_response(lib, assign, st, law, F, P.RelaxConfig(), P.StiffnessConfig(),
+                              want_tangent=False)
+        resp, status, ost = oracle_batch([on], [0, 0], F, tangent=False,
+                                         law=O.Law(buckling_off=True))
+        assert br.failed == list(np.nonzero(status)[0])
+        for p in range(2):
+            if status[p]:
+                continue
+            r = br.records[p]
+            assert r["base_report"]["iterations"] == resp[p]["base_report"]["iterations"]
+            assert same_bits(r["sigma"], resp[p]["sigma"])
+        check_states(st, ost)
+
+
 def test_failed_points_reported(small_lib):
     pnets, _ = small_lib
     lib = P.RveLibrary(pnets)
