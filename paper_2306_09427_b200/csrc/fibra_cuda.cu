@@ -862,10 +862,14 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     inc[P.a[f]].push_back(f);
     if (P.b[f] != P.a[f]) inc[P.b[f]].push_back(f);
   }
-  std::vector<int> own_k(P.M, -1), hrec(P.M, -1);
+  std::vector<int> own_k(P.M, -1), own_i(P.M, -1), hrec(P.M, -1);
   for (int q = 0; q < C; ++q) {
     const ClusterPart& Q = plan.parts[q];
-    for (size_t k = 0; k < Q.fibers.size(); ++k) own_k[Q.fibers[k]] = static_cast<int>(k);
+    for (size_t k = 0; k < Q.slot_fiber.size(); ++k)  // record = compact fiber slot
+      if (Q.slot_fiber[k] >= 0) {
+        own_k[Q.fibers[Q.slot_fiber[k]]] = static_cast<int>(k);
+        own_i[Q.fibers[Q.slot_fiber[k]]] = Q.slot_fiber[k];
+      }
     for (size_t h = 0; h < Q.h_fiber.size(); ++h) hrec[Q.h_fiber[h]] = static_cast<int>(h);
   }
   // halo slot of a remote node in part q, and the push lists of the owners
@@ -887,7 +891,6 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     const ClusterPart& Q = plan.parts[q];
     PartDev& D = parts[q];
     D = PartDev{};
-    const int n_own = static_cast<int>(Q.fibers.size());
     const int n_h = static_cast<int>(Q.h_fiber.size());
     // records: [one per fiber slot of the fiber threads, compact index k = j*FT + tid (dummy
     // slots included, so the kernel derives the offset)][copies of remote fibers (heads
@@ -913,9 +916,8 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
       for (int f : inc[pn]) {
         int e;
         if (plan.owner_of_fiber[f] == q) {
-          const int k = own_k[f];
-          e = 24 * k;
-          if (Q.tail_pn[k] == pn) e |= static_cast<int>(0x80000000u);
+          e = 24 * own_k[f];
+          if (Q.tail_pn[own_i[f]] == pn) e |= static_cast<int>(0x80000000u);
         } else {
           e = 24 * (own_slots + hrec[f]);
         }
@@ -936,9 +938,11 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     std::vector<int> fab(FS, (24 * TS) | ((24 * (TS + 1)) << 16)), fgt(FS), fgh(FS, -1), fid(FS, -1);
     std::vector<double> fl0(FS, 0.5), fea(FS, P.M > 0 ? P.ea[0] : 1.0), flt(FS, 1.0), flh(FS, 1.0);
     for (int fs = 0; fs < FS; ++fs) fgt[fs] = 24 * ((fs / T) * FT + fs % T);  // (reducer: unused)
-    for (int k = 0; k < n_own; ++k) {
+    for (int k = 0; k < static_cast<int>(Q.slot_fiber.size()); ++k) {
+      const int i = Q.slot_fiber[k];
+      if (i < 0) continue;  // dummy slot
       const int fs = (k / FT) * T + k % FT;
-      const int f = Q.fibers[k], tl = Q.tail_pn[k], hd = Q.head_pn[k];
+      const int f = Q.fibers[i], tl = Q.tail_pn[i], hd = Q.head_pn[i];
       const int ph = plan.part_of_pn[hd];
       const int xh = ph == q ? 24 * plan.slot_of_pn[hd] : 24 * (TS + 2 + halo_of[q][hd]);
       fab[fs] = (24 * plan.slot_of_pn[tl]) | (xh << 16);

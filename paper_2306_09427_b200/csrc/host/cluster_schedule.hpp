@@ -29,6 +29,8 @@ struct ClusterPart {
   std::vector<int> halo_pn;         // remote nodes whose x this part reads
   std::vector<int> fibers;          // owned fibers, in fiber-slot order
   std::vector<int> tail_pn, head_pn;  // per owned fiber (tail is owned here)
+  std::vector<int> slot_fiber;      // compact fiber slot k -> index into `fibers` (-1 dummy);
+                                    // half-warp groups of 16 slots have bank-distinct x loads
   std::vector<int> h_fiber;         // fibers owned elsewhere whose head lives here
 };
 
