@@ -1117,6 +1117,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   // diagnostics: FIBRA_FORCE_CLUSTER=C places every entry on a C-CTA cluster (kernel timing)
   const char* force_env = getenv("FIBRA_FORCE_CLUSTER");
   const int force_c = force_env ? atoi(force_env) : 0;
+  // diagnostics: FIBRA_CLUSTER_SHAPE=i restricts the cluster kernels to kClusterVariants[i]
+  const char* shape_env = getenv("FIBRA_CLUSTER_SHAPE");
+  const int force_shape = shape_env ? atoi(shape_env) : -1;
   parallel_for(0, n, [&](int i) {
     nets[i] = pack(entries[i]);
     const PackedNet& P = nets[i];
@@ -1127,12 +1130,16 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     const int mp = max_pairs_of(P);
     for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
       if (resident_fits(c, P, kVariants[v], mp, de.sched)) kind_vi[i] = v;
+    // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
+    // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
     for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
-      for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v)
-        if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
-          kind_vi[i] = v;
-          kind_C[i] = cc;
-          kind_cl[i] = 1;
+        for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v) {
+          if (force_shape >= 0 && v != force_shape) continue;
+          if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
+            kind_vi[i] = v;
+            kind_C[i] = cc;
+            kind_cl[i] = 1;
+          }
         }
   });
   for (int i = 0; i < n; ++i) {

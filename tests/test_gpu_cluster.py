@@ -80,6 +80,17 @@ def test_cluster_stress_bitwise(mid_net):
     check_states(st, ost)
 
 
+def test_cluster_2500_fibers_bitwise(oracle_lib):
+    """A config-3 size between the shapes (2.5k fibers: 2 CTAs of the (384, 4, 1) shape)."""
+    pn, on = knn(625, 2500, 11)
+    F = batch_F(4)
+    br, st, shapes = run([pn], [0] * 4, F, tangent=False)
+    assert shapes[0]["cluster"] == 2 and shapes[0]["fibers_per_thread"] == 4
+    resp, status, ost = oracle_batch([on], [0] * 4, F, tangent=False)
+    check_records(br, resp, status, tangent=False)
+    check_states(st, ost)
+
+
 def test_cluster_tangent_mixed_library(mid_net):
     pn, on = mid_net
     sp, so = knn(14, 38, 101, neighbors=9)
