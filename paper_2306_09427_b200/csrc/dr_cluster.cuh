@@ -55,7 +55,8 @@ struct ClusterEntryDev {
   int n_nodes, n_fibers, n_free_nodes, n_fix_nodes;
   double max_lump, max_ea, box_volume, ea0;
   const PartDev* parts;     // [C]
-  const void* pad;
+  int mirror;               // cross fibers evaluated by both CTAs (host/cluster_schedule.hpp)
+  int pad;
 };
 
 struct ClusterParams {
@@ -69,7 +70,8 @@ struct ClusterParams {
 
 struct __align__(16) ClusterCtl {
   int solve, point, q, entry;
-  int flag, collapse, dec, skip;  // skip: last pass whose exact verdict said "continue"
+  int flag, dec, skip, pad0;  // skip: last pass whose exact verdict said "continue"
+  int collapse[2], pad1[2];   // [pass & 1]: a fiber of that pass collapsed somewhere
   double ck_t[2], ck_dt[2];
   double warp_min[32];
   double ex[12];
@@ -144,6 +146,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   double* scr = CP.scratch + static_cast<size_t>(cl_id()) * CP.scratch_stride;
   const unsigned X_sh = sh_addr(X), G_sh = sh_addr(G), ctl_sh = sh_addr(&ctl);
   const unsigned off_solve = offsetof(ClusterCtl, solve), off_collapse = offsetof(ClusterCtl, collapse);
+  // fiber -> node handoff: a CTA barrier when every gathered record is written locally
+  // (mirror mode) and dt needs no cluster-wide minimum (linear law), else a cluster barrier
   const unsigned off_part = offsetof(ClusterCtl, part);
   const unsigned off_wmin = offsetof(ClusterCtl, wmin) + 8 * (rank * NW + warp);  // my warp's slot
   // push this warp's CFL minimum into its slot of every CTA (lane r -> CTA r)
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
 
     const ClusterEntryDev& E = CP.centries[e];
     const PartDev& Q = E.parts[rank];
+    const bool local_handoff = LAW == 0 && E.mirror;
     const double scale = P.density_scale / E.max_lump;  // setup_mass relax.cpp:35-43
     const int F0 = Q.f0, NSLOT = Q.node_slots;
     if (e != cur_entry) {
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       ctl.ck_t[0] = ctl.t;
       ctl.ck_dt[0] = 0.0;
       ctl.force_floor = P.ea_scale * E.max_ea * 1e-12;  // relax.cpp:112
-      ctl.collapse = 0;
+      ctl.collapse[0] = ctl.collapse[1] = 0;
       ctl.skip = -1;
     }
     if (LAW == 0) push_wmin(warp_min(lmin));
@@ -331,6 +336,9 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
 
     int k = 0;
     int target = -1;
+    // first pass at which a fiber collapsed (the reference throws there, network.cpp:291):
+    // decisive once the lagged verdicts of every earlier pass have been taken
+    int cpass = -1;
     double dt_k = 0;
     int status = det_ok ? FIBRA_OK : FIBRA_E_KINEMATICS;
     int conv = 0;
@@ -424,13 +432,13 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         if constexpr (B1 < FPT)
           fiber_block(std::integral_constant<int, B1>(), std::integral_constant<int, FPT>());
         if (collapsed)
-          for (unsigned r = 0; r < C; ++r) cl_st_s32(cl_map(ctl_sh + off_collapse, r), 1);
+          for (unsigned r = 0; r < C; ++r) cl_st_s32(cl_map(ctl_sh + off_collapse + 4 * (k & 1), r), 1);
         if (LAW != 0) push_wmin(warp_min(kmin));
       }
-      cl_sync();
+      if (local_handoff) __syncthreads(); else cl_sync();
 
       // ================= node phase (pass k) =================
-      if (target < 0 && k >= 2) {
+      if (target < 0 && k >= 2 && (cpass < 0 || k - 2 < cpass)) {
         const int d = ctl.dec;
         if ((d & (kDecConv | kDecExact)) || k - 2 == P.max_iterations) {
           target = k - 2;  // replay from the newest checkpoint at or before it
@@ -454,10 +462,12 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
               push_x(j, sl, xr[0], xr[1], xr[2]);
             }
           }
-          if (tid == 0) {
-            ctl.t = ctl.ck_t[b];
-            ctl.collapse = 0;
-          }
+          if (tid == 0) ctl.t = ctl.ck_t[b];
+          cpass = -1;
+          // discard collapse flags of the passes after the target: once every push of this
+          // pass has landed (first barrier), and before anyone pushes again (second)
+          cl_sync();
+          if (tid == 0) ctl.collapse[0] = ctl.collapse[1] = 0;
           cl_sync();
           continue;
         }
@@ -469,7 +479,12 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         }
         if (tid == 0) ctl.t += dt_k;
       }
-      if (ctl.collapse) {
+      // collapse flags of this pass (cluster barrier after the fiber phase), or of the
+      // previous pass (local handoff: the last cluster barrier ended node phase k-1)
+      // (a replay target always precedes a known collapse, so replays never see one)
+      if (cpass < 0 && (local_handoff ? (k >= 1 && ctl.collapse[(k - 1) & 1]) : ctl.collapse[k & 1]))
+        cpass = local_handoff ? k - 1 : k;
+      if (cpass >= 0 && k - 2 >= cpass - 1) {  // the verdicts of all earlier passes are taken
         status = FIBRA_E_COLLAPSE;
         break;
       }

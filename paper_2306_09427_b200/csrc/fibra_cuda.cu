@@ -706,8 +706,11 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
 
 bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& v, int C,
                   int max_pairs, ClusterPlan& plan) {
+  // mirror mode first (one cluster barrier per iteration), else copies of remote records
   if (!build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
-                          v.NPT, plan))
+                          v.NPT, true, plan) &&
+      !build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
+                          v.NPT, false, plan))
     return false;
   const int TS = v.NPT * v.T;
   if (24 * (TS + 2 + plan.max_halo) >= 65536) return false;  // 16-bit x offsets
@@ -862,13 +865,16 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
     inc[P.a[f]].push_back(f);
     if (P.b[f] != P.a[f]) inc[P.b[f]].push_back(f);
   }
-  std::vector<int> own_k(P.M, -1), own_i(P.M, -1), hrec(P.M, -1);
+  // per part: record (= compact fiber slot) and plan index of every fiber it evaluates (a
+  // mirrored cross fiber has one in each of its two parts), copy index of remote records
+  std::vector<std::vector<int>> own_k(C, std::vector<int>(P.M, -1)), own_i(C, std::vector<int>(P.M, -1));
+  std::vector<int> hrec(P.M, -1);
   for (int q = 0; q < C; ++q) {
     const ClusterPart& Q = plan.parts[q];
-    for (size_t k = 0; k < Q.slot_fiber.size(); ++k)  // record = compact fiber slot
+    for (size_t k = 0; k < Q.slot_fiber.size(); ++k)
       if (Q.slot_fiber[k] >= 0) {
-        own_k[Q.fibers[Q.slot_fiber[k]]] = static_cast<int>(k);
-        own_i[Q.fibers[Q.slot_fiber[k]]] = Q.slot_fiber[k];
+        own_k[q][Q.fibers[Q.slot_fiber[k]]] = static_cast<int>(k);
+        own_i[q][Q.fibers[Q.slot_fiber[k]]] = Q.slot_fiber[k];
       }
     for (size_t h = 0; h < Q.h_fiber.size(); ++h) hrec[Q.h_fiber[h]] = static_cast<int>(h);
   }
@@ -915,9 +921,9 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
       if (pn < 0) continue;
       for (int f : inc[pn]) {
         int e;
-        if (plan.owner_of_fiber[f] == q) {
-          e = 24 * own_k[f];
-          if (Q.tail_pn[own_i[f]] == pn) e |= static_cast<int>(0x80000000u);
+        if (own_k[q][f] >= 0) {  // evaluated here
+          e = 24 * own_k[q][f];
+          if (Q.tail_pn[own_i[q][f]] == pn) e |= static_cast<int>(0x80000000u);
         } else {
           e = 24 * (own_slots + hrec[f]);
         }
@@ -944,10 +950,12 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
       const int fs = (k / FT) * T + k % FT;
       const int f = Q.fibers[i], tl = Q.tail_pn[i], hd = Q.head_pn[i];
       const int ph = plan.part_of_pn[hd];
-      const int xh = ph == q ? 24 * plan.slot_of_pn[hd] : 24 * (TS + 2 + halo_of[q][hd]);
-      fab[fs] = (24 * plan.slot_of_pn[tl]) | (xh << 16);
+      auto xoff = [&](int pn) {  // own slot or halo slot (mirror mode: either end may be remote)
+        return plan.part_of_pn[pn] == q ? 24 * plan.slot_of_pn[pn] : 24 * (TS + 2 + halo_of[q][pn]);
+      };
+      fab[fs] = xoff(tl) | (xoff(hd) << 16);
       fgt[fs] = 24 * k;
-      if (ph != q)
+      if (ph != q && !plan.mirror)
         fgh[fs] = (ph << 24) |
                   (24 * (own_slots + hrec[f]));
       fid[fs] = f;
@@ -991,6 +999,7 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
   E.max_ea = d.max_ea;
   E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
   E.ea0 = P.M > 0 ? P.ea[0] : 1.0;
+  E.mirror = plan.mirror ? 1 : 0;
   parts_off = A.reserve(sizeof(PartDev) * C);  // filled at commit, once pointers are known
   K.ts = TS;
   K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + plan.max_halo)));

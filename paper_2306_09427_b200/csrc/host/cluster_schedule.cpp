@@ -50,8 +50,10 @@ void optimize_gather_banks(ClusterPlan& P, int c, int M, const int* a_pn, const 
                            int own_slots);
 
 bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
-                        const double* ref, int C, int T, int FPT, int NPT, ClusterPlan& P) {
+                        const double* ref, int C, int T, int FPT, int NPT, bool mirror,
+                        ClusterPlan& P) {
   P = ClusterPlan();
+  P.mirror = mirror;
   P.C = C;
   P.T = T;
   P.FPT = FPT;
@@ -118,7 +120,15 @@ bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
     const int ph = P.part_of_pn[head];
     if (ph != o) {
       Q.halo_pn.push_back(head);
-      P.parts[ph].h_fiber.push_back(f);
+      if (mirror) {  // the head's CTA evaluates it too (tail read from its halo)
+        ClusterPart& R = P.parts[ph];
+        R.fibers.push_back(f);
+        R.tail_pn.push_back(tail);
+        R.head_pn.push_back(head);
+        R.halo_pn.push_back(tail);
+      } else {
+        P.parts[ph].h_fiber.push_back(f);
+      }
     }
   }
   std::vector<int> copies(N, 0);
@@ -141,7 +151,7 @@ bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
     int open = 0;
     std::vector<int> leftovers;
     for (size_t i = 0; i < Q.fibers.size(); ++i) {
-      const bool internal = P.part_of_pn[Q.head_pn[i]] == c;
+      const bool internal = mirror || P.part_of_pn[Q.head_pn[i]] == c;
       bool placed = false;
       for (int g = 0; g < open + 1 && g < groups && !placed; ++g) {
         if (fill[g] == 16) continue;
@@ -190,7 +200,7 @@ void optimize_gather_banks(ClusterPlan& P, int c, int M, const int* a_pn, const 
   // readers of every record: (half-warp, CSR entry index) of the local nodes gathering it;
   // the two entries of a step are separate load instructions, so the entry index is the cell
   std::vector<std::vector<std::pair<int, int>>> readers(n_rec);
-  std::vector<int> rec_of_own(M, -1), rec_of_h(M, -1);
+  std::vector<int> rec_of_own(M, -1), rec_of_h(M, -1);  // this part's records
   for (int k = 0; k < static_cast<int>(Q.slot_fiber.size()); ++k)
     if (Q.slot_fiber[k] >= 0) rec_of_own[Q.fibers[Q.slot_fiber[k]]] = k;
   for (size_t h = 0; h < Q.h_fiber.size(); ++h) rec_of_h[Q.h_fiber[h]] = own_slots + static_cast<int>(h);
@@ -206,7 +216,7 @@ void optimize_gather_banks(ClusterPlan& P, int c, int M, const int* a_pn, const 
   for (int sl = 0; sl < Q.node_slots; ++sl) {
     for (size_t i = 0; i < inc[sl].size(); ++i) {
       const int f = inc[sl][i];
-      const int r = P.owner_of_fiber[f] == c ? rec_of_own[f] : rec_of_h[f];
+      const int r = rec_of_own[f] >= 0 ? rec_of_own[f] : rec_of_h[f];
       if (r >= 0) readers[r].push_back({sl / 16, static_cast<int>(i)});
     }
     max_steps = std::max(max_steps, static_cast<int>(inc[sl].size()));
@@ -273,11 +283,15 @@ extern "C" int fibra_cluster_report(const fibra_net_desc* d, int C, int T, int F
     b[f] = d->fiber_packed_dofs[6 * f + 3] / 3;
   }
   fibra_b200::ClusterPlan plan;
-  const bool ok = fibra_b200::build_cluster_plan(N, d->n_free / 3, M, a.data(), b.data(),
-                                                 d->packed_ref, C, T, FPT, NPT, plan);
+  bool ok = fibra_b200::build_cluster_plan(N, d->n_free / 3, M, a.data(), b.data(),
+                                           d->packed_ref, C, T, FPT, NPT, true, plan);
+  if (!ok)
+    ok = fibra_b200::build_cluster_plan(N, d->n_free / 3, M, a.data(), b.data(), d->packed_ref,
+                                        C, T, FPT, NPT, false, plan);
   int min_fibers = M, cross = 0;
   for (const auto& q : plan.parts) min_fibers = std::min(min_fibers, static_cast<int>(q.fibers.size()));
-  for (const auto& q : plan.parts) cross += static_cast<int>(q.h_fiber.size());
+  if (ok)
+    for (int f = 0; f < M; ++f) cross += plan.part_of_pn[a[f]] != plan.part_of_pn[b[f]];
   out[0] = ok;
   out[1] = plan.max_fibers;
   out[2] = plan.parts.empty() ? 0 : min_fibers;

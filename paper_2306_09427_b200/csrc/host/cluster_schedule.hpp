@@ -16,6 +16,11 @@
 // So every x load of the fiber phase and every record load of the CSR gather is local;
 // only stores cross SMs.  Each node still accumulates its incident fibers in ascending
 // fiber id (network.cpp:298-303).
+//
+// Mirror mode (when the parts have room): a cross fiber is evaluated by *both* CTAs that hold
+// one of its ends (same halo x, same arithmetic, so the same bits), so every record a node
+// gathers is written by its own CTA and the fiber -> node handoff needs only a CTA barrier;
+// one cluster barrier per DR iteration remains (after the x push).
 #pragma once
 
 #include <vector>
@@ -31,7 +36,7 @@ struct ClusterPart {
   std::vector<int> tail_pn, head_pn;  // per owned fiber (tail is owned here)
   std::vector<int> slot_fiber;      // compact fiber slot k -> index into `fibers` (-1 dummy);
                                     // half-warp groups of 16 slots have bank-distinct x loads
-  std::vector<int> h_fiber;         // fibers owned elsewhere whose head lives here
+  std::vector<int> h_fiber;         // fibers owned elsewhere whose head lives here (copies)
 };
 
 struct ClusterPlan {
@@ -42,12 +47,14 @@ struct ClusterPlan {
   std::vector<ClusterPart> parts;   // [C]
   int max_halo = 0, max_records = 0, max_fibers = 0, max_node_slots = 0;
   int max_push = 0;                 // most halo copies of one node
+  bool mirror = false;              // cross fibers evaluated in both parts, no copies
 };
 
 // ref: packed reference coordinates (3N); nodes [0, NFN) are free.  Returns false when a
 // part exceeds the per-CTA capacity of the kernel shape (T threads, FPT fibers and NPT
 // nodes per thread; the last warp owns no fibers).
 bool build_cluster_plan(int N, int NFN, int M, const int* a_pn, const int* b_pn,
-                        const double* ref, int C, int T, int FPT, int NPT, ClusterPlan& plan);
+                        const double* ref, int C, int T, int FPT, int NPT, bool mirror,
+                        ClusterPlan& plan);
 
 }  // namespace fibra_b200
