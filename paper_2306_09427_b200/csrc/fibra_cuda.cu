@@ -69,9 +69,9 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
     const float k = static_cast<float>(hint[p]);
     hi = (k == k && k > 0) ? ~__float_as_uint(k) : 0xffffffffu;
   }
-  // [kernel class : 3][cost : 29][point : 32] -- the order is grouped by class
-  key[p] = (static_cast<unsigned long long>(cls[p]) << 61) |
-           (static_cast<unsigned long long>(hi >> 3) << 32) | static_cast<unsigned>(p);
+  // [kernel class : 4][cost : 28][point : 32] -- the order is grouped by class
+  key[p] = (static_cast<unsigned long long>(cls[p]) << 60) |
+           (static_cast<unsigned long long>(hi >> 4) << 32) | static_cast<unsigned>(p);
   if (!polar_decompose(f, o.R, o.U)) {  // KinematicsError -> failed point
     o.status = FIBRA_E_KINEMATICS;
     solve_skip[p] = FIBRA_E_KINEMATICS;
@@ -259,7 +259,7 @@ __global__ void fp64_peak_kernel(double* sink, int iters, double c) {
 // ---------------------------------------------------------------------------------
 // kernel classes (shapes in variants.hpp, instantiated in kernels_*.cu)
 // ---------------------------------------------------------------------------------
-constexpr int kMaxClasses = 8;
+constexpr int kMaxClasses = 16;  // 4 bits of the schedule key
 
 struct DeviceEntry {
   EntryDev dev;           // resident-kernel entry
