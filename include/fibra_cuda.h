@@ -188,6 +188,12 @@ enum { FIBRA_SCHED_BATCH = 0, FIBRA_SCHED_STRAIN = 1, FIBRA_SCHED_HINT = 2 };
  * thread, nodes per thread}.  RVEs beyond one CTA's shared memory (about 1.3k fibers) run
  * on a thread-block cluster of C = 2..16 CTAs (csrc/dr_cluster.cuh). */
 int fibra_cuda_entry_kernel(const fibra_ctx* ctx, int32_t entry, int32_t* out);
+
+/* orientation_p2 (network.cpp:398-415; NetworkBatchProvider::orientation, batch.cpp:
+ * 296-302) of the device-resident state u of `points`, about ref_dir[3]: the length-
+ * weighted P2 order parameter of the fibres, in the reference's summation order. */
+int fibra_cuda_orientation(fibra_ctx* ctx, const int32_t* points, int32_t n,
+                           const double* ref_dir, double* out);
 int fibra_cuda_set_schedule(fibra_ctx* ctx, int32_t mode, const double* cost_hint);
 /* Warm data host->device: u (total dofs), t, iters, converged (n_points); any may be NULL */
 int fibra_cuda_upload_states(fibra_ctx* ctx, const double* u, const double* t,

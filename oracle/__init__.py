@@ -124,6 +124,8 @@ def lib():
         L.or_norm2_sq.argtypes = [C.c_int64, _dp]
         L.or_det.restype = C.c_double
         L.or_det.argtypes = [_dp]
+        L.or_orientation_p2.restype = C.c_double
+        L.or_orientation_p2.argtypes = [C.POINTER(CNetwork), _dp, _dp]
         _lib = L
     return _lib
 
@@ -258,6 +260,13 @@ def homogenized_stress(net: Network, state: State, F):
     return sig, float(asym[0])
 
 
+def orientation_p2(net: Network, u, ref_dir) -> float:
+    """orientation_p2 (network.cpp:398-415)."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    d = np.ascontiguousarray(ref_dir, dtype=np.float64)
+    return float(lib().or_orientation_p2(C.byref(net.c), _ptr(u, _dp), _ptr(d, _dp)))
+
+
 def internal_forces(net: Network, u, law: Law = None):
     law = law or Law()
     u = np.ascontiguousarray(u, dtype=np.float64)
@@ -386,6 +395,8 @@ def ref():
                                       C.POINTER(CRelaxCfg), _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                       _dp, _lp, _bp, C.c_int, C.POINTER(CReport)]
         L.ref_homogenized_stress.argtypes = [C.c_void_p, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        L.ref_orientation_p2.restype = C.c_double
+        L.ref_orientation_p2.argtypes = [C.c_void_p, _dp, _dp]
         L.ref_internal_forces.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int,
                                           _dp, _dp]
         L.ref_batch_stress.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_double, C.c_double,
@@ -489,6 +500,12 @@ def ref_homogenized_stress(rnet: RefNetwork, state: State, F):
     if rc:
         raise OracleError(rc, ref().ref_last_error().decode())
     return sig, float(asym[0])
+
+
+def ref_orientation_p2(rnet: RefNetwork, u, ref_dir) -> float:
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    d = np.ascontiguousarray(ref_dir, dtype=np.float64)
+    return float(ref().ref_orientation_p2(rnet.h, _ptr(u, _dp), _ptr(d, _dp)))
 
 
 def ref_batch_stress(rnet: RefNetwork, F, cfg: RelaxConfig = None, law: Law = None, workers=1):

@@ -585,6 +585,24 @@ double or_strain_energy(const or_network* net, const or_law* law, const double* 
   return e;
 }
 
+double or_orientation_p2(const or_network* net, const double* u, const double ref_dir[3]) {
+  /* network.cpp:398-415, same expression order */
+  const double* ref = net->packed_ref;
+  double wsum = 0, acc = 0;
+  for (int f = 0; f < net->n_fibers; ++f) {
+    const int32_t* p = net->fiber_dofs + 6 * f;
+    const double d0 = (ref[p[3]] + u[p[3]]) - (ref[p[0]] + u[p[0]]);
+    const double d1 = (ref[p[4]] + u[p[4]]) - (ref[p[1]] + u[p[1]]);
+    const double d2 = (ref[p[5]] + u[p[5]]) - (ref[p[2]] + u[p[2]]);
+    const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (!(len > 0)) continue;
+    const double c = (d0 * ref_dir[0] + d1 * ref_dir[1] + d2 * ref_dir[2]) / len;
+    acc += len * 0.5 * (3.0 * c * c - 1.0);
+    wsum += len;
+  }
+  return wsum > 0 ? acc / wsum : 0.0;
+}
+
 int or_homogenized_stress(const or_network* net, const or_state* st, const double F[9],
                           double sigma[6], double* asym_out) {
   /* network.cpp:341-372 */

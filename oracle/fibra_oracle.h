@@ -111,6 +111,9 @@ int or_internal_forces_cfl(const or_network* net, const or_law* law, const doubl
 int or_homogenized_stress(const or_network* net, const or_state* st, const double F[9],
                           double sigma[6], double* asym);
 double or_strain_energy(const or_network* net, const or_law* law, const double* u);
+/* orientation_p2 (network.cpp:398-415): length-weighted P2 order parameter of the fibres
+ * about ref_dir in the state u (packed DOFs) */
+double or_orientation_p2(const or_network* net, const double* u, const double ref_dir[3]);
 
 /* ---- BLAS-1 contract (kernels.hpp:8-15) ---- */
 double or_norm2_sq(int64_t n, const double* x);

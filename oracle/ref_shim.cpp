@@ -240,6 +240,13 @@ int ref_relax_solve(void* h, int law_kind, double ea_scale, double nonlin, int b
   }
 }
 
+// the reference's own orientation_p2 (network.cpp:398-415)
+double ref_orientation_p2(void* h, const double* u, const double* dir) {
+  FiberNetwork& net = *static_cast<FiberNetwork*>(h);
+  const std::span<const double> uu(u, static_cast<std::size_t>(net.n_dof()));
+  return orientation_p2(net, uu, Vec3{dir[0], dir[1], dir[2]});
+}
+
 int ref_homogenized_stress(void* h, const double* u, const double* f_int, int converged,
                            const double* F, double* sigma6, double* asym) {
   FiberNetwork& net = *static_cast<FiberNetwork*>(h);

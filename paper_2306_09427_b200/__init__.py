@@ -387,6 +387,15 @@ class DeviceBatch:
     def reset_states(self):
         self._check(self._L.fibra_cuda_reset_states(self._ctx))
 
+    def orientation(self, points, ref_dir) -> np.ndarray:
+        """orientation_p2 (network.cpp:398-415) of the device-resident states of `points`."""
+        pts = np.ascontiguousarray(points, dtype=np.int32).reshape(-1)
+        d = np.ascontiguousarray(ref_dir, dtype=np.float64).reshape(3)
+        out = np.zeros(max(len(pts), 1))
+        self._check(self._L.fibra_cuda_orientation(self._ctx, _ptr(pts, _capi._ip), len(pts),
+                                                   _ptr(d, _capi._dp), _ptr(out, _capi._dp)))
+        return out[:len(pts)]
+
     def entry_kernel(self, entry: int) -> dict:
         """Kernel shape of a library entry: cluster size (1 = one CTA per RVE) and per-CTA
         threads / fibers per thread / nodes per thread."""
@@ -529,6 +538,13 @@ class NetworkBatchProvider:
             self._db.download_states(self._states)
             self._dirty = False
         return self._states
+
+    def orientation(self, point: int, ref_dir) -> Optional[float]:
+        """NetworkBatchProvider::orientation (batch.cpp:296-302): orientation_p2 of the
+        point's current state; None when the point is out of range."""
+        if point < 0 or point >= self._db.n_points:
+            return None
+        return float(self._db.orientation([point], ref_dir)[0])
 
     def respond(self, deformation) -> ProviderResult:
         rec = self._db.solve(deformation, self.law, self.relax_cfg, self.stiff_cfg, True)

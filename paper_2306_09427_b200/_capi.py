@@ -30,7 +30,7 @@ EXPORTS = [
     "fibra_cluster_report",
     "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
-    "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel",
+    "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel", "fibra_cuda_orientation",
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
     "fibra_cuda_solve_device", "fibra_cuda_synchronize", "fibra_cuda_last_stats",
     "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile",
@@ -138,6 +138,7 @@ def load(build_if_missing: bool = True):
         "fibra_cuda_reset_states": (C.c_int, [vp]),
         "fibra_cuda_set_schedule": (C.c_int, [vp, C.c_int32, _dp]),
         "fibra_cuda_entry_kernel": (C.c_int, [vp, C.c_int32, _ip]),
+        "fibra_cuda_orientation": (C.c_int, [vp, _ip, C.c_int32, _dp, _dp]),
         "fibra_cuda_upload_states": (C.c_int, [vp, _dp, _dp, _lp, _bp]),
         "fibra_cuda_download_states": (C.c_int, [vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                                  _lp, _bp]),

@@ -98,6 +98,41 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
   prep[p] = o;
 }
 
+// orientation_p2 (network.cpp:398-415) of the device-resident state: reference fibre order
+// and expression order, one thread per requested point (sequential sums as the reference)
+struct OrientDev {
+  int n_fibers, pad;
+  const int* a;         // [M] packed node of the fibre's end a (fiber_packed_dofs / 3)
+  const int* b;         // [M]
+  const double* ref;    // [3N] packed reference coordinates
+};
+
+__global__ void orientation_kernel(int n, const int* __restrict__ points,
+                                   const int* __restrict__ entry_of_point,
+                                   const long long* __restrict__ offsets,
+                                   const OrientDev* __restrict__ ents, const double* u,
+                                   double r0, double r1, double r2, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = points[i];
+  const OrientDev& E = ents[entry_of_point[p]];
+  const double* up = u + offsets[p];
+  const double* ref = E.ref;
+  double wsum = 0, acc = 0;
+  for (int f = 0; f < E.n_fibers; ++f) {
+    const int pa = 3 * E.a[f], pb = 3 * E.b[f];
+    const double d0 = (ref[pb] + up[pb]) - (ref[pa] + up[pa]);
+    const double d1 = (ref[pb + 1] + up[pb + 1]) - (ref[pa + 1] + up[pa + 1]);
+    const double d2 = (ref[pb + 2] + up[pb + 2]) - (ref[pa + 2] + up[pa + 2]);
+    const double len = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
+    if (!(len > 0)) continue;
+    const double c = (d0 * r0 + d1 * r1 + d2 * r2) / len;
+    acc += len * 0.5 * (3.0 * c * c - 1.0);
+    wsum += len;
+  }
+  out[i] = wsum > 0 ? acc / wsum : 0.0;
+}
+
 // order[rank of key[p]] = p (keys are unique): a counting rank, O(n^2 / 256) smem compares,
 // a few microseconds at thousands of points
 __global__ void rank_kernel(int n, const unsigned long long* __restrict__ key, int* order) {
@@ -264,6 +299,7 @@ constexpr int kMaxClasses = 16;  // 4 bits of the schedule key
 struct DeviceEntry {
   EntryDev dev;           // resident-kernel entry
   ClusterEntryDev cdev;   // cluster-kernel entry
+  OrientDev orient;       // reference-order fibres + packed reference (orientation_p2)
   Schedule sched;
   std::vector<void*> allocs;
   int cls = -1;           // kernel class
@@ -337,6 +373,7 @@ struct fibra_ctx {
   double* h_F = nullptr;                 // pinned staging
   fibra_point_result* h_res = nullptr;   // pinned staging
   int* d_ticket = nullptr;               // [kMaxClasses][2]
+  OrientDev* d_orient = nullptr;         // [n_entries]
   unsigned long long* d_counters = nullptr;
   cudaEvent_t ev[4] = {};
   cudaEvent_t ev_fork = nullptr;
@@ -422,6 +459,8 @@ void free_library(fibra_ctx* c) {
     if (k.done) cudaEventDestroy(k.done);
   }
   c->classes.clear();
+  cudaFree(c->d_orient);
+  c->d_orient = nullptr;
 }
 
 int ensure_scratch(fibra_ctx* c, int n) {
@@ -1187,6 +1226,11 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     parallel_for(lo, hi, [&](int i) {
       DeviceEntry& de = c->entries[i];
       const KClass& K = c->classes[de.cls];
+      de.orient = OrientDev{};
+      de.orient.n_fibers = nets[i].M;
+      arenas[i - lo].add(&de.orient.a, nets[i].a);
+      arenas[i - lo].add(&de.orient.b, nets[i].b);
+      arenas[i - lo].add(&de.orient.ref, nets[i].ref);
       if (K.cluster)
         build_cluster_entry(de, nets[i], entries[i], plans[i], kClusterVariants[K.vi],
                             arenas[i - lo], parts[i - lo], parts_off[i - lo], caps[i - lo]);
@@ -1201,6 +1245,12 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       nets[i] = PackedNet();
       plans[i] = ClusterPlan();
     }
+  }
+  {
+    std::vector<OrientDev> host(n);
+    for (int i = 0; i < n; ++i) host[i] = c->entries[i].orient;
+    FB_CUDA(c, cudaMalloc(&c->d_orient, sizeof(OrientDev) * n));
+    FB_CUDA(c, cudaMemcpy(c->d_orient, host.data(), sizeof(OrientDev) * n, cudaMemcpyHostToDevice));
   }
   for (KClass& K : c->classes) {
     if (K.smem() > static_cast<size_t>(c->max_smem))
@@ -1265,6 +1315,32 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   }
   FB_CUDA(c, cudaMemcpy(c->d_offsets, c->offsets.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice));
   return fibra_cuda_reset_states(c);
+}
+
+int fibra_cuda_orientation(fibra_ctx* c, const int32_t* points, int32_t n, const double* ref_dir,
+                           double* out) {
+  if (!c || n < 0 || (n && (!points || !ref_dir || !out))) return FIBRA_E_ARG;
+  if (!c->d_orient || c->offsets.empty())
+    return set_err(c, FIBRA_E_ARG, "upload_library and bind_points must precede orientation");
+  if (n == 0) return FIBRA_OK;
+  for (int i = 0; i < n; ++i)
+    if (points[i] < 0 || points[i] >= c->n_points)
+      return set_err(c, FIBRA_E_ARG, "orientation: point out of range");
+  FB_CUDA(c, cudaSetDevice(c->device));
+  int* d_pts = nullptr;
+  double* d_out = nullptr;
+  FB_CUDA(c, cudaMalloc(&d_pts, sizeof(int) * n));
+  FB_CUDA(c, cudaMalloc(&d_out, sizeof(double) * n));
+  FB_CUDA(c, cudaMemcpyAsync(d_pts, points, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+  orientation_kernel<<<(n + 127) / 128, 128, 0, c->stream>>>(
+      n, d_pts, c->d_entry_of_point, c->d_offsets, c->d_orient, c->d_state[0], ref_dir[0],
+      ref_dir[1], ref_dir[2], d_out);
+  FB_CUDA(c, cudaGetLastError());
+  FB_CUDA(c, cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_pts);
+  cudaFree(d_out);
+  return FIBRA_OK;
 }
 
 int fibra_cuda_entry_kernel(const fibra_ctx* c, int32_t entry, int32_t* out) {

@@ -26,10 +26,16 @@ int main() {
   spec.nodes = 12;
   spec.fibers = 32;
   lib.entries.push_back(generate_network(spec, 102));
+  // a network beyond one CTA (1,900 fibers): solved on a thread-block cluster
+  spec.nodes = 712;
+  spec.fibers = 1900;
+  spec.neighbors = 10;
+  lib.entries.push_back(generate_network(spec, 7));
+  const int n_entries = 3;
   const int n = 8;
   BatchAssignment assign;
   std::mt19937_64 pick(7);
-  for (int p = 0; p < n; ++p) assign.entry_of_point.push_back(static_cast<int32_t>(pick() % 2));
+  for (int p = 0; p < n; ++p) assign.entry_of_point.push_back(static_cast<int32_t>(pick() % n_entries));
   PackedStates st;  // init_batch (batch.cpp:94-145) without the Eigen-dependent TU
   st.offsets.assign(n + 1, 0);
   for (int p = 0; p < n; ++p) {
@@ -55,9 +61,9 @@ int main() {
   const BatchResult br = fibra_b200::batch_response(lib, assign, st, FiberLaw{}, fs, RelaxConfig{},
                                                     StiffnessConfig{}, pool);
   // oracle
-  std::vector<or_network> onets(2);
+  std::vector<or_network> onets(n_entries);
   std::vector<const or_network*> optr;
-  for (int e = 0; e < 2; ++e) {
+  for (int e = 0; e < n_entries; ++e) {
     const FiberNetwork& net = lib.entries[e];
     std::vector<double> c(3 * net.n_nodes()), ar, mo;
     std::vector<int32_t> fa, fb;
@@ -86,7 +92,7 @@ int main() {
   std::vector<int32_t> status(n);
   or_batch_response(optr.data(), assign.entry_of_point.data(), n, st.offsets.data(), u.data(), v.data(),
                     a.data(), fi.data(), fd.data(), m.data(), im.data(), t.data(), it.data(), cv.data(),
-                    st.n_free.data(), &law, F.data(), &rc, 1e-5, 1, 1, 1, out.data(), status.data());
+                    st.n_free.data(), &law, F.data(), &rc, 1e-5, 1, 1, 8, out.data(), status.data());
   int bad = 0;
   for (int p = 0; p < n; ++p) {
     const double s6[6] = {br.responses[p].sigma.xx, br.responses[p].sigma.yy, br.responses[p].sigma.zz,

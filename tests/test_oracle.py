@@ -100,6 +100,21 @@ def test_relax_warm_and_capped_vs_reference_live(oracle_lib):
 
 
 @ref
+def test_orientation_p2_bitwise_vs_reference_live(oracle_lib):
+    """orientation_p2 (network.cpp:398-415) on a relaxed state and on the reference state."""
+    rn = O.ref_generate("knn", nodes=40, fibers=110, neighbors=10, seed=5)
+    on = O.network_from_ref(rn)
+    s, _ = O.ref_relax_solve(rn, np.diag([1.2, 0.95, 1.0]))
+    for d in ([1.0, 0.0, 0.0], [0.0, 0.6, 0.8], [0.3, -0.4, 0.8660254037844386]):
+        for u in (s.u, np.zeros_like(s.u)):
+            a = O.orientation_p2(on, u, d)
+            b = O.ref_orientation_p2(rn, u, d)
+            assert np.float64(a).view(np.uint64) == np.float64(b).view(np.uint64)
+    # stretching along x aligns fibres with x: P2 grows
+    assert O.orientation_p2(on, s.u, [1, 0, 0]) > O.orientation_p2(on, np.zeros_like(s.u), [1, 0, 0])
+
+
+@ref
 def test_internal_forces_bitwise_vs_reference_live(oracle_lib):
     rn = O.ref_generate("knn", nodes=60, fibers=200, neighbors=8, seed=3)
     on = O.network_from_ref(rn)
