@@ -119,8 +119,9 @@ def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
     oracle restatement.  Returns (rve_solves_per_s, kind, seconds, iterations, n_sampled)."""
     import oracle as O
     from paper_2306_09427_b200.synth import config1_spec
+    idx = sample_points(len(F), sample)  # evenly spaced: iteration counts are heavy-tailed
     if args.config == 2 and O.ref_available() and not args.tangent:
-        Fs = F[:sample]
+        Fs = F[idx]
         spec = config1_spec()
         rnet = O.ref_generate("knn", nodes=spec.nodes, fibers=spec.fibers,
                               neighbors=spec.neighbors, merge_radius=spec.merge_radius,
@@ -130,7 +131,6 @@ def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
         dt = time.perf_counter() - t0
         return len(Fs) / dt, "reference", dt, int(iters.sum()), len(Fs)
     O.build(ref=False)
-    idx = np.arange(min(sample, len(F))) if args.config == 2 else sample_points(len(F), sample)
     used = sorted({int(eop[i]) for i in idx})
     remap = {e: k for k, e in enumerate(used)}
     onets = [O.Network(nets[e].coords, nets[e].fiber_nodes[:, 0], nets[e].fiber_nodes[:, 1],
@@ -161,7 +161,7 @@ def run_reference(args, rank, world):
         iters += its
         done += k
     value = done / secs
-    which = "first" if args.config == 2 else "evenly spaced"
+    which = "evenly spaced"
     line = {"impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": scaling,
@@ -369,7 +369,7 @@ def main():
             nw = os.cpu_count() or 1
             sample = max(8, nw)
             r, kind, secs, its, k = cpu_sample_rate(args, nets, eop, F, nw, sample)
-            which = "first" if args.config == 2 else "evenly spaced"
+            which = "evenly spaced"
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": nw, "kind": kind,
                                     "sample": f"{which} {k} points of this workload on "
                                               f"{nw} host threads ({secs:.1f} s, {its} DR "

@@ -518,6 +518,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
         double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
+#pragma unroll 2
         for (int kp = 0; kp < npair[j]; ++kp) {  // two incidences per step
           const int2 ep = cent[kp * (NPT * T) + sl];
           const double* g0 = sm_at<double>(G, ep.x);  // this node's own signed record
