@@ -3,13 +3,19 @@
 // --fmad=false -lineinfo (see paper_2306_09427_b200/build.py).
 //
 // One fibra_cuda_solve == the reference batch_response (proj/src/batch.cpp:155-187) for
-// every point, split into three launches on the context stream:
+// every point:
 //   prep_kernel   per point: polar_decompose(F) (tensor.cpp:203-224), probe stretches
-//                 U + h T_q (stiffness.cpp:86-127); one thread per point
-//   dr_persistent_kernel   all DR solves (bases first, then probes) from a ticket queue
+//                 U + h T_q (stiffness.cpp:86-127), schedule key; one thread per point;
+//                 then a CUB radix sort orders the points longest-expected-first per class
+//   DR kernels    one persistent launch per kernel class (resident: dr_kernel.cuh, one RVE
+//                 per CTA; cluster: dr_cluster.cuh, one RVE per thread-block cluster), all
+//                 DR solves of the class (bases, then probes in base-completion order) from
+//                 the class's ticket queue; classes run concurrently on forked streams
 //   post_kernel   per point: A from probes (stiffness.cpp:15-41), C = push-forward(A, F)
 //                 (tensor.cpp:286-300), sigma = R sigma_U R^T (stiffness.cpp:171-173)
 #include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -46,7 +52,7 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
                             double fd_rel_step, PrepOut* prep, double* solve_F, int* solve_skip,
                             int* base_flag, int* done_list, int sched_mode,
                             const double* __restrict__ hint, const int* __restrict__ cls,
-                            unsigned long long* key) {
+                            unsigned* key, int* pidx) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double f[9];
@@ -69,9 +75,10 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
     const float k = static_cast<float>(hint[p]);
     hi = (k == k && k > 0) ? ~__float_as_uint(k) : 0xffffffffu;
   }
-  // [kernel class : 4][cost : 28][point : 32] -- the order is grouped by class
-  key[p] = (static_cast<unsigned long long>(cls[p]) << 60) |
-           (static_cast<unsigned long long>(hi >> 4) << 32) | static_cast<unsigned>(p);
+  // [kernel class : 4][cost : 28], sorted stably (ties keep point order) -- the order is
+  // grouped by class
+  key[p] = (static_cast<unsigned>(cls[p]) << 28) | (hi >> 4);
+  pidx[p] = p;
   if (!polar_decompose(f, o.R, o.U)) {  // KinematicsError -> failed point
     o.status = FIBRA_E_KINEMATICS;
     solve_skip[p] = FIBRA_E_KINEMATICS;
@@ -131,23 +138,6 @@ __global__ void orientation_kernel(int n, const int* __restrict__ points,
     wsum += len;
   }
   out[i] = wsum > 0 ? acc / wsum : 0.0;
-}
-
-// order[rank of key[p]] = p (keys are unique): a counting rank, O(n^2 / 256) smem compares,
-// a few microseconds at thousands of points
-__global__ void rank_kernel(int n, const unsigned long long* __restrict__ key, int* order) {
-  __shared__ unsigned long long tile[256];
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long k = p < n ? key[p] : 0;
-  int rank = 0;
-  for (int b = 0; b < n; b += 256) {
-    __syncthreads();
-    if (b + static_cast<int>(threadIdx.x) < n) tile[threadIdx.x] = key[b + threadIdx.x];
-    __syncthreads();
-    const int m = min(256, n - b);
-    for (int j = 0; j < m; ++j) rank += tile[j] < k;
-  }
-  if (p < n) order[rank] = p;
 }
 
 // homogenized_stress (network.cpp:341-372) from the boundary moment sums of a converged
@@ -368,7 +358,11 @@ struct fibra_ctx {
   int* d_flag = nullptr;
   int* d_done = nullptr;
   int* d_order = nullptr;
-  unsigned long long* d_key = nullptr;
+  unsigned* d_key = nullptr;             // schedule keys, sorted with the point ids by CUB
+  unsigned* d_key_sorted = nullptr;
+  int* d_pidx = nullptr;
+  void* d_sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
   fibra_point_result* d_res = nullptr;
   double* h_F = nullptr;                 // pinned staging
   fibra_point_result* h_res = nullptr;   // pinned staging
@@ -432,6 +426,13 @@ void free_scratch(fibra_ctx* c) {
   cudaFree(c->d_done);
   cudaFree(c->d_order);
   cudaFree(c->d_key);
+  cudaFree(c->d_key_sorted);
+  cudaFree(c->d_pidx);
+  cudaFree(c->d_sort_tmp);
+  c->d_key_sorted = nullptr;
+  c->d_pidx = nullptr;
+  c->d_sort_tmp = nullptr;
+  c->sort_tmp_bytes = 0;
   cudaFree(c->d_res);
   cudaFreeHost(c->h_F);
   cudaFreeHost(c->h_res);
@@ -477,6 +478,11 @@ int ensure_scratch(fibra_ctx* c, int n) {
   if ((rc = dalloc(c, &c->d_done, n))) return rc;
   if ((rc = dalloc(c, &c->d_order, n))) return rc;
   if ((rc = dalloc(c, &c->d_key, n))) return rc;
+  if ((rc = dalloc(c, &c->d_key_sorted, n))) return rc;
+  if ((rc = dalloc(c, &c->d_pidx, n))) return rc;
+  FB_CUDA(c, cub::DeviceRadixSort::SortPairs(nullptr, c->sort_tmp_bytes, c->d_key, c->d_key_sorted,
+                                             c->d_pidx, c->d_order, n));
+  FB_CUDA(c, cudaMalloc(&c->d_sort_tmp, std::max<size_t>(c->sort_tmp_bytes, 1)));
   if ((rc = dalloc(c, &c->d_res, n))) return rc;
   FB_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_F), 9 * sizeof(double) * n));
   FB_CUDA(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_res), sizeof(fibra_point_result) * n));
@@ -564,10 +570,11 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   prep_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, sc ? sc->fd_rel_step : 1e-5,
                                                 c->d_prep, c->d_solveF, c->d_skip, c->d_flag,
                                                 c->d_done, c->sched_mode, c->d_hint,
-                                                c->d_class_of_point, c->d_key);
+                                                c->d_class_of_point, c->d_key, c->d_pidx);
   FB_CUDA(c, cudaGetLastError());
-  rank_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, c->d_key, c->d_order);
-  FB_CUDA(c, cudaGetLastError());
+  size_t tmp_bytes = c->sort_tmp_bytes;  // longest expected solve first, grouped by class
+  FB_CUDA(c, cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tmp_bytes, c->d_key, c->d_key_sorted,
+                                             c->d_pidx, c->d_order, n, 0, 32, st));
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
   FB_CUDA(c, cudaEventRecord(c->ev_fork, st));
 
@@ -578,7 +585,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
     return c->classes[a].C > c->classes[b].C;
   });
-  int launches = 3;  // prep, rank, post
+  int launches = 2;  // ours: prep and post, plus one DR kernel per class (the sort is CUB's)
   bool prof_used = false;
   for (int ci : launch_order) {
     KClass& K = c->classes[ci];
@@ -1293,7 +1300,7 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
     cls[p] = c->entries[e].cls;
     ++c->classes[cls[p]].n_points;
   }
-  int off = 0;  // the schedule order groups points by class (rank_kernel keys)
+  int off = 0;  // the schedule order groups points by class (sort keys)
   for (auto& K : c->classes) {
     K.point_off = off;
     off += K.n_points;
