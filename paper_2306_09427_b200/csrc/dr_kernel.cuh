@@ -84,6 +84,7 @@ struct DrParams {
   const int* order;            // base ticket -> point (longest expected solve first)
   int* done_list;              // points in base-completion order (-1: not yet)
   int* ticket;                 // [0] next ticket, [1] done_list fill count
+  int first_wave_sms;          // > 0: the grid is two blocks per SM over this many SMs
   unsigned long long* counters;  // [0] iterations [1] fiber-iterations [2] pipe ops [3] solves
   double* ckpt;                // [grid][2][6][ck_stride]
   int ck_stride, ck_interval;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   int npair[NPT];
   double nref[NPT][3], ninv[NPT], ncm[NPT];
   int cur_entry = -1;
+  bool first_ticket = true;
   double s_uni = 0;  // UEA: the common ea_scale*EA
 #define SJ(j) (UEA ? s_uni : fs[j])
 
@@ -227,9 +229,20 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     // [nc, 7nc) are probes, served in the order base solves finish (six per finished base),
     // so a CTA only waits for a base when every finished base's probes are already taken.
     // Solve index: base p -> p, probe q of p -> n + 6p + q (the layout post_kernel reads);
-    // -1 = queue drained.
+    // -1 = queue drained.  The first wave is dealt by block index: the block scheduler puts
+    // blocks [0, #SM) one per SM and blocks [#SM, 2 #SM) in the second slots, so SM j runs
+    // tickets j and 2 #SM - 1 - j -- the longest expected solve next to the shortest of
+    // the wave, and two of the longest never share an SM; later tickets come from the
+    // counter.
     if (tid == 0) {
-      const int t = atomicAdd(P.ticket, 1);
+      int t;
+      if (first_ticket) {
+        const int b = static_cast<int>(blockIdx.x), m = P.first_wave_sms;
+        t = (m > 0 && b >= m) ? 3 * m - 1 - b : b;
+      } else {
+        t = static_cast<int>(gridDim.x) + atomicAdd(P.ticket, 1);
+      }
+      first_ticket = false;
       int s = -1;
       if (t < P.n_solves) {
         int p, q = -1, flag = 1;

@@ -611,6 +611,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.T, smem));
       if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "DR kernel does not fit on an SM");
       const int grid = std::min(n_solves, per_sm * c->n_sm);
+      P.first_wave_sms = (per_sm == 2 && grid == 2 * c->n_sm) ? c->n_sm : 0;
       if ((r = grow(c, &K.d_ckpt, K.ckpt_cap, static_cast<size_t>(grid) * 12 * K.ck_stride)))
         return r;
       P.entries = K.d_entries;
