@@ -150,7 +150,7 @@ def run_reference(args, rank, world):
     n_workers = os.cpu_count() or 1
     import paper_2306_09427_b200  # noqa: F401  (network generator only; no GPU use)
     nets, eop, F, desc, total, scaling = workload(args, 1, 0)
-    sample = max(8, 2 * n_workers)
+    sample = max(8, 4 * n_workers)  # >> threads: the heavy tail must not idle the pool
     for _ in range(max(1, min(args.warmup, 1))):
         cpu_sample_rate(args, nets, eop, F, n_workers, min(sample, n_workers))
     secs, iters, done = 0.0, 0, 0
@@ -356,7 +356,7 @@ def main():
             "roofline": {"bound": "fp64_pipe", "achieved": achieved / 1e9, "peak": peak / 1e9,
                          "unit": "Gop/s (FP64-pipe lane ops)", "frac": achieved / peak,
                          "traffic": measured_traffic(args, args.steps),
-                         "traffic_unit": "DRAM bytes per DR launch (ncu, profiles/r01_dr_traffic.json)",
+                         "traffic_unit": "DRAM bytes per DR launch (ncu --set full, profiles/r01_dr_traffic.json)",
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
@@ -367,7 +367,7 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             nw = os.cpu_count() or 1
-            sample = max(8, nw)
+            sample = max(8, 4 * nw)  # >> threads: the heavy tail must not idle the pool
             r, kind, secs, its, k = cpu_sample_rate(args, nets, eop, F, nw, sample)
             which = "evenly spaced"
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": nw, "kind": kind,
