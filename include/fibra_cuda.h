@@ -95,6 +95,9 @@ int fibra_assign_random(uint64_t seed, int32_t n_points, int32_t n_entries, int3
  * out[6] = {fits, conflicting fiber groups, gather excess wavefronts, gather steps,
  *           g*d records, node slots}. */
 int fibra_schedule_report(const fibra_net_desc* net, int T, int FPT, int NPT, int64_t* out);
+/* Diagnostics: that schedule's node slot placement, pn_of_slot[cap] (-1 = empty slot). */
+int fibra_schedule_slots(const fibra_net_desc* net, int T, int FPT, int NPT, int32_t* pn_of_slot,
+                         int32_t cap);
 /* Diagnostics: the cluster partition (csrc/host/cluster_schedule.cpp) of one network over C
  * CTAs of shape (T, FPT, NPT).  out[8] = {fits, max fibers per CTA, min fibers per CTA, max
  * node slots, max halo nodes, max records, max halo copies of a node, cross-CTA fibers}. */

@@ -270,6 +270,22 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
 }  // namespace fibra_b200
 
 // Diagnostics (C-ABI, no GPU needed): schedule quality of one network for a kernel shape.
+// Diagnostics: the node slot placement (packed node per slot, -1 empty) of that schedule.
+extern "C" int fibra_schedule_slots(const fibra_net_desc* d, int T, int FPT, int NPT,
+                                    int32_t* pn_of_slot, int32_t cap) {
+  const int N = d->n_nodes, M = d->n_fibers;
+  std::vector<int> a(M), b(M);
+  for (int f = 0; f < M; ++f) {
+    a[f] = d->fiber_packed_dofs[6 * f] / 3;
+    b[f] = d->fiber_packed_dofs[6 * f + 3] / 3;
+  }
+  fibra_b200::Schedule s;
+  if (!fibra_b200::build_schedule(N, d->n_free / 3, M, a.data(), b.data(), T, FPT, NPT, s))
+    return 21;
+  for (int i = 0; i < cap; ++i) pn_of_slot[i] = i < s.node_slots ? s.pn_of_slot[i] : -1;
+  return 0;
+}
+
 extern "C" int fibra_schedule_report(const fibra_net_desc* d, int T, int FPT, int NPT,
                                      int64_t* out) {
   const int N = d->n_nodes, M = d->n_fibers;
