@@ -276,6 +276,7 @@ def main():
 
     clocks = ClockSampler(local)
     total_ms, dr_ms, iters, pipe_ops, fiber_iters, failed, launches = 0.0, 0.0, 0, 0, 0, 0, 0
+    alg_flops = 0
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.start()
     for _ in range(args.steps):
@@ -295,6 +296,7 @@ def main():
         pipe_ops += s["pipe_ops"]
         fiber_iters += s["fiber_iterations"]
         launches += s["kernel_launches"]
+        alg_flops += s["alg_flops"]
     clk = clocks.stop()
     rec = np.frombuffer(out_dev.cpu().numpy().tobytes(), dtype=P.RESULT_DTYPE)[:n]
     failed_t = torch.tensor([int((rec["status"] != 0).sum())], device=f"cuda:{local}")
@@ -303,13 +305,13 @@ def main():
     failed = int(failed_t.item())
 
     t = torch.tensor([total_ms, dr_ms], dtype=torch.float64, device=f"cuda:{local}")
-    tot_iters = torch.tensor([iters, pipe_ops, fiber_iters], dtype=torch.float64,
+    tot_iters = torch.tensor([iters, pipe_ops, fiber_iters, alg_flops], dtype=torch.float64,
                              device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tot_iters, op=dist.ReduceOp.SUM)
     max_total_ms, max_dr_ms = t.tolist()
-    all_iters, all_pipe, all_fib = tot_iters.tolist()
+    all_iters, all_pipe, all_fib, all_flops = tot_iters.tolist()
     value = total * args.steps / (max_total_ms * 1e-3)
 
     # ---- end to end through the public API with host buffers ----
@@ -360,6 +362,12 @@ def main():
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
+            "alg_flops": {"achieved_tflops": all_flops / world / (max_dr_ms * 1e-3) / 1e12,
+                          "fma_peak_tflops": 2 * peak / 1e12,
+                          "frac": all_flops / world / (max_dr_ms * 1e-3) / (2 * peak),
+                          "model": "F_alg = 28 M + 12 n_free + 2 n_fix flops per RVE-iteration "
+                                   "(div and sqrt count 1; SURVEY 8d); peak = 2 x the measured "
+                                   "DADD lane-op rate (FMA-counted)"},
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,

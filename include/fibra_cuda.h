@@ -157,6 +157,8 @@ typedef struct {          /* per-call counters for reporting                    
   float dr_kernel_ms;     /* device time of the persistent DR kernel                 */
   float total_ms;         /* device time of the whole solve (prep + DR + post)       */
   int32_t kernel_launches;
+  int64_t alg_flops;      /* sum over solves of iterations * F_alg(net), F_alg = 28 M +
+                             12 n_free + 2 n_fix (div/sqrt count 1)         */
 } fibra_solve_stats;
 
 /* ---- device context ----------------------------------------------------------------- */

@@ -90,7 +90,7 @@ class SolveStats(C.Structure):
     _fields_ = [("solves", C.c_int64), ("iterations", C.c_int64),
                 ("fiber_iterations", C.c_int64), ("pipe_ops", C.c_int64),
                 ("dr_kernel_ms", C.c_float), ("total_ms", C.c_float),
-                ("kernel_launches", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("alg_flops", C.c_int64)]
 
 
 _lib = None

@@ -722,6 +722,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         atomicAdd(P.counters + 2, static_cast<unsigned long long>(n_done) *
                                       (51ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
         atomicAdd(P.counters + 3, 1ull);
+        atomicAdd(P.counters + 4, static_cast<unsigned long long>(n_done) *  // F_alg
+                                      (28ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
       }
     }
     if (is_base) {  // every CTA wrote part of the base state its probes warm-start from

@@ -86,6 +86,7 @@ struct DrParams {
   int* ticket;                 // [0] next ticket, [1] done_list fill count
   int first_wave_sms;          // > 0: the grid is two blocks per SM over this many SMs
   unsigned long long* counters;  // [0] iterations [1] fiber-iterations [2] pipe ops [3] solves
+                                 // [4] algorithmic flops
   double* ckpt;                // [grid][2][6][ck_stride]
   int ck_stride, ck_interval;
   int n_points;                // all bound points (solve index layout)
@@ -772,6 +773,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       atomicAdd(P.counters + 2, static_cast<unsigned long long>(n_done) *
                                     (51ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
       atomicAdd(P.counters + 3, 1ull);
+      atomicAdd(P.counters + 4, static_cast<unsigned long long>(n_done) *  // F_alg
+                                    (28ull * M + 12ull * 3 * NFN + 2ull * 3 * NFIX));
     }
     if (base_solve) {
       // every thread wrote part of the converged u its probes warm-start from: each one

@@ -565,7 +565,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   cudaStream_t st = c->stream;
   FB_CUDA(c, cudaEventRecord(c->ev[0], st));
   FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, 2 * kMaxClasses * sizeof(int), st));
-  FB_CUDA(c, cudaMemsetAsync(c->d_counters, 0, 4 * sizeof(unsigned long long), st));
+  FB_CUDA(c, cudaMemsetAsync(c->d_counters, 0, 5 * sizeof(unsigned long long), st));
   const int tb = 128;
   prep_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, sc ? sc->fd_rel_step : 1e-5,
                                                 c->d_prep, c->d_solveF, c->d_skip, c->d_flag,
@@ -1104,7 +1104,7 @@ int fibra_cuda_open(int device, fibra_ctx** out) {
   c->max_smem -= 4096;  // the kernels' static control blocks (ClusterCtl ~3 KB)
   if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
-  if (cudaMalloc(&c->d_counters, 4 * sizeof(unsigned long long)) != cudaSuccess)
+  if (cudaMalloc(&c->d_counters, 5 * sizeof(unsigned long long)) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
   for (auto& e : c->ev)
     if (cudaEventCreate(&e) != cudaSuccess) return bail(FIBRA_E_CUDA);
@@ -1512,13 +1512,14 @@ int fibra_cuda_synchronize(fibra_ctx* c) {
 int fibra_cuda_last_stats(fibra_ctx* c, fibra_solve_stats* s) {
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
-  unsigned long long cnt[4] = {0, 0, 0, 0};
+  unsigned long long cnt[5] = {0, 0, 0, 0, 0};
   FB_CUDA(c, cudaMemcpy(cnt, c->d_counters, sizeof cnt, cudaMemcpyDeviceToHost));
   std::memset(s, 0, sizeof *s);
   s->iterations = static_cast<int64_t>(cnt[0]);
   s->fiber_iterations = static_cast<int64_t>(cnt[1]);
   s->pipe_ops = static_cast<int64_t>(cnt[2]);
   s->solves = static_cast<int64_t>(cnt[3]);
+  s->alg_flops = static_cast<int64_t>(cnt[4]);
   float ms = 0;
   if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]) == cudaSuccess) s->dr_kernel_ms = ms;
   if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]) == cudaSuccess) s->total_ms = ms;
