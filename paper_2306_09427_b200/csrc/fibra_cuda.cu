@@ -312,6 +312,7 @@ struct KClass {
   int n_points = 0, point_off = 0;        // bound points of the class, offset in the order
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
+  cudaEvent_t done_t = nullptr;  // timed copy of `done` (FIBRA_CLASS_TIMES diagnostics)
   double* d_ckpt = nullptr;
   size_t ckpt_cap = 0;
   double* d_scratch = nullptr;
@@ -458,6 +459,7 @@ void free_library(fibra_ctx* c) {
     cudaFree(k.d_scratch);
     if (k.stream) cudaStreamDestroy(k.stream);
     if (k.done) cudaEventDestroy(k.done);
+    if (k.done_t) cudaEventDestroy(k.done_t);
   }
   c->classes.clear();
   cudaFree(c->d_orient);
@@ -673,6 +675,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     }
     FB_CUDA(c, cudaGetLastError());
     FB_CUDA(c, cudaEventRecord(K.done, K.stream));
+    FB_CUDA(c, cudaEventRecord(K.done_t, K.stream));
     FB_CUDA(c, cudaStreamWaitEvent(st, K.done, 0));
     ++launches;
   }
@@ -1279,6 +1282,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     }
     FB_CUDA(c, cudaStreamCreateWithFlags(&K.stream, cudaStreamNonBlocking));
     FB_CUDA(c, cudaEventCreateWithFlags(&K.done, cudaEventDisableTiming));
+    FB_CUDA(c, cudaEventCreate(&K.done_t));
   }
   return FIBRA_OK;
 }
@@ -1524,6 +1528,20 @@ int fibra_cuda_last_stats(fibra_ctx* c, fibra_solve_stats* s) {
   if (cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]) == cudaSuccess) s->dr_kernel_ms = ms;
   if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]) == cudaSuccess) s->total_ms = ms;
   s->kernel_launches = c->last_launches;
+  if (getenv("FIBRA_CLASS_TIMES"))  // diagnostics: per kernel class, ms from the fork
+    for (size_t k = 0; k < c->classes.size(); ++k) {
+      const KClass& K = c->classes[k];
+      if (!K.n_points) continue;
+      float t = -1;
+      cudaEventElapsedTime(&t, c->ev[1], K.done_t);
+      std::fprintf(stderr, "class %zu: %s %s C=%d points=%d done at %.1f ms\n", k,
+                   K.cluster ? "cluster" : "resident",
+                   K.cluster ? (std::to_string(kClusterVariants[K.vi].T) + "/" +
+                                std::to_string(kClusterVariants[K.vi].FPT)).c_str()
+                             : (std::to_string(kVariants[K.vi].T) + "/" +
+                                std::to_string(kVariants[K.vi].FPT)).c_str(),
+                   K.C, K.n_points, t);
+    }
   return FIBRA_OK;
 }
 
