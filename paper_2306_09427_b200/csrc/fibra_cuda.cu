@@ -580,12 +580,17 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
   FB_CUDA(c, cudaEventRecord(c->ev_fork, st));
 
-  // classes run concurrently; cluster classes (largest RVEs) are launched first
+  // classes run concurrently, each as a full persistent grid; resident classes launch first
+  // (config 3: their small, sparse RVEs relax longest; launching the clusters first left
+  // them waiting for SMs -- 10.97 s vs 10.40 s), later launches take SMs as earlier ones
+  // drain (FIBRA_RESIDENT_FIRST=0 reverses the order)
   std::vector<int> launch_order;
   for (int k = 0; k < static_cast<int>(c->classes.size()); ++k)
     if (c->classes[k].n_points) launch_order.push_back(k);
+  const char* lo_env = getenv("FIBRA_RESIDENT_FIRST");
+  const bool resident_first = !(lo_env && lo_env[0] == '0');
   std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
-    return c->classes[a].C > c->classes[b].C;
+    return resident_first ? c->classes[a].C < c->classes[b].C : c->classes[a].C > c->classes[b].C;
   });
   int launches = 2;  // ours: prep and post, plus one DR kernel per class (the sort is CUB's)
   bool prof_used = false;
