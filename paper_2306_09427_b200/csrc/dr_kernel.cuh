@@ -192,6 +192,12 @@ __device__ __forceinline__ double law_energy(double s, double stretch, double rl
   return rl * s / B * (expm1(B * e) / B - e);
 }
 
+// g*d record offsets in fib_g are 16-bit byte offsets >> kGShift: 8-byte units for the large
+// shapes (FPT >= 4: up to 512 KB of records, ~10k fibres), bytes otherwise (no shift in the
+// hot loop of the config-1/2 shape)
+template <int FPT>
+constexpr int kGShift = FPT >= 4 ? 3 : 0;
+
 // UEA: every fiber of the library has the same area*modulus (true for generated
 // networks), so the axial stiffness s = ea_scale*EA is one scalar instead of FPT registers.
 template <int T, int FPT, int NPT, int LAWBO, int MINB, bool UEA>
@@ -459,8 +465,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         }
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {  // head record +g*d, tail record (-g)*d == -(g*d)
-          double* gh = sm_at<double>(G, static_cast<unsigned>(fgo[j]) >> 16);
-          double* gt = sm_at<double>(G, fgo[j] & 0xffff);
+          double* gh = sm_at<double>(G, (static_cast<unsigned>(fgo[j]) >> 16) << kGShift<FPT>);
+          double* gt = sm_at<double>(G, (fgo[j] & 0xffff) << kGShift<FPT>);
           const double ng = -g[j];
           gh[0] = g[j] * dx[j];
           gh[1] = g[j] * dy[j];

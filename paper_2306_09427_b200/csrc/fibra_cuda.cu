@@ -752,7 +752,8 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
     return false;
   const int TS = v.NPT * v.T;
   const int gd_total = S.gd_slots + 33;
-  if (S.node_slots * 24 >= 65536 || 24 * gd_total >= 65536) return false;  // 16-bit offsets
+  const int gshift = v.FPT >= 4 ? 3 : 0;  // kGShift (dr_kernel.cuh)
+  if (S.node_slots * 24 >= 65536 || ((24 * gd_total) >> gshift) >= 65536) return false;  // 16 bit
   const size_t smem = align16(24 * static_cast<size_t>(TS + 2)) +
                       align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
                       8ull * TS + 4ull * (TS + 1) + 8ull * max_pairs * TS;
@@ -817,6 +818,7 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
                           const Variant& v, Arena& A, Caps& K) {
   const Schedule& S = de.sched;
   const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS, TS+1
+  const int gshift = v.FPT >= 4 ? 3 : 0;  // record offsets in 8-byte units (kGShift)
   const int FS = S.fiber_slots;
   std::vector<int> slot_pn(TS, -1);
   std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
@@ -869,11 +871,11 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     const int f = S.fiber_of_fslot[fs];
     if (f < 0) {  // dummy: unit segment between the two dummy x records
       fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
-      fg[fs] = (24 * dummy_tail[fs]) | ((24 * dummy_head[fs]) << 16);
+      fg[fs] = ((24 * dummy_tail[fs]) >> gshift) | (((24 * dummy_head[fs]) >> gshift) << 16);
       continue;
     }
     fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
-    fg[fs] = (24 * S.rec_tail[f]) | ((24 * S.rec_head[f]) << 16);
+    fg[fs] = ((24 * S.rec_tail[f]) >> gshift) | (((24 * S.rec_head[f]) >> gshift) << 16);
     fid[fs] = f;
     fl0[fs] = P.l0[f];
     fea[fs] = P.ea[f];
@@ -1178,6 +1180,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   std::vector<PackedNet> nets(n);
   std::vector<ClusterPlan> plans(n);
   std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1);
+  std::vector<Caps> est(n);  // the entry's shared-memory components (exact, = the build's)
   // diagnostics: FIBRA_FORCE_CLUSTER=C places every entry on a C-CTA cluster (kernel timing)
   const char* force_env = getenv("FIBRA_FORCE_CLUSTER");
   const int force_c = force_env ? atoi(force_env) : 0;
@@ -1193,7 +1196,15 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     de.n_nodes = P.N;
     const int mp = max_pairs_of(P);
     for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
-      if (resident_fits(c, P, kVariants[v], mp, de.sched)) kind_vi[i] = v;
+      if (resident_fits(c, P, kVariants[v], mp, de.sched)) {
+        kind_vi[i] = v;
+        const int TS = kVariants[v].NPT * kVariants[v].T;
+        est[i].ts = TS;
+        est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2)));
+        est[i].g_bytes = static_cast<int>(align16(std::max<size_t>(
+            24ull * (de.sched.gd_slots + 33), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
+        est[i].csr_cap = 2 * mp * TS;
+      }
     // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
     // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
     for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
@@ -1203,6 +1214,15 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             kind_vi[i] = v;
             kind_C[i] = cc;
             kind_cl[i] = 1;
+            const ClusterVariant& cv = kClusterVariants[v];
+            const int TS = cv.NPT * cv.T;
+            size_t max_h = 0;
+            for (const ClusterPart& q : plans[i].parts) max_h = std::max(max_h, q.h_fiber.size());
+            est[i].ts = TS;
+            est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2 + plans[i].max_halo)));
+            est[i].g_bytes = static_cast<int>(align16(24ull * (cv.FPT * (cv.T - 32) + max_h + 1)));
+            est[i].csr_cap = mp * TS;
+            est[i].push_cap = plans[i].max_push * TS;
           }
         }
   });
@@ -1213,10 +1233,17 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
                                          std::to_string(nets[i].N) +
                                          " nodes) exceeds a 16-CTA cluster");
     const bool cl = kind_cl[i] != 0;
+    // a class's footprint is the per-component maximum over its entries: join the first
+    // class of this kernel shape that still fits the device with this entry, else open one
+    auto fits_with = [&](const KClass& K) {
+      KClass T = K;
+      merge_caps(T, est[i]);
+      return T.smem() <= static_cast<size_t>(c->max_smem);
+    };
     int k = 0;
     const int nk = static_cast<int>(c->classes.size());
     while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].vi == kind_vi[i] &&
-                       c->classes[k].C == kind_C[i]))
+                       c->classes[k].C == kind_C[i] && fits_with(c->classes[k])))
       ++k;
     if (k == nk) {
       if (nk == kMaxClasses) return set_err(c, FIBRA_E_ARG, "too many kernel classes in one library");
@@ -1226,6 +1253,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       K.C = kind_C[i];
       c->classes.push_back(K);
     }
+    merge_caps(c->classes[k], est[i]);
     c->entries[i].cls = k;
     KClass& K = c->classes[k];
     const PackedNet& P = nets[i];

@@ -14,7 +14,7 @@ const Variant kVariants[] = {
     FB_V(256, 3, 1, 2),  // <= 256 node slots, <= 672 fibers
     FB_V(384, 3, 1, 2),  // <= 384 node slots, <= 1056 fibers (config 1/2 networks)
     FB_V(512, 2, 1, 2),  // <= 512 node slots, <= 960 fibers
-    FB_V(512, 4, 1, 1),  // <= 512 node slots; 16-bit record offsets cap fibers at ~1.3k
+    FB_V(512, 4, 1, 1),  // <= 512 node slots, <= 1920 fibers (record offsets in 8-byte units)
     FB_V(512, 6, 2, 1),  // <= 1024 node slots (node-heavy segments networks)
     FB_V(768, 7, 2, 1),  // <= 1536 node slots
 };

@@ -26,7 +26,7 @@ int main() {
   spec.nodes = 12;
   spec.fibers = 32;
   lib.entries.push_back(generate_network(spec, 102));
-  // a network beyond one CTA (1,900 fibers): solved on a thread-block cluster
+  // a 1,900-fibre network: one CTA of a large resident shape (8-byte record offsets)
   spec.nodes = 712;
   spec.fibers = 1900;
   spec.neighbors = 10;

@@ -37,7 +37,24 @@ def check_states(gst, ost, points=None):
             assert same_bits(g[sl], o[sl]), f"point {p}: state array {k} differs"
 
 
-def run(pnets, eop, F, tangent, relax=None, law=None):
+def run(pnets, eop, F, tangent, relax=None, law=None, force_cluster=None):
+    """batch_response on the GPU; `force_cluster` = C puts every entry on a C-CTA cluster
+    (FIBRA_FORCE_CLUSTER) -- networks up to ~2.5k fibres would otherwise run resident."""
+    import os
+    old = os.environ.get("FIBRA_FORCE_CLUSTER")
+    if force_cluster:
+        os.environ["FIBRA_FORCE_CLUSTER"] = str(force_cluster)
+    try:
+        return _run(pnets, eop, F, tangent, relax, law)
+    finally:
+        if force_cluster:
+            if old is None:
+                del os.environ["FIBRA_FORCE_CLUSTER"]
+            else:
+                os.environ["FIBRA_FORCE_CLUSTER"] = old
+
+
+def _run(pnets, eop, F, tangent, relax=None, law=None):
     lib = P.RveLibrary(list(pnets), policy="explicit", explicit_assignment=list(eop))
     st, assign = P.init_batch(np.zeros(len(eop), np.int32), lib, 0)
     db = P.DeviceBatch(lib, assign)
@@ -73,8 +90,8 @@ def mid_net(oracle_lib):
 def test_cluster_stress_bitwise(mid_net):
     pn, on = mid_net
     F = batch_F(6)
-    br, st, shapes = run([pn], [0] * 6, F, tangent=False)
-    assert shapes[0]["cluster"] >= 2
+    br, st, shapes = run([pn], [0] * 6, F, tangent=False, force_cluster=2)
+    assert shapes[0]["cluster"] == 2
     resp, status, ost = oracle_batch([on], [0] * 6, F, tangent=False)
     check_records(br, resp, status, tangent=False)
     check_states(st, ost)
@@ -84,15 +101,15 @@ def test_cluster_2500_fibers_bitwise(oracle_lib):
     """A config-3 size between the shapes (2.5k fibers: 2 CTAs of the (384, 4, 1) shape)."""
     pn, on = knn(625, 2500, 11)
     F = batch_F(4)
-    br, st, shapes = run([pn], [0] * 4, F, tangent=False)
+    br, st, shapes = run([pn], [0] * 4, F, tangent=False, force_cluster=2)
     assert shapes[0]["cluster"] == 2 and shapes[0]["fibers_per_thread"] == 4
     resp, status, ost = oracle_batch([on], [0] * 4, F, tangent=False)
     check_records(br, resp, status, tangent=False)
     check_states(st, ost)
 
 
-def test_cluster_tangent_mixed_library(mid_net):
-    pn, on = mid_net
+def test_cluster_tangent_mixed_library(oracle_lib):
+    pn, on = lattice_pair(12, 6000, 5)  # beyond the resident shapes: a cluster entry
     sp, so = knn(14, 38, 101, neighbors=9)
     F = batch_F(4)
     eop = [1, 0, 1, 0]
@@ -122,7 +139,7 @@ def test_cluster_exponential_law(mid_net):
     pn, on = mid_net
     F = batch_F(3)
     law = P.FiberLaw(kind="exponential", nonlinearity=4.0)
-    br, st, shapes = run([pn], [0] * 3, F, tangent=True, law=law)
+    br, st, shapes = run([pn], [0] * 3, F, tangent=True, law=law, force_cluster=2)
     assert shapes[0]["cluster"] >= 2
     resp, status, ost = oracle_batch([on], [0] * 3, F, tangent=True,
                                      law=O.Law(kind=1, nonlinearity=4.0))
@@ -145,7 +162,7 @@ def test_cluster_config3_size_capped(oracle_lib):
 def test_cluster_identity_and_collapse(mid_net):
     pn, on = mid_net
     F = np.stack([np.eye(3), np.diag([1e-9, 1e-9, 1e-9]), batch_F(1)[0]])
-    br, st, _ = run([pn], [0] * 3, F, tangent=False)
+    br, st, _ = run([pn], [0] * 3, F, tangent=False, force_cluster=2)
     resp, status, ost = oracle_batch([on], [0] * 3, F, tangent=False)
     assert br.records[0]["base_report"]["iterations"] == 0
     assert br.records[1]["status"] == 3 and status[1] == 3

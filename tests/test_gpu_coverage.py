@@ -56,13 +56,24 @@ def with_random_ea(pn, seed):
     return net, onet
 
 
-@pytest.mark.parametrize("size", [(375, 1000, 1), (712, 1900, 7)])
-def test_nonuniform_ea_bitwise(oracle_lib, size):
+@pytest.mark.parametrize("size,force", [((375, 1000, 1), None), ((712, 1900, 7), "2")])
+def test_nonuniform_ea_bitwise(oracle_lib, size, force, monkeypatch):
+    if force:  # the cluster kernel's non-uniform-EA instances
+        monkeypatch.setenv("FIBRA_FORCE_CLUSTER", force)
     pn, _ = knn(*size)
     net, onet = with_random_ea(pn, 17)
     assert not np.all(net.fiber_area == net.fiber_area[0])
     br, st, resp, status, ost, shape = solve(net, onet, batch_F(3), tangent=True)
-    assert shape["cluster"] == (1 if size[1] == 1000 else 2)
+    assert shape["cluster"] == (2 if force else 1)
+    check(br, st, resp, status, ost, tangent=True)
+
+
+def test_large_resident_shapes_bitwise(oracle_lib):
+    """1.9k-fibre knn RVEs run on one CTA of a large resident shape (g*d record offsets in
+    8-byte units), stress and tangent bitwise."""
+    pn, on = knn(712, 1900, 7)
+    br, st, resp, status, ost, shape = solve(pn, on, batch_F(3), tangent=True)
+    assert shape["cluster"] == 1 and shape["fibers_per_thread"] >= 4
     check(br, st, resp, status, ost, tangent=True)
 
 

@@ -18,7 +18,9 @@ pytestmark = pytest.mark.gpu
 
 def test_provider_warm_calls_and_orientation(oracle_lib):
     small, osmall = knn(20, 56, 31)
-    big, obig = knn(712, 1900, 7)
+    big = P.generate_lattice_network(12, 6000, 5)  # a cluster entry (beyond the resident shapes)
+    obig = O.Network(big.coords, big.fiber_nodes[:, 0], big.fiber_nodes[:, 1], big.fiber_area,
+                     big.fiber_modulus, big.box_half)
     lib = P.RveLibrary([small, big])
     n = 6
     prov = P.NetworkBatchProvider(np.zeros(n, np.int32), lib, seed=3)
