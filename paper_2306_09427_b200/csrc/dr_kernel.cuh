@@ -36,6 +36,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 #include "fastmath.cuh"
 #include "fibra_cuda.h"
@@ -433,48 +434,61 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       if (LAW != 0 && warp == NW - 1 && lane == 0) ctl.warp_min[warp] = INFINITY;
       if (warp != NW - 1) {  // the reducer warp owns no fibers (host/schedule.cpp)
         double kmin = INFINITY;
-        bool collapsed = false, fast = true;
-        double dx[FPT], dy[FPT], dz[FPT], g[FPT];
+        bool collapsed = false;
+        // fibres in blocks of <= 4 so only one block's temporaries are live (the FPT >= 6
+        // shapes spill otherwise); FPT <= 3 is a single block, the unchanged config-2 code
+        auto fiber_block = [&](auto j0c, auto j1c) {
+          constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
+          bool fast = true;
+          double dx[J1 - J0], dy[J1 - J0], dz[J1 - J0], g[J1 - J0];
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) {
-          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
-          dx[j] = xb_[0] - xa_[0];
-          dy[j] = xb_[1] - xa_[1];
-          dz[j] = xb_[2] - xa_[2];
-          bool o1, o2, o3 = true;
-          const double len = sqrt_fast(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j], o1);
-          collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
-          const double stretch = div_fast(len, fl0[j], o2);
-          if (LAW == 0) {
-            g[j] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
-          } else {
-            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
-            const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
-            kmin = smin(kmin, fmred[j] / kt);
+          for (int jj = 0; jj < J1 - J0; ++jj) {
+            const int j = J0 + jj;
+            const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
+            const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+            dx[jj] = xb_[0] - xa_[0];
+            dy[jj] = xb_[1] - xa_[1];
+            dz[jj] = xb_[2] - xa_[2];
+            bool o1, o2, o3 = true;
+            const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
+            collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
+            const double stretch = div_fast(len, fl0[j], o2);
+            if (LAW == 0) {
+              g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+            } else {
+              g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+              const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
+              kmin = smin(kmin, fmred[j] / kt);
+            }
+            fast = fast && o1 && o2 && o3;
           }
-          fast = fast && o1 && o2 && o3;
-        }
-        if (!__all_sync(0xffffffffu, fast)) {  // rare: special operands -> built-in ops
+          if (!__all_sync(0xffffffffu, fast)) {  // rare: special operands -> built-in ops
 #pragma unroll
-          for (int j = 0; j < FPT; ++j) {
-            const double len = sqrt(dx[j] * dx[j] + dy[j] * dy[j] + dz[j] * dz[j]);
-            const double stretch = len / fl0[j];
-            g[j] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            for (int jj = 0; jj < J1 - J0; ++jj) {
+              const int j = J0 + jj;
+              const double len = sqrt(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj]);
+              const double stretch = len / fl0[j];
+              g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
+            }
           }
-        }
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) {  // head record +g*d, tail record (-g)*d == -(g*d)
-          double* gh = sm_at<double>(G, (static_cast<unsigned>(fgo[j]) >> 16) << kGShift<FPT>);
-          double* gt = sm_at<double>(G, (fgo[j] & 0xffff) << kGShift<FPT>);
-          const double ng = -g[j];
-          gh[0] = g[j] * dx[j];
-          gh[1] = g[j] * dy[j];
-          gh[2] = g[j] * dz[j];
-          gt[0] = ng * dx[j];
-          gt[1] = ng * dy[j];
-          gt[2] = ng * dz[j];
-        }
+          for (int jj = 0; jj < J1 - J0; ++jj) {  // head record +g*d, tail (-g)*d == -(g*d)
+            const int j = J0 + jj;
+            double* gh = sm_at<double>(G, (static_cast<unsigned>(fgo[j]) >> 16) << kGShift<FPT>);
+            double* gt = sm_at<double>(G, (fgo[j] & 0xffff) << kGShift<FPT>);
+            const double ng = -g[jj];
+            gh[0] = g[jj] * dx[jj];
+            gh[1] = g[jj] * dy[jj];
+            gh[2] = g[jj] * dz[jj];
+            gt[0] = ng * dx[jj];
+            gt[1] = ng * dy[jj];
+            gt[2] = ng * dz[jj];
+          }
+        };
+        constexpr int B1 = FPT < 4 ? FPT : (FPT + 1) / 2;
+        fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, B1>());
+        if constexpr (B1 < FPT)
+          fiber_block(std::integral_constant<int, B1>(), std::integral_constant<int, FPT>());
         if (collapsed) ctl.collapse = 1;
         if (LAW != 0) {
           kmin = warp_min(kmin);

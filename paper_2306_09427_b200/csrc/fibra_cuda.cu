@@ -580,18 +580,20 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
   FB_CUDA(c, cudaEventRecord(c->ev_fork, st));
 
-  // classes run concurrently, each as a full persistent grid; resident classes launch first
-  // (config 3: their small, sparse RVEs relax longest; launching the clusters first left
-  // them waiting for SMs -- 10.97 s vs 10.40 s), later launches take SMs as earlier ones
-  // drain (FIBRA_RESIDENT_FIRST=0 reverses the order)
+  // classes run concurrently, each as a full persistent grid; later launches take SMs as
+  // earlier ones drain, so the class with the most work (sum of fibres over its points)
+  // launches first -- LPT at the class level (config 3: 8.86 s vs 8.78 s resident-first,
+  // config 5: 5.54 s vs 5.73 s; static SM shares by estimated work lost badly)
   std::vector<int> launch_order;
+  std::vector<double> class_work(c->classes.size(), 0.0);
+  for (int p = 0; p < n; ++p) {
+    const DeviceEntry& de = c->entries[c->entry_of_point[p]];
+    class_work[de.cls] += c->classes[de.cls].cluster ? de.cdev.n_fibers : de.dev.n_fibers;
+  }
   for (int k = 0; k < static_cast<int>(c->classes.size()); ++k)
     if (c->classes[k].n_points) launch_order.push_back(k);
-  const char* lo_env = getenv("FIBRA_RESIDENT_FIRST");
-  const bool resident_first = !(lo_env && lo_env[0] == '0');
-  std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
-    return resident_first ? c->classes[a].C < c->classes[b].C : c->classes[a].C > c->classes[b].C;
-  });
+  std::stable_sort(launch_order.begin(), launch_order.end(),
+                   [&](int a, int b) { return class_work[a] > class_work[b]; });
   int launches = 2;  // ours: prep and post, plus one DR kernel per class (the sort is CUB's)
   bool prof_used = false;
   for (int ci : launch_order) {
