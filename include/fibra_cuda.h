@@ -102,6 +102,13 @@ int fibra_schedule_slots(const fibra_net_desc* net, int T, int FPT, int NPT, int
  * CTAs of shape (T, FPT, NPT).  out[8] = {fits, max fibers per CTA, min fibers per CTA, max
  * node slots, max halo nodes, max records, max halo copies of a node, cross-CTA fibers}. */
 int fibra_cluster_report(const fibra_net_desc* net, int C, int T, int FPT, int NPT, int64_t* out);
+/* Diagnostics (no CUDA): one cluster-kernel force pass emulated on the host from the
+ * uploaded per-CTA arrays (f_emul) vs direct assembly (f_direct); u, f over 3 n_nodes packed
+ * dofs.  shape indexes the cluster shapes. */
+int fibra_debug_cluster_forces(const fibra_net_desc* net, int C, int shape, int mirror,
+                               const double* u, double* f_emul, double* f_direct);
+int fibra_debug_resident_forces(const fibra_net_desc* net, int shape, const double* u,
+                                double* f_emul, double* f_direct);
 
 /* ---- solver configuration records ------------------------------------------------- */
 typedef struct {          /* FiberLaw network.hpp:27-38                              */

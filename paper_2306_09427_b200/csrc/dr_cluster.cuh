@@ -65,6 +65,8 @@ struct ClusterParams {
   double* scratch;          // per cluster: SF[3N] | SX[3N] | SW[3 NFN] | SE[M]
   long long scratch_stride;
   int push_cap;             // push_dst ints staged in shared memory
+  int halo_stride;          // bytes between the two halo banks (mirror mode)
+  int debug_no_local;       // diagnostics: cluster barrier for the fiber -> node handoff too
   int pad;
 };
 
@@ -136,7 +138,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   const int lane = tid & 31, warp = tid >> 5;
   const unsigned rank = cl_rank(), C = cl_size();
 
-  // shared layout: [X: own slots | 2 dummy | halo][G: records][SPART][CSR pairs][push list]
+  // shared layout: [X: own slots | 2 dummy | halo bank 0 | halo bank 1][G: records][SPART]
+  //                [CSR pairs][push list]
   unsigned char* X = smem;
   unsigned char* G = smem + P.x_bytes;
   double* spart = reinterpret_cast<double*>(G + P.g_bytes);
@@ -213,7 +216,16 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
 
     const ClusterEntryDev& E = CP.centries[e];
     const PartDev& Q = E.parts[rank];
-    const bool local_handoff = LAW == 0 && E.mirror;
+    const bool local_handoff = LAW == 0 && E.mirror && !CP.debug_no_local;
+    // With a CTA barrier only between the phases, a neighbour may already push x of pass
+    // k+1 while this CTA still reads the halo of pass k: halo copies are double-buffered by
+    // pass parity (it cannot get two passes ahead: the cluster barrier after every node
+    // phase bounds it).  Fixed nodes' copies are written to both banks at setup.
+    const int hbase = 24 * (TS + 2);
+    const int bank_stride = local_handoff ? CP.halo_stride : 0;
+    auto xat = [&](int off, int bank) {  // x record: own slot, or halo copy in `bank`
+      return sm_at<double>(X, off + (off >= hbase ? bank * bank_stride : 0));
+    };
     const double scale = P.density_scale / E.max_lump;  // setup_mass relax.cpp:35-43
     const int F0 = Q.f0, NSLOT = Q.node_slots;
     if (e != cur_entry) {
@@ -242,10 +254,11 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         nref[j][2] = Q.slot_ref[3 * sl + 2];
       }
     }
-    auto push_x = [&](int j, int sl, double x0, double x1, double x2) {
+    auto push_x = [&](int j, int sl, double x0, double x1, double x2, int bank) {
       for (int h = 0; h < npush[j]; ++h) {
         const int d = pushd[h * TS + sl];
-        const unsigned a = cl_map(X_sh + (d & 0xffff), static_cast<unsigned>(d) >> 16);
+        const unsigned a = cl_map(X_sh + (d & 0xffff) + bank * bank_stride,
+                                  static_cast<unsigned>(d) >> 16);
         cl_st_f64(a, x0);
         cl_st_f64(a + 8, x1);
         cl_st_f64(a + 16, x2);
@@ -261,8 +274,9 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
     double lmin = INFINITY;
 #pragma unroll
     for (int j = 0; j < FPT; ++j) {  // reduced_mass_l0 relax.cpp:46-55
+      // dummies read the unit segment at TS (in mirror mode a real tail may be a halo node)
       const int ta = (fab[j] & 0xffff) / 24;
-      if (ta < TS) {
+      if (ta != TS) {
         const double ma = Q.fib_lt[j * T + tid] * scale;
         const double mb = Q.fib_lh[j * T + tid] * scale;
         fmred[j] = ma * mb / (ma + mb) * fl0[j];
@@ -310,7 +324,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       xr[0] = nref[j][0] + u[j][0];
       xr[1] = nref[j][1] + u[j][1];
       xr[2] = nref[j][2] + u[j][2];
-      push_x(j, sl, xr[0], xr[1], xr[2]);
+      push_x(j, sl, xr[0], xr[1], xr[2], 0);
+      if (sl >= F0 && bank_stride) push_x(j, sl, xr[0], xr[1], xr[2], 1);  // never updated
       if (sl < F0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -384,8 +399,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
 #pragma unroll
           for (int jj = 0; jj < J1 - J0; ++jj) {
             const int j = J0 + jj;
-            const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-            const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+            const double* xa_ = xat(fab[j] & 0xffff, k & 1);
+            const double* xb_ = xat(static_cast<int>(static_cast<unsigned>(fab[j]) >> 16), k & 1);
             dx[jj] = xb_[0] - xa_[0];
             dy[jj] = xb_[1] - xa_[1];
             dz[jj] = xb_[2] - xa_[2];
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
               xr[0] = nref[j][0] + u[j][0];
               xr[1] = nref[j][1] + u[j][1];
               xr[2] = nref[j][2] + u[j][2];
-              push_x(j, sl, xr[0], xr[1], xr[2]);
+              push_x(j, sl, xr[0], xr[1], xr[2], k & 1);
             }
           }
           if (tid == 0) ctl.t = ctl.ck_t[b];
@@ -612,7 +627,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
           xr[0] = nref[j][0] + u[j][0];
           xr[1] = nref[j][1] + u[j][1];
           xr[2] = nref[j][2] + u[j][2];
-          push_x(j, sl, xr[0], xr[1], xr[2]);
+          push_x(j, sl, xr[0], xr[1], xr[2], (k + 1) & 1);
           if (save) {
             double* ck = ckpt + sb * 6 * P.ck_stride;
 #pragma unroll
@@ -645,8 +660,8 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       for (int j = 0; j < FPT; ++j) {
         const int f = Q.fib_id[j * T + tid];
         if (f >= 0) {  // strain_energy relax.cpp:57-72, from the final x records
-          const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-          const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+          const double* xa_ = xat(fab[j] & 0xffff, k & 1);
+          const double* xb_ = xat(static_cast<int>(static_cast<unsigned>(fab[j]) >> 16), k & 1);
           const double dx = xb_[0] - xa_[0];
           const double dy = xb_[1] - xa_[1];
           const double dz = xb_[2] - xa_[2];

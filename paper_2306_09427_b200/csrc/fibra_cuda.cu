@@ -305,6 +305,7 @@ struct KClass {
   bool cluster = false;
   int vi = 0, C = 1;
   int x_bytes = 0, g_bytes = 0, ts = 0, csr_cap = 0, push_cap = 0, ck_stride = 0;
+  int max_halo = 0;  // cluster: halo slots per bank (two banks, dr_cluster.cuh)
   long long scratch_stride = 0;
   bool uniform_ea = true;
   EntryDev* d_entries = nullptr;          // [n_entries] (resident)
@@ -677,6 +678,8 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       CP.scratch = K.d_scratch;
       CP.scratch_stride = K.scratch_stride;
       CP.push_cap = K.push_cap;
+      CP.halo_stride = 24 * K.max_halo;
+      CP.debug_no_local = getenv("FIBRA_CLUSTER_NO_LOCAL") ? 1 : 0;
       CP.pad = 0;
       FB_CUDA(c, cudaLaunchKernelEx(&cfg, fn, CP));
     }
@@ -765,8 +768,11 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
 bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& v, int C,
                   int max_pairs, ClusterPlan& plan) {
   // mirror mode first (one cluster barrier per iteration), else copies of remote records
-  if (!build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
-                          v.NPT, true, plan) &&
+  // (diagnostics: FIBRA_CLUSTER_MIRROR=0 disables mirror mode)
+  const char* me = getenv("FIBRA_CLUSTER_MIRROR");
+  const bool try_mirror = !(me && me[0] == '0');
+  if (!(try_mirror && build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(),
+                                         C, v.T, v.FPT, v.NPT, true, plan)) &&
       !build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
                           v.NPT, false, plan))
     return false;
@@ -774,7 +780,7 @@ bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& 
   if (24 * (TS + 2 + plan.max_halo) >= 65536) return false;  // 16-bit x offsets
   size_t max_h = 0;
   for (const ClusterPart& q : plan.parts) max_h = std::max(max_h, q.h_fiber.size());
-  const size_t smem = align16(24ull * (TS + 2 + plan.max_halo)) +
+  const size_t smem = align16(24ull * (TS + 2 + 2 * plan.max_halo)) +
                       align16(24ull * (v.FPT * (v.T - 32) + max_h + 1)) + 8ull * TS +
                       8ull * max_pairs * TS + 4ull * plan.max_push * TS;
   return smem <= static_cast<size_t>(c->max_smem);
@@ -801,7 +807,7 @@ struct Arena {
 
 // kernel-class capacities one entry needs (merged into its KClass after the parallel build)
 struct Caps {
-  int ts = 0, x_bytes = 0, g_bytes = 0, csr_cap = 0, push_cap = 0;
+  int ts = 0, x_bytes = 0, g_bytes = 0, csr_cap = 0, push_cap = 0, max_halo = 0;
   long long scratch_stride = 0;
 };
 
@@ -812,6 +818,7 @@ void merge_caps(KClass& K, const Caps& e) {
   K.g_bytes = std::max(K.g_bytes, e.g_bytes);
   K.csr_cap = std::max(K.csr_cap, e.csr_cap);
   K.push_cap = std::max(K.push_cap, e.push_cap);
+  K.max_halo = std::max(K.max_halo, e.max_halo);
   K.scratch_stride = std::max(K.scratch_stride, e.scratch_stride);
 }
 
@@ -1061,7 +1068,8 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
   E.mirror = plan.mirror ? 1 : 0;
   parts_off = A.reserve(sizeof(PartDev) * C);  // filled at commit, once pointers are known
   K.ts = TS;
-  K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + plan.max_halo)));
+  K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + 2 * plan.max_halo)));
+  K.max_halo = plan.max_halo;
   K.g_bytes = static_cast<int>(align16(24ull * max_rec));
   K.csr_cap = max_pairs_all * TS;
   K.push_cap = max_push_all * TS;
@@ -1221,7 +1229,8 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             size_t max_h = 0;
             for (const ClusterPart& q : plans[i].parts) max_h = std::max(max_h, q.h_fiber.size());
             est[i].ts = TS;
-            est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2 + plans[i].max_halo)));
+            est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2 + 2 * plans[i].max_halo)));
+            est[i].max_halo = plans[i].max_halo;
             est[i].g_bytes = static_cast<int>(align16(24ull * (cv.FPT * (cv.T - 32) + max_h + 1)));
             est[i].csr_cap = mp * TS;
             est[i].push_cap = plans[i].max_push * TS;
@@ -1577,6 +1586,170 @@ int fibra_cuda_last_stats(fibra_ctx* c, fibra_solve_stats* s) {
                                 std::to_string(kVariants[K.vi].FPT)).c_str(),
                    K.C, K.n_points, t);
     }
+  return FIBRA_OK;
+}
+
+// Diagnostics: emulate one force pass of the cluster kernel on the host from exactly the
+// per-CTA arrays the upload builds (x pushes, fiber records, signed CSR gather), next to a
+// direct per-fiber assembly.  g = ea * (L - l0) / (l0 * L) stands in for the law; the two
+// force vectors must agree to rounding.  No CUDA calls.
+int fibra_debug_cluster_forces(const fibra_net_desc* d, int C, int shape, int mirror,
+                               const double* u, double* f_emul, double* f_direct) {
+  if (!d || !u || !f_emul || !f_direct || shape < 0 || shape >= kNumClusterVariants) return FIBRA_E_ARG;
+  const PackedNet P = pack(*d);
+  const ClusterVariant& v = kClusterVariants[shape];
+  ClusterPlan plan;
+  if (!build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T, v.FPT,
+                          v.NPT, mirror != 0, plan))
+    return FIBRA_E_CONFIG;
+  DeviceEntry de;
+  Arena A;
+  std::vector<PartDev> parts;
+  size_t parts_off = 0;
+  Caps K;
+  build_cluster_entry(de, P, *d, plan, v, A, parts, parts_off, K);
+  for (auto& f : A.fixes) {
+    const void* addr = A.host.data() + f.second;
+    std::memcpy(f.first, &addr, sizeof addr);
+  }
+  const int T = v.T, TS = v.NPT * T, FS = v.FPT * T, FT = T - 32;
+  const int hs = 3 * (TS + 2 + plan.max_halo);
+  std::vector<std::vector<double>> X(C, std::vector<double>(hs, 0.0));
+  std::vector<std::vector<double>> G(C);
+  for (int q = 0; q < C; ++q) G[q].assign(3 * static_cast<size_t>(parts[q].n_records), 0.0);
+  auto x_of = [&](int pn, int c) { return P.ref[3 * pn + c] + u[3 * pn + c]; };
+  for (int q = 0; q < C; ++q) {  // own x and pushes
+    const PartDev& D = parts[q];
+    X[q][3 * TS + 3] = 1.0;  // dummy records at TS, TS+1: unit segment
+    for (int sl = 0; sl < TS; ++sl) {
+      const int pn = D.slot_pn[sl];
+      if (pn < 0) continue;
+      for (int c = 0; c < 3; ++c) X[q][3 * sl + c] = x_of(pn, c);
+      for (int h = 0; h < D.push_n[sl]; ++h) {
+        const int dd = D.push_dst[static_cast<size_t>(h) * TS + sl];
+        const int r = static_cast<unsigned>(dd) >> 16, o = (dd & 0xffff) / 8;
+        if (r >= C || o + 2 >= hs) return 100 + q;
+        for (int c = 0; c < 3; ++c) X[r][o + c] = x_of(pn, c);
+      }
+    }
+  }
+  for (int q = 0; q < C; ++q) {  // fiber records (+ remote copies)
+    const PartDev& D = parts[q];
+    for (int fs = 0; fs < FS; ++fs) {
+      if (fs % T >= FT || D.fib_id[fs] < 0) continue;
+      const int ta = (D.fib_ab[fs] & 0xffff) / 8, hb = (static_cast<unsigned>(D.fib_ab[fs]) >> 16) / 8;
+      double dx[3], dd = 0;
+      for (int c = 0; c < 3; ++c) {
+        dx[c] = X[q][hb + c] - X[q][ta + c];
+        dd += dx[c] * dx[c];
+      }
+      const double L = std::sqrt(dd), l0 = D.fib_l0[fs];
+      const double g = D.fib_ea[fs] * (L - l0) / (l0 * L);
+      const int go = D.fib_gt[fs] / 8;
+      for (int c = 0; c < 3; ++c) G[q][go + c] = g * dx[c];
+      if (D.fib_gh[fs] >= 0) {
+        const int r = static_cast<unsigned>(D.fib_gh[fs]) >> 24, o = (D.fib_gh[fs] & 0xffffff) / 8;
+        for (int c = 0; c < 3; ++c) G[r][o + c] = g * dx[c];
+      }
+    }
+  }
+  for (int i = 0; i < 3 * P.N; ++i) f_emul[i] = f_direct[i] = 0.0;
+  for (int q = 0; q < C; ++q) {  // signed CSR gather of own nodes
+    const PartDev& D = parts[q];
+    for (int sl = 0; sl < TS; ++sl) {
+      const int pn = D.slot_pn[sl];
+      if (pn < 0) continue;
+      for (int i = 0; i < 2 * D.csr_npairs[sl]; ++i) {
+        const int e = reinterpret_cast<const int*>(D.csr_pairs)[2 * ((i / 2) * TS + sl) + (i % 2)];
+        const int o = (e & 0x7fffffff) / 8;
+        const double sg = (e < 0) ? -1.0 : 1.0;
+        for (int c = 0; c < 3; ++c) f_emul[3 * pn + c] += sg * G[q][o + c];
+      }
+    }
+  }
+  for (int f = 0; f < P.M; ++f) {
+    double dx[3], dd = 0;
+    for (int c = 0; c < 3; ++c) {
+      dx[c] = x_of(P.b[f], c) - x_of(P.a[f], c);
+      dd += dx[c] * dx[c];
+    }
+    const double L = std::sqrt(dd);
+    const double g = P.ea[f] * (L - P.l0[f]) / (P.l0[f] * L);
+    for (int c = 0; c < 3; ++c) {
+      f_direct[3 * P.b[f] + c] += g * dx[c];
+      f_direct[3 * P.a[f] + c] -= g * dx[c];
+    }
+  }
+  return FIBRA_OK;
+}
+
+// Diagnostics: the same host emulation for a resident-kernel entry (kVariants[shape]).
+int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double* u,
+                                double* f_emul, double* f_direct) {
+  if (!d || !u || !f_emul || !f_direct || shape < 0 || shape >= kNumVariants) return FIBRA_E_ARG;
+  const PackedNet P = pack(*d);
+  const Variant& v = kVariants[shape];
+  DeviceEntry de;
+  if (!build_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.FPT, v.NPT, de.sched))
+    return FIBRA_E_CONFIG;
+  Arena A;
+  Caps K;
+  build_resident_entry(de, P, *d, v, A, K);
+  for (auto& f : A.fixes) {
+    const void* addr = A.host.data() + f.second;
+    std::memcpy(f.first, &addr, sizeof addr);
+  }
+  const EntryDev& E = de.dev;
+  const int TS = E.thread_slots, FS = E.fiber_slots, gshift = v.FPT >= 4 ? 3 : 0;
+  std::vector<double> X(3 * static_cast<size_t>(TS + 2), 0.0), G(3 * static_cast<size_t>(E.gd_slots), 0.0);
+  X[3 * TS + 3] = 1.0;
+  auto x_of = [&](int pn, int c) { return P.ref[3 * pn + c] + u[3 * pn + c]; };
+  for (int sl = 0; sl < TS; ++sl)
+    if (E.slot_pn[sl] >= 0)
+      for (int c = 0; c < 3; ++c) X[3 * sl + c] = x_of(E.slot_pn[sl], c);
+  std::vector<int> written(E.gd_slots, 0);
+  for (int fs = 0; fs < FS; ++fs) {
+    const int ta = (E.fib_ab[fs] & 0xffff) / 8, hb = (static_cast<unsigned>(E.fib_ab[fs]) >> 16) / 8;
+    double dx[3], dd = 0;
+    for (int c = 0; c < 3; ++c) {
+      dx[c] = X[hb + c] - X[ta + c];
+      dd += dx[c] * dx[c];
+    }
+    const double L = std::sqrt(dd), l0 = E.fib_l0[fs];
+    const double g = E.fib_ea[fs] * (L - l0) / (l0 * L);
+    const int gt = ((E.fib_g[fs] & 0xffff) << gshift) / 8;
+    const int gh = ((static_cast<unsigned>(E.fib_g[fs]) >> 16) << gshift) / 8;
+    if (E.fib_id[fs] >= 0) {
+      if (written[gt / 3]++ || written[gh / 3]++) return 200;  // two fibers on one record
+    }
+    for (int c = 0; c < 3; ++c) {
+      G[gt + c] = -(g * dx[c]);
+      G[gh + c] = g * dx[c];
+    }
+  }
+  for (int c = 0; c < 3; ++c) G[3 * (E.gd_slots - 1) + c] = 0.0;
+  for (int i = 0; i < 3 * P.N; ++i) f_emul[i] = f_direct[i] = 0.0;
+  for (int sl = 0; sl < TS; ++sl) {
+    const int pn = E.slot_pn[sl];
+    if (pn < 0) continue;
+    for (int i = 0; i < 2 * E.csr_npairs[sl]; ++i) {
+      const int e = reinterpret_cast<const int*>(E.csr_pairs)[2 * ((i / 2) * TS + sl) + (i % 2)];
+      for (int c = 0; c < 3; ++c) f_emul[3 * pn + c] += G[e / 8 + c];
+    }
+  }
+  for (int f = 0; f < P.M; ++f) {
+    double dx[3], dd = 0;
+    for (int c = 0; c < 3; ++c) {
+      dx[c] = x_of(P.b[f], c) - x_of(P.a[f], c);
+      dd += dx[c] * dx[c];
+    }
+    const double L = std::sqrt(dd);
+    const double g = P.ea[f] * (L - P.l0[f]) / (P.l0[f] * L);
+    for (int c = 0; c < 3; ++c) {
+      f_direct[3 * P.b[f] + c] += g * dx[c];
+      f_direct[3 * P.a[f] + c] -= g * dx[c];
+    }
+  }
   return FIBRA_OK;
 }
 

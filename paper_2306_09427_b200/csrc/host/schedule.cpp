@@ -141,13 +141,13 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
       if (bank(b_pn[f]) != bank(a_pn[f])) inc[bank(b_pn[f])].push_back(i);
     }
     std::vector<char> done(members.size(), 0);
-    auto orient_from = [&](int r0) {
+    auto orient_from = [&](int r0) {  // one walk; false if r0 had no edge left
       int r = r0;
-      for (;;) {
+      for (bool first = true;; first = false) {
         int e = -1;
         for (int i : inc[r])
           if (!done[i]) { e = i; break; }
-        if (e < 0) return;
+        if (e < 0) return !first;
         done[e] = 1;
         const int f = members[e];
         const int ra = bank(a_pn[f]);
@@ -159,11 +159,15 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
     };
     for (int r = 0; r < kBanks; ++r)
       if (inc[r].size() == 1) orient_from(r);  // path ends first
-    for (int r = 0; r < kBanks; ++r) orient_from(r);  // then cycles (and any conflicts)
+    // then cycles; a conflicting group (bank degree > 2) needs repeated walks per bank
+    for (int r = 0; r < kBanks; ++r)
+      while (orient_from(r)) {
+      }
     std::array<int, kBanks> tails{}, heads{};
     bool conflict = false;
     for (int i = 0; i < static_cast<int>(members.size()); ++i) {
       const int f = members[i];
+      if (s.tail_pn[f] < 0) return false;  // (every member is oriented above)
       conflict |= tails[bank(s.tail_pn[f])]++ > 0;
       conflict |= heads[bank(s.head_pn[f])]++ > 0;
       s.fiber_of_fslot[kBanks * g + i] = f;

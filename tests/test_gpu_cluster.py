@@ -200,3 +200,25 @@ def test_cluster_lattice_converged(oracle_lib):
     resp, status, ost = oracle_batch([on], [0, 0], F, tangent=True)
     check_records(br, resp, status, tangent=True)
     check_states(st, ost)
+
+
+def config3_pair(p):
+    from paper_2306_09427_b200 import synth
+    pn = synth.config3_network(p)
+    on = O.Network(pn.coords, pn.fiber_nodes[:, 0], pn.fiber_nodes[:, 1], pn.fiber_area,
+                   pn.fiber_modulus, pn.box_half)
+    return pn, on, synth.batch_F(p + 1)[p:p + 1]
+
+
+@pytest.mark.parametrize("p,force", [(27, None), (1439, 2), (280, 2)])
+def test_config3_regressions(oracle_lib, p, force):
+    """Config-3 points that once differed: p=27 fills every fiber slot of the (512, 4, 1)
+    shape (its schedule has conflicting fiber groups), p=1439/280 on a mirror-mode 2-CTA
+    cluster (real fibers whose tail is a halo node)."""
+    pn, on, F = config3_pair(p)
+    br, st, shapes = run([pn], [0], F, tangent=False, force_cluster=force)
+    if force:
+        assert shapes[0]["cluster"] == force
+    resp, status, ost = oracle_batch([on], [0], F, tangent=False)
+    check_records(br, resp, status, tangent=False)
+    check_states(st, ost, points=[p_ for p_ in range(1) if not status[p_]])

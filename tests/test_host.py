@@ -197,3 +197,17 @@ def test_cuda_path_fails_loudly_without_gpu():
     with pytest.raises(P.Error):
         P.batch_response(lib, asg, st, P.FiberLaw(), np.eye(3)[None], P.RelaxConfig(),
                          P.StiffnessConfig())
+
+
+@pytest.mark.parametrize("p", [27, 280, 1439, 3001])
+def test_uploaded_entries_assemble_forces(p):
+    """One force pass emulated on the host from the arrays the upload builds (resident and
+    cluster entries, mirror and copy modes) equals direct assembly bit for bit
+    (fibra_debug_*_forces; tools/emulate_forces.py sweeps config 3)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from emulate_forces import check
+    from paper_2306_09427_b200 import synth
+    net = synth.config3_network(p)
+    u = np.random.default_rng(p).normal(0, 0.01, net.packed_ref_coords.size)
+    assert check(net, u) == []
