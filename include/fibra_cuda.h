@@ -109,6 +109,9 @@ int fibra_debug_cluster_forces(const fibra_net_desc* net, int C, int shape, int 
                                const double* u, double* f_emul, double* f_direct);
 int fibra_debug_resident_forces(const fibra_net_desc* net, int shape, const double* u,
                                 double* f_emul, double* f_direct);
+/* Diagnostics (no CUDA): out[4] = {plan found, mirror mode, dynamic shared bytes, static
+ * control-block bytes} of the cluster plan of `net` on C CTAs of cluster shape `shape`. */
+int fibra_debug_cluster_smem(const fibra_net_desc* net, int C, int shape, int64_t* out);
 
 /* ---- solver configuration records ------------------------------------------------- */
 typedef struct {          /* FiberLaw network.hpp:27-38                              */

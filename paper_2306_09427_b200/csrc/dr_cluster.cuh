@@ -75,8 +75,8 @@ struct __align__(16) ClusterCtl {
   int flag, dec, skip, pad0;  // skip: last pass whose exact verdict said "continue"
   int collapse[2], pad1[2];   // [pass & 1]: a fiber of that pass collapsed somewhere
   double ck_t[2], ck_dt[2];
-  double warp_min[32];
   double ex[12];
+  double se, mom[9];          // exit: strain energy and boundary moment sums (rank 0)
   double t, force_floor;
   double part[2][16][2];       // [pass & 1][rank] partial |f|^2 (free, fixed)
   double wmin[16 * 16];        // [rank * NW + warp] CFL minima of every warp of the cluster
@@ -117,6 +117,31 @@ __device__ __forceinline__ void cl_st_f64(unsigned a, double v) {
 __device__ __forceinline__ void cl_st_s32(unsigned a, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// Reference-order sequential sum of src[start + stride*i], i = 0..count-1 (squared terms for
+// SQ: `acc += v * v`, kernels_scalar.cpp), by one warp: lanes load 32 consecutive terms (the
+// next 32 in flight), then every lane folds them in order through shuffles -- the same
+// additions in the same order as one thread's loop, without its serial L2 round trips.
+template <bool SQ>
+__device__ __forceinline__ double fold_chain(const double* src, int start, int stride, int count,
+                                             int lane) {
+  double acc = 0.0;
+  double v = lane < count ? __ldcg(src + start + stride * lane) : 0.0;
+  for (int c0 = 0; c0 < count; c0 += 32) {
+    const int nx = c0 + 32 + lane;
+    const double vn = nx < count ? __ldcg(src + start + stride * nx) : 0.0;
+    const double t = SQ ? v * v : v;
+    const int n = count - c0;
+    if (n >= 32) {
+#pragma unroll
+      for (int s = 0; s < 32; ++s) acc = acc + __shfl_sync(0xffffffffu, t, s);
+    } else {
+      for (int s = 0; s < n; ++s) acc = acc + __shfl_sync(0xffffffffu, t, s);
+    }
+    v = vn;
+  }
+  return acc;
+}
+
 // min over the n cluster-wide warp slots, evaluated by one warp (every lane gets it)
 __device__ __forceinline__ double slots_min(const double* w, int n, int lane) {
   double m = INFINITY;
@@ -133,6 +158,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   __shared__ ClusterCtl ctl;
   const DrParams& P = CP.d;
   constexpr int NW = T / 32;
+  static_assert(NW <= 16, "ClusterCtl::wmin holds 16 warps per CTA");
   constexpr int TS = NPT * T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -542,15 +568,11 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         }
         __threadfence();
         cl_sync();
-        if (tid < 8) {
-          const int base = tid < 4 ? 0 : 3 * NFN;
-          const int len = tid < 4 ? 3 * NFN : 3 * NFIX;
-          double acc = 0;
-          for (int i = tid & 3; i < len; i += 4) {
-            const double v = __ldcg(SF + base + i);
-            acc += v * v;
-          }
-          ctl.ex[tid] = acc;
+        if (warp < 8) {  // norm2_sq partials (4 free, 4 fixed), one warp per chain
+          const int r = warp & 3, base = warp < 4 ? 0 : 3 * NFN;
+          const int len = warp < 4 ? 3 * NFN : 3 * NFIX;
+          const double acc = fold_chain<true>(SF + base, r, 4, len > r ? (len - r + 3) / 4 : 0, lane);
+          if (lane == 0) ctl.ex[warp] = acc;
         }
         __syncthreads();
         const double res = sqrt((ctl.ex[0] + ctl.ex[1]) + (ctl.ex[2] + ctl.ex[3]));
@@ -673,19 +695,42 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
     __threadfence();
     cl_sync();
     if (rank == 0) {
-      if (status == FIBRA_OK && tid < 12) {  // reference-order reductions (4 partials)
-        const int r = tid & 3, which = tid >> 2;
-        const double* src = which == 0 ? SF : (which == 1 ? SF + 3 * NFN : SW);
-        const int len = which == 1 ? 3 * NFIX : 3 * NFN;
-        double acc = 0;
-        if (which < 2)
-          for (int i = r; i < len; i += 4) {
-            const double v = __ldcg(src + i);
-            acc += v * v;
+      if (status == FIBRA_OK) {  // reference-order reductions (4 partials), one warp each
+        if (warp < 12) {
+          const int r = warp & 3, which = warp >> 2;
+          const double* src = which == 0 ? SF : (which == 1 ? SF + 3 * NFN : SW);
+          const int len = which == 1 ? 3 * NFIX : 3 * NFN;
+          const int cnt = len > r ? (len - r + 3) / 4 : 0;
+          const double acc = which < 2 ? fold_chain<true>(src, r, 4, cnt, lane)
+                                       : fold_chain<false>(src, r, 4, cnt, lane);
+          if (lane == 0) ctl.ex[warp] = acc;
+        }
+        if (warp == NW - 1 && !zero_iter) {  // strain_energy: one chain over the fibers
+          const double se = fold_chain<false>(SE, 0, 1, M, lane);
+          if (lane == 0) ctl.se = se;
+        }
+        if (warp == NW - 2 && conv) {  // homogenized_stress moments, boundary nodes ascending
+          double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+          for (int c0 = NFN; c0 < N; c0 += 32) {
+            const int pn = c0 + lane;
+            double rr[3] = {0, 0, 0}, xx[3] = {0, 0, 0};
+            if (pn < N)
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                rr[c] = __ldcg(SF + 3 * pn + c);
+                xx[c] = __ldcg(SX + 3 * pn + c);
+              }
+            double pr[9];
+#pragma unroll
+            for (int i = 0; i < 9; ++i) pr[i] = rr[i / 3] * xx[i % 3];
+            const int n = min(32, N - c0);
+            for (int s2 = 0; s2 < n; ++s2)
+#pragma unroll
+              for (int i = 0; i < 9; ++i) sm[i] = sm[i] + __shfl_sync(0xffffffffu, pr[i], s2);
           }
-        else
-          for (int i = r; i < len; i += 4) acc += __ldcg(src + i);
-        ctl.ex[tid] = acc;
+          if (lane == 0)
+            for (int i = 0; i < 9; ++i) ctl.mom[i] = sm[i];
+        }
       }
       __syncthreads();
       if (tid == 0) {
@@ -701,22 +746,11 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
           o.converged = conv;
           if (!zero_iter) {
             const double ke = 0.5 * ((ctl.ex[8] + ctl.ex[9]) + (ctl.ex[10] + ctl.ex[11]));
-            double se = 0;
-            for (int f = 0; f < M; ++f) se += __ldcg(SE + f);
+            const double se = ctl.se;
             o.kinetic_fraction = (ke + se) > 0 ? ke / (ke + se) : 0.0;
           }
           if (conv) {  // homogenized_stress moment sums, boundary nodes ascending
-            double sm[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-            for (int pn = NFN; pn < N; ++pn) {
-              const double r0 = __ldcg(SF + 3 * pn), r1 = __ldcg(SF + 3 * pn + 1);
-              const double r2 = __ldcg(SF + 3 * pn + 2);
-              const double x0 = __ldcg(SX + 3 * pn), x1 = __ldcg(SX + 3 * pn + 1);
-              const double x2 = __ldcg(SX + 3 * pn + 2);
-              sm[0] += r0 * x0; sm[1] += r0 * x1; sm[2] += r0 * x2;
-              sm[3] += r1 * x0; sm[4] += r1 * x1; sm[5] += r1 * x2;
-              sm[6] += r2 * x0; sm[7] += r2 * x1; sm[8] += r2 * x2;
-            }
-            for (int i = 0; i < 9; ++i) o.moment[i] = sm[i];
+            for (int i = 0; i < 9; ++i) o.moment[i] = ctl.mom[i];
             o.box_volume = E.box_volume;
           } else {
             o.status = is_base ? FIBRA_E_NOT_CONVERGED : FIBRA_E_PROBE_FAILED;

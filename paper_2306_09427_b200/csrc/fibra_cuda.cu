@@ -765,6 +765,25 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
   return smem <= static_cast<size_t>(c->max_smem);
 }
 
+// the cluster kernel's static control block beyond the common 4 KB reserve
+// (the kernel's only static shared memory)
+constexpr int kClusterCtlExtra = sizeof(ClusterCtl) > 4096 ? static_cast<int>(sizeof(ClusterCtl)) - 4096 : 0;
+
+// Halo x banks: two (by pass parity) in mirror mode, whose fiber -> node handoff is a CTA
+// barrier; one otherwise.  A class's bank stride is 24 x its largest mirror-mode halo
+// (Caps::max_halo), and every mirror entry's x region holds two banks of that entry's halo,
+// so the class's x region (the per-entry maximum) holds both banks of every mirror entry.
+int halo_banks(const ClusterPlan& plan) { return plan.mirror ? 2 : 1; }
+
+size_t cluster_smem(const ClusterPlan& plan, const ClusterVariant& v, int max_pairs) {
+  const int TS = v.NPT * v.T;
+  size_t max_h = 0;
+  for (const ClusterPart& q : plan.parts) max_h = std::max(max_h, q.h_fiber.size());
+  return align16(24ull * (TS + 2 + halo_banks(plan) * plan.max_halo)) +
+         align16(24ull * (v.FPT * (v.T - 32) + max_h + 1)) + 8ull * TS +
+         8ull * max_pairs * TS + 4ull * plan.max_push * TS;
+}
+
 bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& v, int C,
                   int max_pairs, ClusterPlan& plan) {
   // mirror mode first (one cluster barrier per iteration), else copies of remote records
@@ -778,12 +797,7 @@ bool cluster_fits(const fibra_ctx* c, const PackedNet& P, const ClusterVariant& 
     return false;
   const int TS = v.NPT * v.T;
   if (24 * (TS + 2 + plan.max_halo) >= 65536) return false;  // 16-bit x offsets
-  size_t max_h = 0;
-  for (const ClusterPart& q : plan.parts) max_h = std::max(max_h, q.h_fiber.size());
-  const size_t smem = align16(24ull * (TS + 2 + 2 * plan.max_halo)) +
-                      align16(24ull * (v.FPT * (v.T - 32) + max_h + 1)) + 8ull * TS +
-                      8ull * max_pairs * TS + 4ull * plan.max_push * TS;
-  return smem <= static_cast<size_t>(c->max_smem);
+  return cluster_smem(plan, v, max_pairs) <= static_cast<size_t>(c->max_smem - kClusterCtlExtra);
 }
 
 // Host image of one library entry's device arrays: built without CUDA calls (so entries
@@ -1068,8 +1082,8 @@ void build_cluster_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_de
   E.mirror = plan.mirror ? 1 : 0;
   parts_off = A.reserve(sizeof(PartDev) * C);  // filled at commit, once pointers are known
   K.ts = TS;
-  K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + 2 * plan.max_halo)));
-  K.max_halo = plan.max_halo;
+  K.x_bytes = static_cast<int>(align16(24ull * (TS + 2 + halo_banks(plan) * plan.max_halo)));
+  K.max_halo = plan.mirror ? plan.max_halo : 0;
   K.g_bytes = static_cast<int>(align16(24ull * max_rec));
   K.csr_cap = max_pairs_all * TS;
   K.push_cap = max_push_all * TS;
@@ -1121,7 +1135,7 @@ int fibra_cuda_open(int device, fibra_ctx** out) {
   if (cudaMalloc(&c->d_ticket, 2 * kMaxClasses * sizeof(int)) != cudaSuccess) return bail(FIBRA_E_CUDA);
   if (cudaDeviceGetAttribute(&c->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
-  c->max_smem -= 4096;  // the kernels' static control blocks (ClusterCtl ~3 KB)
+  c->max_smem -= 4096;  // the kernels' static control blocks (+ kClusterCtlExtra for ClusterCtl)
   if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
     return bail(FIBRA_E_CUDA);
   if (cudaMalloc(&c->d_counters, 5 * sizeof(unsigned long long)) != cudaSuccess)
@@ -1229,8 +1243,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             size_t max_h = 0;
             for (const ClusterPart& q : plans[i].parts) max_h = std::max(max_h, q.h_fiber.size());
             est[i].ts = TS;
-            est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2 + 2 * plans[i].max_halo)));
-            est[i].max_halo = plans[i].max_halo;
+            est[i].x_bytes = static_cast<int>(
+                align16(24ull * (TS + 2 + halo_banks(plans[i]) * plans[i].max_halo)));
+            est[i].max_halo = plans[i].mirror ? plans[i].max_halo : 0;
             est[i].g_bytes = static_cast<int>(align16(24ull * (cv.FPT * (cv.T - 32) + max_h + 1)));
             est[i].csr_cap = mp * TS;
             est[i].push_cap = plans[i].max_push * TS;
@@ -1249,7 +1264,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     auto fits_with = [&](const KClass& K) {
       KClass T = K;
       merge_caps(T, est[i]);
-      return T.smem() <= static_cast<size_t>(c->max_smem);
+      return T.smem() <= static_cast<size_t>(c->max_smem - (cl ? kClusterCtlExtra : 0));
     };
     int k = 0;
     const int nk = static_cast<int>(c->classes.size());
@@ -1308,7 +1323,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     FB_CUDA(c, cudaMemcpy(c->d_orient, host.data(), sizeof(OrientDev) * n, cudaMemcpyHostToDevice));
   }
   for (KClass& K : c->classes) {
-    if (K.smem() > static_cast<size_t>(c->max_smem))
+    if (K.smem() > static_cast<size_t>(c->max_smem - (K.cluster ? kClusterCtlExtra : 0)))
       return set_err(c, FIBRA_E_ARG, "library shared-memory footprint exceeds the device limit");
     if (K.cluster) {
       std::vector<ClusterEntryDev> host(n, ClusterEntryDev{});
@@ -1750,6 +1765,24 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
       f_direct[3 * P.a[f] + c] -= g * dx[c];
     }
   }
+  return FIBRA_OK;
+}
+
+// Diagnostics (no CUDA): the cluster plan's dynamic shared-memory footprint for shape `shape`
+// on C CTAs.  out[4] = {plan found, mirror mode, dynamic bytes, static ClusterCtl bytes}.
+int fibra_debug_cluster_smem(const fibra_net_desc* d, int C, int shape, int64_t* out) {
+  if (!d || !out || shape < 0 || shape >= kNumClusterVariants) return FIBRA_E_ARG;
+  const PackedNet P = pack(*d);
+  const ClusterVariant& v = kClusterVariants[shape];
+  ClusterPlan plan;
+  const bool ok = build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T,
+                                     v.FPT, v.NPT, true, plan) ||
+                  build_cluster_plan(P.N, P.NFN, P.M, P.a.data(), P.b.data(), P.ref.data(), C, v.T,
+                                     v.FPT, v.NPT, false, plan);
+  out[0] = ok;
+  out[1] = ok && plan.mirror;
+  out[2] = ok ? static_cast<int64_t>(cluster_smem(plan, v, max_pairs_of(P))) : 0;
+  out[3] = static_cast<int64_t>(sizeof(ClusterCtl));
   return FIBRA_OK;
 }
 

@@ -211,3 +211,16 @@ def test_uploaded_entries_assemble_forces(p):
     net = synth.config3_network(p)
     u = np.random.default_rng(p).normal(0, 0.01, net.packed_ref_coords.size)
     assert check(net, u) == []
+
+
+def test_config4_lattices_fit_16_cta_clusters():
+    """Every config-4 lattice (50k fibers) fits the (512, 7, 2) cluster shape on 16 CTAs within
+    B200's 227 KB opt-in shared memory less the kernels' 4 KB static reserve
+    (fibra_debug_cluster_smem mirrors upload_library's footprint)."""
+    from paper_2306_09427_b200 import synth
+    for i in range(0, 64, 3):
+        out = np.zeros(4, np.int64)
+        net = synth.config4_network(i)  # (the descriptor points into its arrays)
+        _capi.load().fibra_debug_cluster_smem(net.desc(), 16, 2, out.ctypes.data_as(_capi._lp))
+        assert out[0] == 1 and out[3] <= 4096, (i, out)
+        assert out[2] <= 232448 - 4096, (i, out)
