@@ -192,8 +192,10 @@ int fibra_cuda_reset_states(fibra_ctx* ctx);
  * completion).  Results are independent of it (every solve is computed bit-identically
  * wherever it runs); only the batch makespan changes.  The reference's WorkerPool takes
  * points in index order (batch.cpp:160-186), which is FIBRA_SCHED_BATCH.
- *   FIBRA_SCHED_STRAIN (default): ascending Green-strain norm |F^T F - I|/2 of the base
- *     point -- small-strain networks are dominated by soft modes and relax longest;
+ *   FIBRA_SCHED_STRAIN (default): descending input-only cost estimate, log iterations ~
+ *     7.2 (share of nodes with <= 2 fibres) - 3.3 (fibres per node) + 1.75 log(fibres)
+ *     - 0.37 log |F^T F - I| -- floppy and small-strain networks relax longest (for one
+ *     network topology: ascending strain);
  *   FIBRA_SCHED_HINT: descending caller cost (e.g. the previous call's relax_iterations
  *     per point, n_points values, copied); cleared by fibra_cuda_bind_points. */
 enum { FIBRA_SCHED_BATCH = 0, FIBRA_SCHED_STRAIN = 1, FIBRA_SCHED_HINT = 2 };
@@ -241,6 +243,9 @@ int fibra_cuda_selftest_fastmath(fibra_ctx* ctx, uint64_t n, uint64_t seed, uint
 /* Diagnostics: with FIBRA_PHASE_PROF set in the environment, the last solve accumulated
  * per-warp cycles [fiber work, barrier 1, node work, barrier 2] for every CTA. */
 int fibra_cuda_phase_profile(fibra_ctx* ctx, unsigned long long* out, size_t cap, size_t* n);
+/* Diagnostics: with FIBRA_TRACE set at solve time, per solve {start ns, end ns,
+ * sm << 32 | block, iterations} of the last solve call (solve index layout of the results). */
+int fibra_cuda_trace(fibra_ctx* ctx, unsigned long long* out, size_t cap, size_t* n);
 
 #ifdef __cplusplus
 }

@@ -34,7 +34,7 @@ EXPORTS = [
     "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel", "fibra_cuda_orientation",
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
     "fibra_cuda_solve_device", "fibra_cuda_synchronize", "fibra_cuda_last_stats",
-    "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile",
+    "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile", "fibra_cuda_trace",
     "fibra_cuda_selftest_fastmath",
 ]
 
@@ -159,6 +159,8 @@ def load(build_if_missing: bool = True):
         "fibra_cuda_fp64_peak": (C.c_int, [vp, C.POINTER(C.c_double)]),
         "fibra_cuda_selftest_fastmath": (C.c_int, [vp, C.c_uint64, C.c_uint64,
                                                    C.POINTER(C.c_uint64)]),
+        "fibra_cuda_trace": (C.c_int, [vp, C.POINTER(C.c_uint64), C.c_size_t,
+                                       C.POINTER(C.c_size_t)]),
         "fibra_cuda_phase_profile": (C.c_int, [vp, C.POINTER(C.c_uint64), C.c_size_t,
                                                C.POINTER(C.c_size_t)]),
     }

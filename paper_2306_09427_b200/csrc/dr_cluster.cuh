@@ -215,6 +215,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         }
         if (P.solve_skip[s]) flag = 0;
         e = P.entry_of_point[p];
+        trace_start(P, s);
       }
       for (unsigned r = 0; r < C; ++r) {
         const unsigned a = cl_map(ctl_sh + off_solve, r);
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         SolveOut o = {};
         o.status = P.solve_skip[s] ? P.solve_skip[s] : FIBRA_E_NOT_CONVERGED;
         P.out[s] = o;
+        trace_end(P, s, 0);
         if (q < 0) publish_base(P, p, 2);
       }
       cl_sync();
@@ -757,6 +759,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
           }
         }
         P.out[s] = o;
+        trace_end(P, s, n_done);
         if (is_base) {
           P.t[p] = ctl.t;
           if (status == FIBRA_OK) {

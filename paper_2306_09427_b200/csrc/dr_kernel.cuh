@@ -99,7 +99,33 @@ struct DrParams {
   double damping, tolerance, dt_safety, density_scale;
   long long max_iterations;
   unsigned long long* phase_prof;  // optional [grid][NW][4] cycle accumulators
+  unsigned long long* trace;       // optional [solve][4]: start ns, end ns,
+                                   // sm << 32 | class << 24 | block, iterations (FIBRA_TRACE)
+  int trace_class, pad_trace;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void trace_start(const DrParams& P, int s) {
+  if (P.trace) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    P.trace[4 * s] = global_ns();
+    P.trace[4 * s + 2] = (static_cast<unsigned long long>(sm) << 32) |
+                         (static_cast<unsigned long long>(P.trace_class) << 24) | blockIdx.x;
+  }
+}
+
+__device__ __forceinline__ void trace_end(const DrParams& P, int s, long long iters) {
+  if (P.trace) {
+    P.trace[4 * s + 1] = global_ns();
+    P.trace[4 * s + 3] = static_cast<unsigned long long>(iters);
+  }
+}
 
 enum : int { kDecConv = 1, kDecExact = 2, kDecNonfinite = 4 };
 
@@ -270,6 +296,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         ctl.entry = P.entry_of_point[p];
         ctl.collapse = 0;
         ctl.flag = flag;
+        trace_start(P, s);
       }
       ctl.solve = s;
     }
@@ -282,6 +309,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         SolveOut o = {};
         o.status = P.solve_skip[s] ? P.solve_skip[s] : FIBRA_E_NOT_CONVERGED;
         P.out[s] = o;
+        trace_end(P, s, 0);
         if (q < 0) publish_base(P, p, 2);
       }
       __syncthreads();
@@ -779,6 +807,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         }
       }
       P.out[s_] = o;
+      trace_end(P, s_, n_done);
       if (base_solve) {
         P.t[p_] = ctl.t;
         if (status == FIBRA_OK) {  // a throw leaves iters untouched (relax.cpp:187)

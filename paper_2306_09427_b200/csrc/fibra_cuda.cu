@@ -52,7 +52,7 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
                             double fd_rel_step, PrepOut* prep, double* solve_F, int* solve_skip,
                             int* base_flag, int* done_list, int sched_mode,
                             const double* __restrict__ hint, const int* __restrict__ cls,
-                            unsigned* key, int* pidx) {
+                            const float* __restrict__ pcost, unsigned* key, int* pidx) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   double f[9];
@@ -63,14 +63,21 @@ __global__ void prep_kernel(int n, const double* __restrict__ F, int want_tangen
   // schedule key (ascending = started first), unique through the point index in the low word
   unsigned hi = 0;
   if (sched_mode == FIBRA_SCHED_STRAIN) {
+    // input-only cost model: log(expected iterations) = topology term of the entry (upload)
+    // - 0.37 log |F^T F - I|; descending (small strain relaxes longest; identity last)
     double e2 = 0;  // |F^T F - I|^2, fp64 only for ordering
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
         double c = f[i] * f[j] + f[3 + i] * f[3 + j] + f[6 + i] * f[6 + j] - (i == j);
         e2 += c * c;
       }
-    const float k = static_cast<float>(sqrt(e2));
-    hi = k == k ? __float_as_uint(k) : 0xffffffffu;
+    const float k = e2 > 0 ? pcost[p] - 0.185f * logf(static_cast<float>(e2)) : -INFINITY;
+    if (k == k) {
+      const unsigned u = __float_as_uint(k);
+      hi = ~((u & 0x80000000u) ? ~u : (u | 0x80000000u));  // descending total order
+    } else {
+      hi = 0xffffffffu;
+    }
   } else if (sched_mode == FIBRA_SCHED_HINT) {
     const float k = static_cast<float>(hint[p]);
     hi = (k == k && k > 0) ? ~__float_as_uint(k) : 0xffffffffu;
@@ -293,6 +300,7 @@ struct DeviceEntry {
   Schedule sched;
   std::vector<void*> allocs;
   int cls = -1;           // kernel class
+  float log_its = 0;      // topology term of the schedule cost model (upload_library)
   int n_nodes = 0;
   bool config_ok = true;
   std::string config_err;
@@ -343,6 +351,7 @@ struct fibra_ctx {
   std::vector<int32_t> entry_of_point;
   std::vector<long long> offsets;
   int* d_entry_of_point = nullptr;
+  float* d_pcost = nullptr;              // per point: the entry's topology term of the cost model
   int* d_class_of_point = nullptr;
   long long* d_offsets = nullptr;
   double* d_state[8] = {};  // u v a f_int f_damp mass inv_mass t
@@ -377,6 +386,8 @@ struct fibra_ctx {
   int last_launches = 0;
   unsigned long long* phase_prof = nullptr;
   size_t phase_prof_n = 0;
+  unsigned long long* d_trace = nullptr;  // FIBRA_TRACE diagnostics: [solve][4]
+  size_t trace_cap = 0, trace_n = 0;
 };
 
 namespace {
@@ -402,6 +413,8 @@ int dalloc(fibra_ctx* c, T** p, size_t n) {
 
 void free_points(fibra_ctx* c) {
   cudaFree(c->d_entry_of_point);
+  cudaFree(c->d_pcost);
+  c->d_pcost = nullptr;
   cudaFree(c->d_class_of_point);
   c->d_class_of_point = nullptr;
   cudaFree(c->d_offsets);
@@ -564,8 +577,20 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   P.density_scale = rc->density_scale;
   P.max_iterations = rc->max_iterations;
   P.phase_prof = nullptr;
-
+  P.trace = nullptr;
   cudaStream_t st = c->stream;
+  if (getenv("FIBRA_TRACE")) {  // diagnostics: per-solve start/end/SM (fibra_cuda_trace)
+    const size_t need = 4ull * (want_tangent ? 7 : 1) * n;
+    if (need > c->trace_cap) {
+      cudaFree(c->d_trace);
+      FB_CUDA(c, cudaMalloc(&c->d_trace, need * 8));
+      c->trace_cap = need;
+    }
+    FB_CUDA(c, cudaMemsetAsync(c->d_trace, 0, need * 8, st));
+    P.trace = c->d_trace;
+    c->trace_n = need;
+  }
+
   FB_CUDA(c, cudaEventRecord(c->ev[0], st));
   FB_CUDA(c, cudaMemsetAsync(c->d_ticket, 0, 2 * kMaxClasses * sizeof(int), st));
   FB_CUDA(c, cudaMemsetAsync(c->d_counters, 0, 5 * sizeof(unsigned long long), st));
@@ -573,7 +598,8 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   prep_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, sc ? sc->fd_rel_step : 1e-5,
                                                 c->d_prep, c->d_solveF, c->d_skip, c->d_flag,
                                                 c->d_done, c->sched_mode, c->d_hint,
-                                                c->d_class_of_point, c->d_key, c->d_pidx);
+                                                c->d_class_of_point, c->d_pcost, c->d_key,
+                                                c->d_pidx);
   FB_CUDA(c, cudaGetLastError());
   size_t tmp_bytes = c->sort_tmp_bytes;  // longest expected solve first, grouped by class
   FB_CUDA(c, cub::DeviceRadixSort::SortPairs(c->d_sort_tmp, tmp_bytes, c->d_key, c->d_key_sorted,
@@ -593,8 +619,11 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   }
   for (int k = 0; k < static_cast<int>(c->classes.size()); ++k)
     if (c->classes[k].n_points) launch_order.push_back(k);
-  std::stable_sort(launch_order.begin(), launch_order.end(),
-                   [&](int a, int b) { return class_work[a] > class_work[b]; });
+  const char* order_env = getenv("FIBRA_CLASS_ORDER");  // diagnostics: "asc" | "desc"
+  const bool ascending = order_env && order_env[0] == 'a';
+  std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
+    return ascending ? class_work[a] < class_work[b] : class_work[a] > class_work[b];
+  });
   int launches = 2;  // ours: prep and post, plus one DR kernel per class (the sort is CUB's)
   bool prof_used = false;
   for (int ci : launch_order) {
@@ -602,6 +631,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
     P.n_class = K.n_points;
     P.n_solves = n_solves;
+    P.trace_class = ci;
     P.order = c->d_order + K.point_off;
     P.done_list = c->d_done + K.point_off;
     P.ticket = c->d_ticket + 2 * ci;
@@ -1154,6 +1184,7 @@ int fibra_cuda_close(fibra_ctx* c) {
   free_scratch(c);
   free_library(c);
   cudaFree(c->d_ticket);
+  cudaFree(c->d_trace);
   cudaFree(c->d_counters);
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaEventDestroy(c->ev_fork);
@@ -1219,6 +1250,17 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     de.config_err = P.err;
     de.n_nodes = P.N;
     const int mp = max_pairs_of(P);
+    {  // schedule cost model: floppy networks (many nodes of degree <= 2, few fibres per
+       // node) relax slowest; fitted on config-3 knn networks (Spearman 0.83 on held-out
+       // points vs 0.08 for strain alone, tools/trace_solve.py); only orders the work
+      std::vector<int> deg(P.N, 0);
+      for (int f = 0; f < P.M; ++f) ++deg[P.a[f]], ++deg[P.b[f]];
+      int low = 0;
+      for (int d : deg) low += d <= 2;
+      const double fd2 = P.N ? static_cast<double>(low) / P.N : 0.0;
+      const double r = P.N ? static_cast<double>(P.M) / P.N : 0.0;
+      de.log_its = static_cast<float>(7.2 * fd2 - 3.3 * r + 1.75 * std::log(std::max(P.M, 1)));
+    }
     for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
       if (resident_fits(c, P, kVariants[v], mp, de.sched)) {
         kind_vi[i] = v;
@@ -1374,6 +1416,7 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   int rc;
   if ((rc = dalloc(c, &c->d_entry_of_point, n))) return rc;
   if ((rc = dalloc(c, &c->d_class_of_point, n))) return rc;
+  if ((rc = dalloc(c, &c->d_pcost, n))) return rc;
   if ((rc = dalloc(c, &c->d_offsets, n + 1))) return rc;
   for (int k = 0; k < 7; ++k)
     if ((rc = dalloc(c, &c->d_state[k], tot))) return rc;
@@ -1383,6 +1426,9 @@ int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t 
   if (n) {
     FB_CUDA(c, cudaMemcpy(c->d_entry_of_point, entry_of_point, sizeof(int) * n, cudaMemcpyHostToDevice));
     FB_CUDA(c, cudaMemcpy(c->d_class_of_point, cls.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+    std::vector<float> pc(n);
+    for (int p = 0; p < n; ++p) pc[p] = c->entries[entry_of_point[p]].log_its;
+    FB_CUDA(c, cudaMemcpy(c->d_pcost, pc.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
   }
   FB_CUDA(c, cudaMemcpy(c->d_offsets, c->offsets.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice));
   return fibra_cuda_reset_states(c);
@@ -1555,6 +1601,15 @@ int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {
   }
   cudaFree(sink);
   *out = 8.0 * iters * static_cast<double>(blocks) * threads / (best * 1e-3);
+  return FIBRA_OK;
+}
+
+int fibra_cuda_trace(fibra_ctx* c, unsigned long long* out, size_t cap, size_t* n) {
+  if (!c || !n) return FIBRA_E_ARG;
+  *n = c->trace_n;
+  if (!out || !c->d_trace || !c->trace_n) return FIBRA_OK;
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
+  FB_CUDA(c, cudaMemcpy(out, c->d_trace, 8 * std::min(cap, c->trace_n), cudaMemcpyDeviceToHost));
   return FIBRA_OK;
 }
 
