@@ -101,7 +101,9 @@ struct DrParams {
   unsigned long long* phase_prof;  // optional [grid][NW][4] cycle accumulators
   unsigned long long* trace;       // optional [solve][4]: start ns, end ns,
                                    // sm << 32 | class << 24 | block, iterations (FIBRA_TRACE)
-  int trace_class, pad_trace;
+  int trace_class;
+  int shared_queue;                // several launches share this class's ticket counter:
+                                   // every ticket comes from it (no first-wave dealing)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -270,7 +272,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     // counter.
     if (tid == 0) {
       int t;
-      if (first_ticket) {
+      if (P.shared_queue) {
+        t = atomicAdd(P.ticket, 1);
+      } else if (first_ticket) {
         const int b = static_cast<int>(blockIdx.x), m = P.first_wave_sms;
         t = (m > 0 && b >= m) ? 3 * m - 1 - b : b;
       } else {

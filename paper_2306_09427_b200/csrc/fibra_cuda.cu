@@ -319,9 +319,10 @@ struct KClass {
   EntryDev* d_entries = nullptr;          // [n_entries] (resident)
   ClusterEntryDev* d_centries = nullptr;  // [n_entries] (cluster)
   int n_points = 0, point_off = 0;        // bound points of the class, offset in the order
-  cudaStream_t stream = nullptr;
-  cudaEvent_t done = nullptr;
-  cudaEvent_t done_t = nullptr;  // timed copy of `done` (FIBRA_CLASS_TIMES diagnostics)
+  cudaStream_t stream = nullptr;   // head launch (several classes) or the class's only launch
+  cudaStream_t stream2 = nullptr;  // body launch
+  cudaEvent_t done = nullptr, done2 = nullptr;
+  cudaEvent_t done_t = nullptr;  // timed end of both (FIBRA_CLASS_TIMES diagnostics)
   double* d_ckpt = nullptr;
   size_t ckpt_cap = 0;
   double* d_scratch = nullptr;
@@ -472,7 +473,9 @@ void free_library(fibra_ctx* c) {
     cudaFree(k.d_ckpt);
     cudaFree(k.d_scratch);
     if (k.stream) cudaStreamDestroy(k.stream);
+    if (k.stream2) cudaStreamDestroy(k.stream2);
     if (k.done) cudaEventDestroy(k.done);
+    if (k.done2) cudaEventDestroy(k.done2);
     if (k.done_t) cudaEventDestroy(k.done_t);
   }
   c->classes.clear();
@@ -607,41 +610,48 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   FB_CUDA(c, cudaEventRecord(c->ev[1], st));
   FB_CUDA(c, cudaEventRecord(c->ev_fork, st));
 
-  // classes run concurrently, each as a full persistent grid; later launches take SMs as
-  // earlier ones drain, so the class with the most work (sum of fibres over its points)
-  // launches first -- LPT at the class level (config 3: 8.86 s vs 8.78 s resident-first,
-  // config 5: 5.54 s vs 5.73 s; static SM shares by estimated work lost badly)
+  // Classes run concurrently as persistent grids sharing the device.  One full grid per
+  // class, launched by descending work, runs the classes nearly back to back (a later
+  // launch gets SMs only as earlier grids drain), so each class's longest solves -- 500k
+  // iteration caps of 1-2 s -- start only when its turn comes (FIBRA_TRACE timelines,
+  // DESIGN.md "Scheduling the batch").  With several classes, each one first gets a "head"
+  // launch sized to its share of the estimated work (cost model: sum over its points of
+  // exp(log_its) x fibres), so every class's longest-expected solves start at once; then the
+  // "body" launches (the rest of each full grid, descending work) fill SMs as heads drain.
+  // All launches of a class draw from its one ticket queue.
   std::vector<int> launch_order;
-  std::vector<double> class_work(c->classes.size(), 0.0);
+  std::vector<double> class_work(c->classes.size(), 0.0), class_cost(c->classes.size(), 0.0);
   for (int p = 0; p < n; ++p) {
     const DeviceEntry& de = c->entries[c->entry_of_point[p]];
-    class_work[de.cls] += c->classes[de.cls].cluster ? de.cdev.n_fibers : de.dev.n_fibers;
+    const int m = c->classes[de.cls].cluster ? de.cdev.n_fibers : de.dev.n_fibers;
+    class_work[de.cls] += m;
+    class_cost[de.cls] += std::exp(static_cast<double>(de.log_its)) * m;
   }
+  double cost_total = 0;
   for (int k = 0; k < static_cast<int>(c->classes.size()); ++k)
-    if (c->classes[k].n_points) launch_order.push_back(k);
+    if (c->classes[k].n_points) {
+      launch_order.push_back(k);
+      cost_total += class_cost[k];
+    }
   const char* order_env = getenv("FIBRA_CLASS_ORDER");  // diagnostics: "asc" | "desc"
   const bool ascending = order_env && order_env[0] == 'a';
   std::stable_sort(launch_order.begin(), launch_order.end(), [&](int a, int b) {
     return ascending ? class_work[a] < class_work[b] : class_work[a] > class_work[b];
   });
-  int launches = 2;  // ours: prep and post, plus one DR kernel per class (the sort is CUB's)
+  const char* heads_env = getenv("FIBRA_CLASS_HEADS");  // diagnostics: "0" = one grid per class
+  const bool heads = launch_order.size() > 1 && !(heads_env && heads_env[0] == '0');
+  int launches = 2;  // ours: prep and post, plus the DR launches (the sort is CUB's)
   bool prof_used = false;
+  // per class: full grid (CTAs, or clusters), head size, kernel handles
+  struct Plan {
+    int full = 0, head = 0, per_unit = 1;
+  };
+  std::vector<Plan> plan(c->classes.size());
   for (int ci : launch_order) {
     KClass& K = c->classes[ci];
     const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
-    P.n_class = K.n_points;
-    P.n_solves = n_solves;
-    P.trace_class = ci;
-    P.order = c->d_order + K.point_off;
-    P.done_list = c->d_done + K.point_off;
-    P.ticket = c->d_ticket + 2 * ci;
-    P.x_bytes = K.x_bytes;
-    P.g_bytes = K.g_bytes;
-    P.part_slots = K.ts;
-    P.csr_cap = K.csr_cap;
-    P.ck_stride = K.ck_stride;
     const size_t smem = K.smem();
-    FB_CUDA(c, cudaStreamWaitEvent(K.stream, c->ev_fork, 0));
+    int cap = 0;  // co-resident CTAs (resident) or clusters (cluster) on the device
     if (!K.cluster) {
       const Variant& v = kVariants[K.vi];
       KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
@@ -650,25 +660,8 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       int per_sm = 0;
       FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.T, smem));
       if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "DR kernel does not fit on an SM");
-      const int grid = std::min(n_solves, per_sm * c->n_sm);
-      P.first_wave_sms = (per_sm == 2 && grid == 2 * c->n_sm) ? c->n_sm : 0;
-      if ((r = grow(c, &K.d_ckpt, K.ckpt_cap, static_cast<size_t>(grid) * 12 * K.ck_stride)))
-        return r;
-      P.entries = K.d_entries;
-      P.ckpt = K.d_ckpt;
-      P.phase_prof = nullptr;
-      if (getenv("FIBRA_PHASE_PROF") && !prof_used) {  // diagnostics: per-warp phase cycles
-        static unsigned long long* buf = nullptr;
-        static size_t cap = 0;
-        const size_t need = static_cast<size_t>(grid) * (v.T / 32) * 4;
-        if (need > cap) { cudaFree(buf); cudaMalloc(&buf, need * 8); cap = need; }
-        cudaMemsetAsync(buf, 0, need * 8, K.stream);
-        P.phase_prof = buf;
-        c->phase_prof = buf;
-        c->phase_prof_n = need;
-        prof_used = true;
-      }
-      fn<<<grid, v.T, smem, K.stream>>>(P);
+      cap = per_sm * c->n_sm;
+      plan[ci].per_unit = per_sm;
     } else {
       const ClusterVariant& v = kClusterVariants[K.vi];
       ClusterFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
@@ -685,27 +678,82 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       cfg.gridDim = dim3(K.C);
       cfg.blockDim = dim3(v.T);
       cfg.dynamicSmemBytes = smem;
-      cfg.stream = K.stream;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      int max_clusters = 0;
-      FB_CUDA(c, cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg));
-      if (max_clusters < 1)
+      FB_CUDA(c, cudaOccupancyMaxActiveClusters(&cap, fn, &cfg));
+      if (cap < 1)
         return set_err(c, FIBRA_E_ARG, "cluster DR kernel cannot be co-scheduled on this device");
-      const int nclu = std::min(n_solves, max_clusters);
-      cfg.gridDim = dim3(nclu * K.C);
-      if ((r = grow(c, &K.d_ckpt, K.ckpt_cap,
-                    static_cast<size_t>(nclu) * K.C * 12 * K.ck_stride)))
-        return r;
-      if ((r = grow(c, &K.d_scratch, K.scratch_cap, static_cast<size_t>(nclu) * K.scratch_stride)))
-        return r;
+    }
+    plan[ci].full = std::min(n_solves, cap);
+    if (heads) {
+      const double share = cost_total > 0 ? class_cost[ci] / cost_total : 1.0;
+      plan[ci].head = std::max(1, std::min(plan[ci].full, static_cast<int>(std::lround(cap * share))));
+    }
+  }
+  // launch `units` CTAs (resident) or clusters (cluster) of class ci on stream `sm`, using
+  // checkpoint / scratch slots from `slot0` on
+  auto launch = [&](int ci, int units, int slot0, cudaStream_t sm) -> int {
+    KClass& K = c->classes[ci];
+    const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
+    P.n_class = K.n_points;
+    P.n_solves = n_solves;
+    P.trace_class = ci;
+    P.shared_queue = heads ? 1 : 0;
+    P.order = c->d_order + K.point_off;
+    P.done_list = c->d_done + K.point_off;
+    P.ticket = c->d_ticket + 2 * ci;
+    P.x_bytes = K.x_bytes;
+    P.g_bytes = K.g_bytes;
+    P.part_slots = K.ts;
+    P.csr_cap = K.csr_cap;
+    P.ck_stride = K.ck_stride;
+    const size_t smem = K.smem();
+    if (!K.cluster) {
+      const Variant& v = kVariants[K.vi];
+      KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      // (several classes may share a kernel function: its shared-memory limit is set per launch)
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      P.first_wave_sms = (!heads && plan[ci].per_unit == 2 && units == 2 * c->n_sm) ? c->n_sm : 0;
+      P.entries = K.d_entries;
+      P.ckpt = K.d_ckpt + static_cast<size_t>(slot0) * 12 * K.ck_stride;
+      P.phase_prof = nullptr;
+      if (getenv("FIBRA_PHASE_PROF") && !prof_used) {  // diagnostics: per-warp phase cycles
+        static unsigned long long* buf = nullptr;
+        static size_t pcap = 0;
+        const size_t need = static_cast<size_t>(units) * (v.T / 32) * 4;
+        if (need > pcap) { cudaFree(buf); cudaMalloc(&buf, need * 8); pcap = need; }
+        cudaMemsetAsync(buf, 0, need * 8, sm);
+        P.phase_prof = buf;
+        c->phase_prof = buf;
+        c->phase_prof_n = need;
+        prof_used = true;
+      }
+      fn<<<units, v.T, smem, sm>>>(P);
+    } else {
+      const ClusterVariant& v = kClusterVariants[K.vi];
+      ClusterFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = K.C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(units * K.C);
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = sm;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
       ClusterParams CP;
       CP.d = P;
       CP.d.entries = nullptr;
-      CP.d.ckpt = K.d_ckpt;
+      CP.d.ckpt = K.d_ckpt + static_cast<size_t>(slot0) * K.C * 12 * K.ck_stride;
       CP.d.phase_prof = nullptr;
       CP.centries = K.d_centries;
-      CP.scratch = K.d_scratch;
+      CP.scratch = K.d_scratch + static_cast<size_t>(slot0) * K.scratch_stride;
       CP.scratch_stride = K.scratch_stride;
       CP.push_cap = K.push_cap;
       CP.halo_stride = 24 * K.max_halo;
@@ -714,10 +762,35 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       FB_CUDA(c, cudaLaunchKernelEx(&cfg, fn, CP));
     }
     FB_CUDA(c, cudaGetLastError());
-    FB_CUDA(c, cudaEventRecord(K.done, K.stream));
-    FB_CUDA(c, cudaEventRecord(K.done_t, K.stream));
-    FB_CUDA(c, cudaStreamWaitEvent(st, K.done, 0));
     ++launches;
+    return FIBRA_OK;
+  };
+  for (int ci : launch_order) {  // checkpoint / scratch slots for the class's full grid
+    KClass& K = c->classes[ci];
+    const size_t units = static_cast<size_t>(plan[ci].full);
+    if ((r = grow(c, &K.d_ckpt, K.ckpt_cap, units * (K.cluster ? K.C : 1) * 12 * K.ck_stride)))
+      return r;
+    if (K.cluster && (r = grow(c, &K.d_scratch, K.scratch_cap, units * K.scratch_stride))) return r;
+    FB_CUDA(c, cudaStreamWaitEvent(K.stream, c->ev_fork, 0));
+    FB_CUDA(c, cudaStreamWaitEvent(K.stream2, c->ev_fork, 0));
+  }
+  if (heads) {
+    std::vector<int> by_cost = launch_order;
+    std::stable_sort(by_cost.begin(), by_cost.end(),
+                     [&](int a, int b) { return class_cost[a] > class_cost[b]; });
+    for (int ci : by_cost)
+      if ((r = launch(ci, plan[ci].head, 0, c->classes[ci].stream))) return r;
+  }
+  for (int ci : launch_order) {
+    KClass& K = c->classes[ci];
+    const int head = heads ? plan[ci].head : 0;
+    if (plan[ci].full > head && (r = launch(ci, plan[ci].full - head, head, K.stream2))) return r;
+    FB_CUDA(c, cudaEventRecord(K.done, K.stream));
+    FB_CUDA(c, cudaEventRecord(K.done2, K.stream2));
+    FB_CUDA(c, cudaStreamWaitEvent(K.stream2, K.done, 0));
+    FB_CUDA(c, cudaEventRecord(K.done_t, K.stream2));
+    FB_CUDA(c, cudaStreamWaitEvent(st, K.done2, 0));
+    FB_CUDA(c, cudaStreamWaitEvent(st, K.done, 0));
   }
   FB_CUDA(c, cudaEventRecord(c->ev[2], st));
   post_kernel<<<(n + tb - 1) / tb, tb, 0, st>>>(n, dF, want_tangent, c->d_prep, c->d_out,
@@ -1382,7 +1455,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       FB_CUDA(c, cudaMemcpy(K.d_entries, host.data(), sizeof(EntryDev) * n, cudaMemcpyHostToDevice));
     }
     FB_CUDA(c, cudaStreamCreateWithFlags(&K.stream, cudaStreamNonBlocking));
+    FB_CUDA(c, cudaStreamCreateWithFlags(&K.stream2, cudaStreamNonBlocking));
     FB_CUDA(c, cudaEventCreateWithFlags(&K.done, cudaEventDisableTiming));
+    FB_CUDA(c, cudaEventCreateWithFlags(&K.done2, cudaEventDisableTiming));
     FB_CUDA(c, cudaEventCreate(&K.done_t));
   }
   return FIBRA_OK;
