@@ -222,3 +222,24 @@ def test_config3_regressions(oracle_lib, p, force):
     resp, status, ost = oracle_batch([on], [0], F, tangent=False)
     check_records(br, resp, status, tangent=False)
     check_states(st, ost, points=[p_ for p_ in range(1) if not status[p_]])
+
+
+def test_multiclass_head_launches_tangent(oracle_lib):
+    """Four config-3 networks in four kernel classes (two resident shapes, a large resident
+    shape, a 2-CTA cluster) with the tangent: the multi-class path launches a head and a body
+    grid per class on one ticket queue, and probes follow base completion across both
+    launches -- records and states bitwise."""
+    pairs = [config3_pair(p) for p in (1439, 27, 0, 5)]
+    pn, on = [q[0] for q in pairs], [q[1] for q in pairs]
+    eop = [0, 1, 2, 3, 3, 2, 1, 0]
+    F = batch_F(len(eop))
+    relax = P.RelaxConfig(tolerance=1e-4)
+    br, st, shapes = run(pn, eop, F, tangent=True, relax=relax)
+    kinds = {(s["cluster"], s["threads"], s["fibers_per_thread"]) for s in shapes}
+    assert len(kinds) == 4, shapes
+    resp, status, ost = oracle_batch(on, eop, F, tangent=True,
+                                     relax=O.RelaxConfig(tolerance=1e-4))
+    assert not any(status), status
+    assert sum(int(r["relax_iterations"]) for r in resp) > 5000
+    check_records(br, resp, status, tangent=True)
+    check_states(st, ost, points=[p for p in range(len(eop)) if not status[p]])
