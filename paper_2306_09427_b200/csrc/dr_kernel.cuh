@@ -252,13 +252,14 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
   // register-resident topology of the loaded entry
   int fab[FPT], fgo[FPT];
-  double fl0[FPT], fs[FPT], fmred[FPT];
+  double fl0[FPT], frl0[FPT], fs[FPT], fmred[FPT];  // frl0: rcp_refined(l0), loop invariant
   int npair[NPT];
-  double nref[NPT][3], ninv[NPT], ncm[NPT];
+  double ninv[NPT], ncm[NPT];  // (reference coordinates: NREF, read through L1 when used)
   int cur_entry = -1;
   bool first_ticket = true;
   double s_uni = 0;  // UEA: the common ea_scale*EA
 #define SJ(j) (UEA ? s_uni : fs[j])
+#define NREF(j, c) __ldg(E.slot_ref + 3 * ((j) * T + tid) + (c))
 
   for (;;) {
     // Tickets [0, nc) are the base solves of this kernel class in P.order; tickets
@@ -339,15 +340,13 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         fab[j] = E.fib_ab[f];
         fgo[j] = E.fib_g[f];
         fl0[j] = E.fib_l0[f];
+        frl0[j] = rcp_refined(fl0[j]);
         if (!UEA) fs[j] = P.ea_scale * E.fib_ea[f];
       }
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
         npair[j] = E.csr_npairs[sl];
-        nref[j][0] = E.slot_ref[3 * sl];
-        nref[j][1] = E.slot_ref[3 * sl + 1];
-        nref[j][2] = E.slot_ref[3 * sl + 2];
       }
     }
     // ---- per-solve setup (relax.cpp:95-145) ----
@@ -395,19 +394,19 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           for (int c = 0; c < 3; ++c) u[j][c] = 0.0;
         }
       } else {  // affine BC (network.cpp:254-269), Def3::apply tensor.cpp:58-62
-        const double X0 = nref[j][0], X1 = nref[j][1], X2 = nref[j][2];
+        const double X0 = NREF(j, 0), X1 = NREF(j, 1), X2 = NREF(j, 2);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double fx = Fm[3 * c] * X0 + Fm[3 * c + 1] * X1 + Fm[3 * c + 2] * X2;
-          u[j][c] = fx - nref[j][c];
+          u[j][c] = fx - NREF(j, c);
         }
       }
 #pragma unroll
       for (int c = 0; c < 3; ++c) vh[j][c] = 0.0;
       double* xr = sm_at<double>(X, 24 * sl);
-      xr[0] = nref[j][0] + u[j][0];
-      xr[1] = nref[j][1] + u[j][1];
-      xr[2] = nref[j][2] + u[j][2];
+      xr[0] = NREF(j, 0) + u[j][0];
+      xr[1] = NREF(j, 1) + u[j][1];
+      xr[2] = NREF(j, 2) + u[j][2];
       if (sl < F0) {  // checkpoint "resume at pass 0": u_0, v = 0
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -484,7 +483,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
             bool o1, o2, o3 = true;
             const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
             collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
-            const double stretch = div_fast(len, fl0[j], o2);
+            const double stretch = div_fast_rcp(len, fl0[j], frl0[j], o2);
             if (LAW == 0) {
               g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
             } else {
@@ -554,9 +553,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
               }
             }
             double* xr = sm_at<double>(X, 24 * sl);
-            xr[0] = nref[j][0] + u[j][0];
-            xr[1] = nref[j][1] + u[j][1];
-            xr[2] = nref[j][2] + u[j][2];
+            xr[0] = NREF(j, 0) + u[j][0];
+            xr[1] = NREF(j, 1) + u[j][1];
+            xr[2] = NREF(j, 2) + u[j][2];
           }
           if (tid == 0) {
             ctl.t = ctl.ck_t[b];
@@ -657,7 +656,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
                 acc = -(fk[j][c] + fd) * ninv[j];
                 vv = vh[j][c] + h_k * acc;             // relax.cpp:166
               }
-              SX[3 * pn + c] = nref[j][c] + u[j][c];
+              SX[3 * pn + c] = NREF(j, c) + u[j][c];
               if (sl < F0) SW[3 * pn + c] = m * (vv * vv);
               if (base_solve) {
                 const long long d = soff + 3 * pn + c;
@@ -702,9 +701,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
             vh[j][c] = vv + h_n * acc;                          // relax.cpp:155
             u[j][c] = u[j][c] + dt_next * vh[j][c];             // relax.cpp:156
           }
-          xr[0] = nref[j][0] + u[j][0];
-          xr[1] = nref[j][1] + u[j][1];
-          xr[2] = nref[j][2] + u[j][2];
+          xr[0] = NREF(j, 0) + u[j][0];
+          xr[1] = NREF(j, 1) + u[j][1];
+          xr[2] = NREF(j, 2) + u[j][2];
           if (save) {
             double* ck = ckpt + sb * 6 * P.ck_stride;
 #pragma unroll
@@ -714,9 +713,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
             }
           }
         } else if (rewrite_fixed) {
-          xr[0] = nref[j][0] + u[j][0];
-          xr[1] = nref[j][1] + u[j][1];
-          xr[2] = nref[j][2] + u[j][2];
+          xr[0] = NREF(j, 0) + u[j][0];
+          xr[1] = NREF(j, 1) + u[j][1];
+          xr[2] = NREF(j, 2) + u[j][2];
         }
       }
       rewrite_fixed = false;
@@ -839,6 +838,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     __syncthreads();
   }
 #undef SJ
+#undef NREF
 }
 
 }  // namespace fibra_b200
