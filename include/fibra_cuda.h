@@ -32,6 +32,8 @@ extern "C" {
 #define FIBRA_E_NOT_CONVERGED 6   /* SolverError: base not converged (stiffness.cpp:75)*/
 #define FIBRA_E_PROBE_FAILED 7    /* SolverError: probe q failed (stiffness.cpp:106-118)*/
 #define FIBRA_E_SINGULAR 8        /* SolverError: [M][T] singular (stiffness.cpp:33)   */
+#define FIBRA_E_ASM_STRESS 10     /* SolverError: non-finite stress response (macrofem.cpp:122-125) */
+#define FIBRA_E_ASM_RESIDUAL 11   /* SolverError: non-finite assembled residual (macrofem.cpp:186-187) */
 #define FIBRA_E_CUDA 20           /* CUDA runtime error (call-level)                   */
 #define FIBRA_E_ARG 21            /* bad argument / call order (call-level)            */
 #define FIBRA_E_IO 22             /* IoError (network files)                           */
@@ -246,6 +248,44 @@ int fibra_cuda_phase_profile(fibra_ctx* ctx, unsigned long long* out, size_t cap
 /* Diagnostics: with FIBRA_TRACE set at solve time, per solve {start ns, end ns,
  * sm << 32 | block, iterations} of the last solve call (solve index layout of the results). */
 int fibra_cuda_trace(fibra_ctx* ctx, unsigned long long* out, size_t cap, size_t* n);
+
+/* ---- macro assembly (csrc/assembly.cu) ---------------------------------
+ * Replaces fibra::assemble(const MacroMesh&, const DofNumbering&, std::span<const
+ * PointResponse>, const Eigen::VectorXd& f_ext_free)  (macrofem.hpp:77-79, body
+ * macrofem.cpp:104-187).  The mesh topology and DofNumbering (macrofem.hpp:29-33) fix the
+ * sparsity pattern, so it is planned once: assembly_create takes tets[4 n_tets] (node ids),
+ * free_of_dof[3 n_nodes] (-1 = constrained) and n_free.  Each assemble call then takes the
+ * current coords[3 n_nodes], one response record per tet (sigma as SymTensor3 xx,yy,zz,yz,
+ * xz,xy followed by the Mandel66 spatial_c row-major: 42 doubles at the start of every
+ * record; response_stride in doubles = 42 for a PointResponse array, sizeof(
+ * fibra_point_result)/8 for solve results) and f_ext_free[n_free] (NULL = zero), and
+ * returns residual[n_free] = f_int - f_ext and the nnz values of Assembly::stiffness in
+ * Eigen's compressed column-major order (assembly_pattern: col_ptr[n_free+1], row_idx[nnz],
+ * rows ascending per column) -- bit-identical to the reference's setFromTriplets result.
+ * Errors: FIBRA_E_ASM_STRESS / FIBRA_E_KINEMATICS with *bad_element = the first failing
+ * element in element order (the reference's exception), then FIBRA_E_ASM_RESIDUAL. */
+typedef struct fibra_assembly fibra_assembly;
+int fibra_cuda_assembly_create(int device, const int32_t* tets, int32_t n_tets, int32_t n_nodes,
+                               const int32_t* free_of_dof, int32_t n_free, fibra_assembly** out);
+int fibra_cuda_assembly_set_stream(fibra_assembly* as, void* cuda_stream);
+int fibra_cuda_assembly_pattern(const fibra_assembly* as, int64_t* nnz, int64_t* col_ptr,
+                                int32_t* row_idx);
+/* host buffers in and out; blocks */
+int fibra_cuda_assemble(fibra_assembly* as, const double* coords, const double* responses,
+                        int64_t response_stride, const double* f_ext_free, double* residual,
+                        double* values, int32_t* bad_element);
+/* device buffers (e.g. the out_dev of fibra_cuda_solve_device); asynchronous on the
+ * assembly's stream -- fibra_cuda_assembly_status synchronizes and reports errors */
+int fibra_cuda_assemble_device(fibra_assembly* as, const double* coords_dev,
+                               const double* responses_dev, int64_t response_stride,
+                               const double* f_ext_dev, double* residual_dev, double* values_dev);
+int fibra_cuda_assembly_status(fibra_assembly* as, int32_t* bad_element);
+/* device time of the last assemble: ms[3] = {element kernel, pair gather, residual} */
+int fibra_cuda_assembly_times(fibra_assembly* as, float* ms);
+/* out[5] = {n_tets, n_nodes, n_free, nnz, node pairs} */
+int fibra_cuda_assembly_info(const fibra_assembly* as, int64_t* out);
+const char* fibra_cuda_assembly_last_error(const fibra_assembly* as);
+int fibra_cuda_assembly_free(fibra_assembly* as);
 
 #ifdef __cplusplus
 }

@@ -26,7 +26,8 @@ REF_SO = os.path.join(HERE, "_ref", "libfibra_ref.so")
 REF_SRC = "/root/reference/proj"
 
 STATUS = {0: "ok", 1: "config", 2: "kinematics", 3: "collapse", 4: "bad_dt", 5: "diverged",
-          6: "not_converged", 7: "probe_failed", 8: "singular", 9: "unconverged_state"}
+          6: "not_converged", 7: "probe_failed", 8: "singular", 9: "unconverged_state",
+          10: "nonfinite_stress", 11: "nonfinite_residual"}
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -526,3 +527,53 @@ def ref_batch_stress(rnet: RefNetwork, F, cfg: RelaxConfig = None, law: Law = No
 
 def network_from_ref(rnet: RefNetwork, box_half=0.5, tol_bnd=1e-6) -> Network:
     return Network(rnet.coords, rnet.fib_a, rnet.fib_b, rnet.area, rnet.modulus, box_half, tol_bnd)
+
+
+# ----------------------------------------------------------------------------------
+# macro assembly (macrofem.cpp:41-187): the checker of the device assembly
+# ----------------------------------------------------------------------------------
+def tet_geom(coords, tet):
+    """b_matrix (macrofem.cpp:41-60) -> (grad[4,3], volume)."""
+    c = np.ascontiguousarray(coords, dtype=np.float64)
+    n = np.ascontiguousarray(tet, dtype=np.int32)
+    g = np.zeros(12)
+    v = C.c_double(0)
+    L = lib()
+    L.or_tet_geom.argtypes = [_dp, _ip, _dp, C.POINTER(C.c_double)]
+    rc = L.or_tet_geom(_ptr(c, _dp), _ptr(n, _ip), _ptr(g, _dp), C.byref(v))
+    if rc:
+        raise OracleError(rc, "b_matrix")
+    return g.reshape(4, 3), v.value
+
+
+def assemble(tets, coords, sigma, c66, free_of_dof, n_free, f_ext=None):
+    """assemble (macrofem.cpp:104-187) -> (residual, col_ptr, row_idx, values): the
+    free x free stiffness in Eigen's compressed column-major layout.  Element errors raise
+    OracleError with .element set to the first failing element."""
+    tets = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64).reshape(-1, 6)
+    c66 = np.ascontiguousarray(c66, dtype=np.float64).reshape(-1, 36)
+    fod = np.ascontiguousarray(free_of_dof, dtype=np.int32)
+    ne = len(tets)
+    cap = max(1, 144 * ne)
+    res = np.zeros(n_free)
+    cp = np.zeros(n_free + 1, np.int64)
+    ri = np.zeros(cap, np.int32)
+    va = np.zeros(cap)
+    nnz = C.c_int64(0)
+    bad = C.c_int32(-1)
+    fe = None if f_ext is None else np.ascontiguousarray(f_ext, dtype=np.float64)
+    L = lib()
+    L.or_assemble.argtypes = [_ip, C.c_int32, _dp, _dp, _dp, _ip, C.c_int32, _dp, _dp, _lp,
+                              _ip, _dp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+    rc = L.or_assemble(_ptr(tets, _ip), ne, _ptr(coords, _dp), _ptr(sigma, _dp),
+                       _ptr(c66, _dp), _ptr(fod, _ip), n_free,
+                       None if fe is None else _ptr(fe, _dp), _ptr(res, _dp), _ptr(cp, _lp),
+                       _ptr(ri, _ip), _ptr(va, _dp), cap, C.byref(nnz), C.byref(bad))
+    if rc:
+        err = OracleError(rc, f"assemble (element {bad.value})")
+        err.element = bad.value
+        raise err
+    k = nnz.value
+    return res, cp, ri[:k].copy(), va[:k].copy()

@@ -903,3 +903,174 @@ int or_batch_response(const or_network* const* entries, const int32_t* entry_of_
   pthread_mutex_destroy(&j.mu);
   return j.config_error ? OR_CONFIG : OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Macro assembly  macrofem.cpp:41-60 (b_matrix), :64-86 (mandel_b),          */
+/* :104-187 (assemble).  The 3x3 determinant / inverse are Eigen's fixed-size */
+/* paths (Eigen is absent here: restated from Eigen 3.4 Determinant.h         */
+/* determinant_impl<3> and InverseImpl.h compute_inverse<3>), and the         */
+/* SparseMatrix::setFromTriplets duplicate folding (SparseMatrix.h             */
+/* set_from_triplets: first value, then acc = acc + next in triplet order,     */
+/* transposed copy sorts rows within each column).                            */
+/* ------------------------------------------------------------------------- */
+static inline double eig_cof3(const double* m, int i, int j) { /* InverseImpl.h cofactor_3x3 */
+  const int i1 = (i + 1) % 3, i2 = (i + 2) % 3, j1 = (j + 1) % 3, j2 = (j + 2) % 3;
+  return m[3 * i1 + j1] * m[3 * i2 + j2] - m[3 * i1 + j2] * m[3 * i2 + j1];
+}
+
+/* b_matrix (macrofem.cpp:41-60): grad[4][3], volume; OR_KINEMATICS on det <= 0 */
+int or_tet_geom(const double* coords, const int32_t n[4], double grad[12], double* volume) {
+  double jac[9]; /* row-major; columns are edge vectors (:43-47) */
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < 3; ++r) jac[3 * r + c] = coords[3 * n[c + 1] + r] - coords[3 * n[0] + r];
+  /* Eigen determinant_impl<3>: bruteforce_det3_helper(m,0,1,2) - (m,1,0,2) + (m,2,0,1) */
+  const double det = jac[0] * (jac[4] * jac[8] - jac[5] * jac[7]) -
+                     jac[1] * (jac[3] * jac[8] - jac[5] * jac[6]) +
+                     jac[2] * (jac[3] * jac[7] - jac[4] * jac[6]);
+  if (!(det > 0)) return OR_KINEMATICS;
+  /* Eigen compute_inverse<3>: cofactors of column 0, det as (c0*m00 + c1*m10) + c2*m20 */
+  const double c0 = eig_cof3(jac, 0, 0), c1 = eig_cof3(jac, 1, 0), c2 = eig_cof3(jac, 2, 0);
+  const double idet = 1.0 / ((c0 * jac[0] + c1 * jac[3]) + c2 * jac[6]);
+  double inv[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) inv[3 * r + c] = eig_cof3(jac, c, r) * idet;
+  *volume = det / 6.0;
+  for (int a = 0; a < 3; ++a)
+    for (int k = 0; k < 3; ++k) grad[3 * (a + 1) + k] = inv[3 * a + k];
+  for (int k = 0; k < 3; ++k) grad[k] = -grad[3 + k] - grad[6 + k] - grad[9 + k];
+  return OR_OK;
+}
+
+/* mandel_b (macrofem.cpp:64-86): b[6][12] accumulated onto zeros */
+void or_mandel_b(const double grad[12], double b[72]) {
+  static const int pair[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+  for (int i = 0; i < 72; ++i) b[i] = 0;
+  for (int node = 0; node < 4; ++node) {
+    const double* gn = grad + 3 * node;
+    for (int ax = 0; ax < 3; ++ax) {
+      const int col = 3 * node + ax;
+      b[12 * ax + col] += gn[ax];
+      for (int sh = 0; sh < 3; ++sh) {
+        const int i = pair[sh][0], j = pair[sh][1];
+        double v = 0;
+        if (ax == i) v += 0.5 * gn[j];
+        if (ax == j) v += 0.5 * gn[i];
+        b[12 * (3 + sh) + col] += kSqrt2 * v;
+      }
+    }
+  }
+}
+
+/* per-element work of assemble (macrofem.cpp:118-167): fe[12], ke[144] (row-major) */
+int or_element_matrices(const double* coords, const int32_t n[4], const double sigma[6],
+                        const double c66[36], double fe[12], double ke[144]) {
+  double sig[6], grad[12], vol, b[72], cb[72], sf[9];
+  or_mandel(sigma, sig);
+  for (int i = 0; i < 6; ++i)
+    if (!isfinite(sig[i])) return OR_ASM_STRESS; /* :122-125 */
+  if (or_tet_geom(coords, n, grad, &vol)) return OR_KINEMATICS; /* :128-132 */
+  or_mandel_b(grad, b);
+  for (int c = 0; c < 12; ++c) { /* :137-142 */
+    double s = 0;
+    for (int p = 0; p < 6; ++p) s += b[12 * p + c] * sig[p];
+    fe[c] = vol * s;
+  }
+  for (int p = 0; p < 6; ++p) /* :145-150 */
+    for (int c = 0; c < 12; ++c) {
+      double s = 0;
+      for (int q = 0; q < 6; ++q) s += c66[6 * p + q] * b[12 * q + c];
+      cb[12 * p + c] = s;
+    }
+  for (int r = 0; r < 12; ++r) /* :151-157 */
+    for (int c = 0; c < 12; ++c) {
+      double s = 0;
+      for (int p = 0; p < 6; ++p) s += b[12 * p + r] * cb[12 * p + c];
+      ke[12 * r + c] = vol * s;
+    }
+  or_sym_full(sigma, sf); /* :160-168 geometric part */
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      double gsg = 0;
+      for (int p = 0; p < 3; ++p)
+        for (int q = 0; q < 3; ++q) gsg += grad[3 * i + p] * sf[3 * p + q] * grad[3 * j + q];
+      gsg *= vol;
+      for (int ax = 0; ax < 3; ++ax) ke[12 * (3 * i + ax) + 3 * j + ax] += gsg;
+    }
+  return OR_OK;
+}
+
+typedef struct { int32_t r, c; int64_t ord; double v; } or_trip;
+
+static int trip_cmp(const void* x, const void* y) { /* (col, row, triplet order) */
+  const or_trip* a = (const or_trip*)x;
+  const or_trip* b = (const or_trip*)y;
+  if (a->c != b->c) return a->c < b->c ? -1 : 1;
+  if (a->r != b->r) return a->r < b->r ? -1 : 1;
+  return a->ord < b->ord ? -1 : (a->ord > b->ord);
+}
+
+/* assemble (macrofem.cpp:104-187).  tets[4 n_tets], coords[3 n_nodes] (current),
+ * sigma[6 n_tets] (SymTensor3), c66[36 n_tets] (Mandel66 row-major), free_of_dof[3 n_nodes],
+ * f_ext[n_free] (NULL = zero).  Out: residual[n_free]; the compressed column-major matrix
+ * (col_ptr[n_free+1], row_idx/values with capacity cap >= 144 n_tets), *nnz.
+ * On an element error *bad_element = the first failing element (element order). */
+int or_assemble(const int32_t* tets, int32_t n_tets, const double* coords,
+                const double* sigma, const double* c66, const int32_t* free_of_dof,
+                int32_t n_free, const double* f_ext, double* residual, int64_t* col_ptr,
+                int32_t* row_idx, double* values, int64_t cap, int64_t* nnz,
+                int32_t* bad_element) {
+  or_trip* trips = (or_trip*)malloc(sizeof(or_trip) * (size_t)(144 * (int64_t)n_tets + 1));
+  if (!trips) return OR_CONFIG;
+  int64_t nt = 0;
+  *bad_element = -1;
+  for (int32_t i = 0; i < n_free; ++i) residual[i] = 0.0; /* VectorXd::Zero */
+  for (int32_t e = 0; e < n_tets; ++e) {
+    const int32_t* n = tets + 4 * e;
+    double fe[12], ke[144];
+    const int rc = or_element_matrices(coords, n, sigma + 6 * e, c66 + 36 * e, fe, ke);
+    if (rc) {
+      *bad_element = e;
+      free(trips);
+      return rc;
+    }
+    for (int a = 0; a < 4; ++a) /* :170-183 */
+      for (int ax = 0; ax < 3; ++ax) {
+        const int32_t rf = free_of_dof[3 * n[a] + ax];
+        if (rf < 0) continue;
+        residual[rf] += fe[3 * a + ax];
+        for (int bn = 0; bn < 4; ++bn)
+          for (int bx = 0; bx < 3; ++bx) {
+            const int32_t cf = free_of_dof[3 * n[bn] + bx];
+            if (cf < 0) continue;
+            trips[nt].r = rf;
+            trips[nt].c = cf;
+            trips[nt].ord = nt;
+            trips[nt].v = ke[12 * (3 * a + ax) + 3 * bn + bx];
+            ++nt;
+          }
+      }
+  }
+  for (int32_t i = 0; i < n_free; ++i) residual[i] -= f_ext ? f_ext[i] : 0.0; /* :185 */
+  qsort(trips, (size_t)nt, sizeof(or_trip), trip_cmp);
+  int64_t k = -1;
+  for (int32_t c = 0; c <= n_free; ++c) col_ptr[c] = 0;
+  for (int64_t t = 0; t < nt; ++t) {
+    if (k >= 0 && trips[t].r == row_idx[k] && trips[t].c == trips[t - 1].c) {
+      values[k] = values[k] + trips[t].v; /* collapseDuplicates: scalar_sum_op */
+      continue;
+    }
+    if (++k >= cap) {
+      free(trips);
+      return OR_CONFIG;
+    }
+    row_idx[k] = trips[t].r;
+    values[k] = trips[t].v;
+    col_ptr[trips[t].c + 1]++;
+  }
+  *nnz = k + 1;
+  for (int32_t c = 0; c < n_free; ++c) col_ptr[c + 1] += col_ptr[c];
+  free(trips);
+  for (int32_t i = 0; i < n_free; ++i)
+    if (!isfinite(residual[i])) return OR_ASM_RESIDUAL; /* :186-187 */
+  return OR_OK;
+}

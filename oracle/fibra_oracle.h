@@ -36,7 +36,9 @@ enum {
   OR_NOT_CONVERGED = 6,   /* SolverError: base not converged (stiffness.cpp:75-77) */
   OR_PROBE_FAILED = 7,    /* SolverError: probe failed / not converged (stiffness.cpp:106-118) */
   OR_SINGULAR = 8,        /* SolverError: probing system singular (stiffness.cpp:33-34) */
-  OR_NOT_CONVERGED_STATE = 9 /* SolverError: homogenized stress on unconverged state */
+  OR_NOT_CONVERGED_STATE = 9, /* SolverError: homogenized stress on unconverged state */
+  OR_ASM_STRESS = 10,     /* SolverError: non-finite stress response (macrofem.cpp:122-125) */
+  OR_ASM_RESIDUAL = 11    /* SolverError: non-finite assembled residual (macrofem.cpp:186-187) */
 };
 
 /* FiberNetwork (network.hpp:55-101) after construction (network.cpp:67-157). */
@@ -154,6 +156,17 @@ int or_batch_response(const or_network* const* entries, const int32_t* entry_of_
                       const or_law* law, const double* F, const or_relax_cfg* rcfg,
                       double fd_rel_step, int reuse_warm, int want_tangent, int n_threads,
                       or_response* out, int32_t* status);
+
+/* ---- macro assembly (macrofem.cpp:41-187) ---- */
+int or_tet_geom(const double* coords, const int32_t n[4], double grad[12], double* volume);
+void or_mandel_b(const double grad[12], double b[72]);
+int or_element_matrices(const double* coords, const int32_t n[4], const double sigma[6],
+                        const double c66[36], double fe[12], double ke[144]);
+int or_assemble(const int32_t* tets, int32_t n_tets, const double* coords,
+                const double* sigma, const double* c66, const int32_t* free_of_dof,
+                int32_t n_free, const double* f_ext, double* residual, int64_t* col_ptr,
+                int32_t* row_idx, double* values, int64_t cap, int64_t* nnz,
+                int32_t* bad_element);
 
 #ifdef __cplusplus
 }

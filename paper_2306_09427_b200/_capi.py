@@ -19,6 +19,7 @@ _bp = C.POINTER(C.c_uint8)
 FIBRA_OK = 0
 STATUS_NAMES = {0: "ok", 1: "config", 2: "kinematics", 3: "collapse", 4: "bad_dt",
                 5: "diverged", 6: "not_converged", 7: "probe_failed", 8: "singular",
+                10: "non-finite stress response", 11: "non-finite assembled residual",
                 20: "cuda", 21: "arg", 22: "io"}
 
 # every symbol include/fibra_cuda.h declares (checked by tests/test_capi.py)
@@ -36,6 +37,10 @@ EXPORTS = [
     "fibra_cuda_solve_device", "fibra_cuda_synchronize", "fibra_cuda_last_stats",
     "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile", "fibra_cuda_trace",
     "fibra_cuda_selftest_fastmath",
+    "fibra_cuda_assembly_create", "fibra_cuda_assembly_set_stream", "fibra_cuda_assembly_pattern",
+    "fibra_cuda_assemble", "fibra_cuda_assemble_device", "fibra_cuda_assembly_status",
+    "fibra_cuda_assembly_times", "fibra_cuda_assembly_info", "fibra_cuda_assembly_last_error",
+    "fibra_cuda_assembly_free",
 ]
 
 
@@ -163,6 +168,17 @@ def load(build_if_missing: bool = True):
                                        C.POINTER(C.c_size_t)]),
         "fibra_cuda_phase_profile": (C.c_int, [vp, C.POINTER(C.c_uint64), C.c_size_t,
                                                C.POINTER(C.c_size_t)]),
+        "fibra_cuda_assembly_create": (C.c_int, [C.c_int, _ip, C.c_int32, C.c_int32, _ip,
+                                                 C.c_int32, pp]),
+        "fibra_cuda_assembly_set_stream": (C.c_int, [vp, vp]),
+        "fibra_cuda_assembly_pattern": (C.c_int, [vp, _lp, _lp, _ip]),
+        "fibra_cuda_assemble": (C.c_int, [vp, _dp, _dp, C.c_int64, _dp, _dp, _dp, _ip]),
+        "fibra_cuda_assemble_device": (C.c_int, [vp, vp, vp, C.c_int64, vp, vp, vp]),
+        "fibra_cuda_assembly_status": (C.c_int, [vp, _ip]),
+        "fibra_cuda_assembly_times": (C.c_int, [vp, C.POINTER(C.c_float)]),
+        "fibra_cuda_assembly_info": (C.c_int, [vp, _lp]),
+        "fibra_cuda_assembly_last_error": (C.c_char_p, [vp]),
+        "fibra_cuda_assembly_free": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

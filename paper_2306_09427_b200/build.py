@@ -25,6 +25,7 @@ SOURCES = [
     os.path.join(HERE, "csrc", "fibra_cuda.cu"),
     os.path.join(HERE, "csrc", "kernels_resident.cu"),
     os.path.join(HERE, "csrc", "kernels_cluster.cu"),
+    os.path.join(HERE, "csrc", "assembly.cu"),
     os.path.join(HERE, "csrc", "host", "network.cpp"),
     os.path.join(HERE, "csrc", "host", "netgen.cpp"),
     os.path.join(HERE, "csrc", "host", "schedule.cpp"),
