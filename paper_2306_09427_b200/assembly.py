@@ -173,10 +173,11 @@ class MacroAssembler:
         _check(self._h, self._L.fibra_cuda_assembly_set_stream(self._h, C.c_void_p(cuda_stream)))
 
     def assemble(self, coords, sigma=None, spatial_c=None, f_ext_free=None, responses=None,
-                 stride: int = 42) -> Assembly:
+                 stride: int = 42, out=None) -> Assembly:
         """Host arrays in and out.  Responses either as ``sigma`` (n,6) + ``spatial_c``
         (n,6,6), or as ``responses``: a float64 record array whose rows start with the 42
-        doubles of a PointResponse (``stride`` doubles per row)."""
+        doubles of a PointResponse (``stride`` doubles per row).  ``out`` = optional
+        (residual[n_free], values[nnz]) float64 buffers (e.g. pinned) to write into."""
         n = self.mesh.n_elements
         if responses is None:
             responses = np.empty((n, 42))
@@ -186,8 +187,14 @@ class MacroAssembler:
         resp = np.ascontiguousarray(responses).view(np.float64).reshape(-1)
         x = np.ascontiguousarray(coords, dtype=np.float64)
         fe = None if f_ext_free is None else np.ascontiguousarray(f_ext_free, dtype=np.float64)
-        res = np.zeros(self.numbering.n_free)
-        vals = np.zeros(self.nnz)
+        if out is None:
+            res, vals = np.zeros(self.numbering.n_free), np.zeros(self.nnz)
+        else:
+            res, vals = out
+            if (res.dtype != np.float64 or vals.dtype != np.float64 or not res.flags.c_contiguous
+                    or not vals.flags.c_contiguous or res.size != self.numbering.n_free
+                    or vals.size != self.nnz):
+                raise ValueError("out must be contiguous float64 (n_free,) and (nnz,) arrays")
         bad = C.c_int32(-1)
         rc = self._L.fibra_cuda_assemble(self._h, _ptr(x, _capi._dp), _ptr(resp, _capi._dp),
                                          stride, None if fe is None else _ptr(fe, _capi._dp),

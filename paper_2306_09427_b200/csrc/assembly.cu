@@ -37,6 +37,7 @@ namespace {
 constexpr double kSqrt2 = 1.4142135623730951;  // macrofem.cpp:62
 constexpr int kTetsPerCta = 8;
 constexpr int kElemThreads = 12 * kTetsPerCta;
+constexpr int kKeStride = 146;  // padded K_e staging: elements of one warp on distinct banks
 
 __device__ __forceinline__ double cof3(const double* m, int i, int j) {
   // Eigen InverseImpl.h cofactor_3x3<i, j>
@@ -68,29 +69,58 @@ __device__ __forceinline__ double tet_geom(const double* x, double grad[12], dou
   return det;
 }
 
-// column c = 3 node + ax of mandel_b (macrofem.cpp:64-86), accumulated onto zeros
-__device__ __forceinline__ void b_column(const double grad[12], int c, double bc[6]) {
+// column c = 3 node + ax of mandel_b (macrofem.cpp:64-86), accumulated onto zeros; shear
+// rows (23, 13, 12) = pairs (1,2) (0,2) (0,1)
+__device__ __forceinline__ void b_column(const double* grad, int c, double bc[6]) {
   const int node = c / 3, ax = c % 3;
-  const double* gn = grad + 3 * node;
-#pragma unroll
-  for (int p = 0; p < 3; ++p) bc[p] = (p == ax) ? 0.0 + gn[ax] : 0.0;
-  const int pi[3] = {1, 0, 0}, pj[3] = {2, 2, 1};
-#pragma unroll
-  for (int sh = 0; sh < 3; ++sh) {
-    double v = 0;
-    if (ax == pi[sh]) v += 0.5 * gn[pj[sh]];
-    if (ax == pj[sh]) v += 0.5 * gn[pi[sh]];
-    bc[3 + sh] = 0.0 + kSqrt2 * v;
+  const double g0 = grad[3 * node], g1 = grad[3 * node + 1], g2 = grad[3 * node + 2];
+  const double gax = ax == 0 ? g0 : (ax == 1 ? g1 : g2);
+  bc[0] = ax == 0 ? 0.0 + gax : 0.0;
+  bc[1] = ax == 1 ? 0.0 + gax : 0.0;
+  bc[2] = ax == 2 ? 0.0 + gax : 0.0;
+  // sh 0 (1,2): ax 1 -> 0.5 g2, ax 2 -> 0.5 g1; sh 1 (0,2): ax 0 -> 0.5 g2, ax 2 -> 0.5 g0;
+  // sh 2 (0,1): ax 0 -> 0.5 g1, ax 1 -> 0.5 g0  (v = 0 + 0.5 g, else v = 0)
+  const double v0 = ax == 1 ? 0.0 + 0.5 * g2 : (ax == 2 ? 0.0 + 0.5 * g1 : 0.0);
+  const double v1 = ax == 0 ? 0.0 + 0.5 * g2 : (ax == 2 ? 0.0 + 0.5 * g0 : 0.0);
+  const double v2 = ax == 0 ? 0.0 + 0.5 * g1 : (ax == 1 ? 0.0 + 0.5 * g0 : 0.0);
+  bc[3] = 0.0 + kSqrt2 * v0;
+  bc[4] = 0.0 + kSqrt2 * v1;
+  bc[5] = 0.0 + kSqrt2 * v2;
+}
+
+// The three structurally non-zero rows of column c = 3 node + ax of mandel_b, ascending:
+// ax 0 -> rows 0, 4, 5; ax 1 -> 1, 3, 5; ax 2 -> 2, 3, 4 (same values as b_column).
+// Skipping the structural zeros is exact: a sum that starts at +0.0 never becomes -0.0, so
+// adding a +-0 product leaves it unchanged -- provided the other factor is finite (an inf
+// or NaN would turn the product into NaN); callers fall back to the dense loops otherwise.
+__device__ __forceinline__ double sel6(const double v[6], int i) {  // no local-memory indexing
+  return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : i == 3 ? v[3] : i == 4 ? v[4] : v[5];
+}
+
+__device__ __forceinline__ void b_column_sparse(const double* grad, int c, int rows[3],
+                                                double v[3]) {
+  const int node = c / 3, ax = c % 3;
+  const double g0 = grad[3 * node], g1 = grad[3 * node + 1], g2 = grad[3 * node + 2];
+  if (ax == 0) {
+    rows[0] = 0, rows[1] = 4, rows[2] = 5;
+    v[0] = 0.0 + g0, v[1] = 0.0 + kSqrt2 * (0.0 + 0.5 * g2), v[2] = 0.0 + kSqrt2 * (0.0 + 0.5 * g1);
+  } else if (ax == 1) {
+    rows[0] = 1, rows[1] = 3, rows[2] = 5;
+    v[0] = 0.0 + g1, v[1] = 0.0 + kSqrt2 * (0.0 + 0.5 * g2), v[2] = 0.0 + kSqrt2 * (0.0 + 0.5 * g0);
+  } else {
+    rows[0] = 2, rows[1] = 3, rows[2] = 4;
+    v[0] = 0.0 + g2, v[1] = 0.0 + kSqrt2 * (0.0 + 0.5 * g1), v[2] = 0.0 + kSqrt2 * (0.0 + 0.5 * g0);
   }
 }
 
-__global__ void __launch_bounds__(kElemThreads)
+__global__ void __launch_bounds__(kElemThreads, 8)
     asm_element_kernel(int n_tets, const int4* __restrict__ tets, const double* __restrict__ coords,
                        const double* __restrict__ resp, long long stride, double* __restrict__ fe,
                        double* __restrict__ ke, unsigned long long* __restrict__ err) {
   __shared__ double s_resp[kTetsPerCta][42];
-  __shared__ double s_cb[kTetsPerCta][6][12];
-  __shared__ double s_ke[kTetsPerCta * 144];
+  __shared__ double s_x[kTetsPerCta][12];
+  __shared__ double s_geo[kTetsPerCta][14];  // grad[4][3], volume, finite flag
+  __shared__ double s_ke[kTetsPerCta * kKeStride];
   const int le = threadIdx.x / 12, r = threadIdx.x % 12;
   const long long e0 = static_cast<long long>(blockIdx.x) * kTetsPerCta;
   const int n_here = static_cast<int>(min(static_cast<long long>(kTetsPerCta), n_tets - e0));
@@ -98,73 +128,127 @@ __global__ void __launch_bounds__(kElemThreads)
     s_resp[i / 42][i % 42] = resp[(e0 + i / 42) * stride + i % 42];
   const long long e = e0 + le;
   const bool live = le < n_here;
-  double grad[12], vol = 0, det = 1;
-  if (live) {
-    const int4 t = tets[e];
-    double x[12];
-    const int nd[4] = {t.x, t.y, t.z, t.w};
+  if (live && r < 4) {  // node r's coordinates
+    const int* t = reinterpret_cast<const int*>(tets + e);
+    const int nd = t[r];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) x[3 * a + k] = coords[3 * nd[a] + k];
-    det = tet_geom(x, grad, &vol);
+    for (int k = 0; k < 3; ++k) s_x[le][3 * r + k] = coords[3 * nd + k];
   }
   __syncthreads();
   const double* sg = s_resp[le];  // SymTensor3 xx yy zz yz xz xy, then Mandel66 row-major
   const double* cm = sg + 6;
-  if (live) {
-    if (r == 0) {
-      const double m[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
-      bool fin = true;
-      for (int i = 0; i < 6; ++i) fin = fin && isfinite(m[i]);
-      const int code = !fin ? FIBRA_E_ASM_STRESS : (!(det > 0) ? FIBRA_E_KINEMATICS : 0);
-      if (code) atomicMin(err, (static_cast<unsigned long long>(e) << 8) | code);
-    }
-    double bc[6];
-    b_column(grad, r, bc);
-    const double sig[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
-    double s = 0;  // internal force (:137-142)
+  if (live && r == 0) {  // b_matrix once per element, then the error order of :118-132
+    double grad[12], vol;
+    const double det = tet_geom(s_x[le], grad, &vol);
 #pragma unroll
-    for (int p = 0; p < 6; ++p) s += bc[p] * sig[p];
-    fe[e * 12 + r] = vol * s;
+    for (int i = 0; i < 12; ++i) s_geo[le][i] = grad[i];
+    s_geo[le][12] = vol;
+    const double m[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
+    bool fin = true;
 #pragma unroll
-    for (int p = 0; p < 6; ++p) {  // C B, column r (:145-150)
-      double t = 0;
-#pragma unroll
-      for (int q = 0; q < 6; ++q) t += cm[6 * p + q] * bc[q];
-      s_cb[le][p][r] = t;
-    }
+    for (int i = 0; i < 6; ++i) fin = fin && isfinite(m[i]);
+    const int code = !fin ? FIBRA_E_ASM_STRESS : (!(det > 0) ? FIBRA_E_KINEMATICS : 0);
+    if (code) atomicMin(err, (static_cast<unsigned long long>(e) << 8) | code);
+    bool cfin = fin;  // sigma and C finite: the structural-zero skip below is exact
+    for (int i = 0; i < 36; ++i) cfin = cfin && isfinite(cm[i]);
+    s_geo[le][13] = cfin ? 1.0 : 0.0;
   }
   __syncthreads();
+  // thread r owns column c = r = 3 b + bx of K_e: (C B)[:, c] stays in registers and the 12
+  // rows are produced from the register copy of grad (row indices unrolled)
+  const double* grad_s = s_geo[le];
+  double* kb = s_ke + le * kKeStride;
   if (live) {
-    double br[6];
-    b_column(grad, r, br);
-    const int a = r / 3, ax = r % 3;
-    const double sf[9] = {sg[0], sg[5], sg[4], sg[5], sg[1], sg[3], sg[4], sg[3], sg[2]};
-    double* kb = s_ke + le * 144;
+    const int c = r, b = c / 3, bx = c % 3;
+    const double vol = grad_s[12];
+    double g[12];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      double gsg = 0;  // geometric part (:160-168)
+    for (int i = 0; i < 12; ++i) g[i] = grad_s[i];
+    const double sig[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
+    const double sf[9] = {sg[0], sg[5], sg[4], sg[5], sg[1], sg[3], sg[4], sg[3], sg[2]};
+    const double gb[3] = {grad_s[3 * b], grad_s[3 * b + 1], grad_s[3 * b + 2]};
+    double gsg[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      double t = 0;  // geometric part (:160-168), i = a, j = b
 #pragma unroll
       for (int p = 0; p < 3; ++p)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) gsg += grad[3 * a + p] * sf[3 * p + q] * grad[3 * b + q];
-      gsg *= vol;
+        for (int q = 0; q < 3; ++q) t += g[3 * a + p] * sf[3 * p + q] * gb[q];
+      gsg[a] = t * vol;
+    }
+    bool finite = grad_s[13] != 0.0;
+    double cb[6];
+    if (finite) {  // structural zeros of B skipped (exact, see b_column_sparse)
+      int rc_[3];
+      double vc[3];
+      b_column_sparse(grad_s, c, rc_, vc);
+      double s = 0;  // internal force (:137-142)
 #pragma unroll
-      for (int bx = 0; bx < 3; ++bx) {
-        const int c = 3 * b + bx;
-        double s = 0;  // V B^T C B (:151-157)
+      for (int k = 0; k < 3; ++k) s += vc[k] * sel6(sig, rc_[k]);
+      fe[e * 12 + c] = vol * s;
 #pragma unroll
-        for (int p = 0; p < 6; ++p) s += br[p] * s_cb[le][p][c];
-        double k = vol * s;
-        if (bx == ax) k += gsg;
-        kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+      for (int p = 0; p < 6; ++p) {  // C B, column c (:145-150)
+        double t = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) t += cm[6 * p + rc_[k]] * vc[k];
+        cb[p] = t;
       }
+#pragma unroll
+      for (int p = 0; p < 6; ++p) finite = finite && isfinite(cb[p]);
+    } else {
+      double bc[6];
+      b_column(grad_s, c, bc);
+      double s = 0;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) s += bc[p] * sig[p];
+      fe[e * 12 + c] = vol * s;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) {
+        double t = 0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q) t += cm[6 * p + q] * bc[q];
+        cb[p] = t;
+      }
+    }
+    if (finite) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          // rows of B column 3a+ax (compile-time after unrolling): ax 0 -> 0,4,5 ...
+          const double gx = g[3 * a + ax];
+          const double h0 = ax == 0 ? g[3 * a + 2] : (ax == 1 ? g[3 * a + 2] : g[3 * a + 1]);
+          const double h1 = ax == 0 ? g[3 * a + 1] : g[3 * a];
+          const int p1 = ax == 0 ? 4 : 3, p2 = ax == 2 ? 4 : 5;
+          double t = 0;  // V B^T C B (:151-157)
+          t += (0.0 + gx) * cb[ax];
+          t += (0.0 + kSqrt2 * (0.0 + 0.5 * h0)) * cb[p1];
+          t += (0.0 + kSqrt2 * (0.0 + 0.5 * h1)) * cb[p2];
+          double k = vol * t;
+          if (bx == ax) k += gsg[a];
+          kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+        }
+    } else {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int ax = 0; ax < 3; ++ax) {
+          double br[6];
+          b_column(g, 3 * a + ax, br);
+          double t = 0;
+#pragma unroll
+          for (int p = 0; p < 6; ++p) t += br[p] * cb[p];
+          double k = vol * t;
+          if (bx == ax) k += gsg[a];
+          kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+        }
     }
   }
   __syncthreads();
   double* out = ke + e0 * 144;
-  for (int i = threadIdx.x; i < n_here * 144; i += kElemThreads) out[i] = s_ke[i];
+  for (int i = threadIdx.x; i < n_here * 144; i += kElemThreads)
+    out[i] = s_ke[(i / 144) * kKeStride + i % 144];
 }
 
 // one thread per node pair (A row node, B column node); contrib = e << 4 | a << 2 | b
@@ -255,6 +339,7 @@ struct fibra_assembly {
   int* d_nonfinite = nullptr;
   double *d_coords = nullptr, *d_resp = nullptr, *d_fext = nullptr, *d_residual = nullptr,
          *d_values = nullptr;
+  long long resp_cap = 0;
   cudaEvent_t ev[4] = {};
   int bad_element = -1;
 };
@@ -483,21 +568,27 @@ int fibra_cuda_assemble(fibra_assembly* as, const double* coords, const double* 
   AS_CUDA(as, cudaSetDevice(as->device));
   if (!as->d_coords) {
     AS_CUDA(as, cudaMalloc(&as->d_coords, sizeof(double) * 3 * std::max(1, as->n_nodes)));
-    AS_CUDA(as, cudaMalloc(&as->d_resp, sizeof(double) * 42 * std::max(1, as->n_tets)));
     AS_CUDA(as, cudaMalloc(&as->d_fext, sizeof(double) * std::max(1, as->n_free)));
     AS_CUDA(as, cudaMalloc(&as->d_residual, sizeof(double) * std::max(1, as->n_free)));
     AS_CUDA(as, cudaMalloc(&as->d_values, sizeof(double) * std::max<long long>(1, as->nnz)));
   }
+  // the record array travels as one contiguous copy (a pitched 2D copy of 42-double rows
+  // runs row by row); the kernel reads sigma + C at the caller's stride
+  const long long rec_doubles = static_cast<long long>(response_stride) * as->n_tets;
+  if (rec_doubles > as->resp_cap) {
+    if (as->d_resp) cudaFree(as->d_resp);
+    as->d_resp = nullptr;
+    AS_CUDA(as, cudaMalloc(&as->d_resp, sizeof(double) * std::max(1LL, rec_doubles)));
+    as->resp_cap = rec_doubles;
+  }
   AS_CUDA(as, cudaMemcpyAsync(as->d_coords, coords, sizeof(double) * 3 * as->n_nodes,
                               cudaMemcpyHostToDevice, as->stream));
-  // only sigma + Mandel C of each record travel (42 of response_stride doubles)
-  AS_CUDA(as, cudaMemcpy2DAsync(as->d_resp, sizeof(double) * 42, responses,
-                                sizeof(double) * response_stride, sizeof(double) * 42, as->n_tets,
-                                cudaMemcpyHostToDevice, as->stream));
+  AS_CUDA(as, cudaMemcpyAsync(as->d_resp, responses, sizeof(double) * rec_doubles,
+                              cudaMemcpyHostToDevice, as->stream));
   if (f_ext_free)
     AS_CUDA(as, cudaMemcpyAsync(as->d_fext, f_ext_free, sizeof(double) * as->n_free,
                                 cudaMemcpyHostToDevice, as->stream));
-  int rc = fibra_cuda_assemble_device(as, as->d_coords, as->d_resp, 42,
+  int rc = fibra_cuda_assemble_device(as, as->d_coords, as->d_resp, response_stride,
                                       f_ext_free ? as->d_fext : nullptr, as->d_residual,
                                       as->d_values);
   if (rc) return rc;

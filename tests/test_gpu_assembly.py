@@ -118,3 +118,23 @@ def test_assembly_of_solved_responses(oracle_lib):
     A.status()
     assert np.array_equal(bits(d_res.cpu().numpy()), bits(ref[0]))
     assert np.array_equal(bits(d_val.cpu().numpy()), bits(ref[3]))
+
+
+def test_assembly_nonfinite_tangent(oracle_lib):
+    """The reference checks only sigma (macrofem.cpp:122-125); an inf in C propagates into
+    K as inf/NaN.  Those elements take the kernel's dense path (the structural-zero skip is
+    exact only for finite factors); compare with NaN == NaN (payload bits differ between
+    x86 and the GPU) and bitwise everywhere else."""
+    mesh, num, sig, cm, f_ext = case(3, 2, 2, 9)
+    cm[4, 7] = np.inf
+    cm[30, 0] = -np.inf
+    cm[31, 13] = np.nan
+    sig[12] = 1e300  # C B finite, but products overflow in K
+    res, cp, ri, va = O.assemble(mesh.tets, mesh.coords.ravel(), sig, cm, num.free_of_dof,
+                                 num.n_free, f_ext)
+    asm = MacroAssembler(mesh, num).assemble(mesh.coords, sig, cm, f_ext)
+    assert np.array_equal(asm.col_ptr, cp) and np.array_equal(asm.row_idx, ri)
+    assert np.array_equal(bits(asm.residual), bits(res))
+    nan = np.isnan(va)
+    assert nan.any() and np.array_equal(np.isnan(asm.values), nan)
+    assert np.array_equal(bits(asm.values[~nan]), bits(va[~nan]))

@@ -84,10 +84,12 @@ def main():
     # e2e through the host call (pinned buffers)
     x_h = torch.from_numpy(np.ascontiguousarray(mesh.coords)).pin_memory().numpy()
     r_h = torch.from_numpy(resp).pin_memory().numpy()
-    A.assemble(x_h, responses=r_h, stride=42)
+    o_h = (torch.empty(nf, dtype=torch.float64).pin_memory().numpy(),
+           torch.empty(nnz, dtype=torch.float64).pin_memory().numpy())
+    A.assemble(x_h, responses=r_h, stride=42, out=o_h)
     t = time.perf_counter()
     for _ in range(args.steps):
-        asm = A.assemble(x_h, responses=r_h, stride=42)
+        A.assemble(x_h, responses=r_h, stride=42, out=o_h)
     e2e_ms = (time.perf_counter() - t) * 1e3 / args.steps
     # algorithmic bytes: responses + tets + coords in, compressed values + residual out
     alg = ne * (42 * 8 + 16) + mesh.n_nodes * 24 + nnz * 8 + nf * 8
