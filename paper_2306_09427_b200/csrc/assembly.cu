@@ -113,142 +113,174 @@ __device__ __forceinline__ void b_column_sparse(const double* grad, int c, int r
   }
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Persistent over tiles of kTetsPerCta tets.  While tile t is computed, the records and
+// node coordinates of tile t+1 are in flight (cp.async into the other shared stage) and the
+// node ids of tile t+2 are being loaded into registers, so the dependent tet -> coordinate
+// gather and the record staging leave the critical path.
 __global__ void __launch_bounds__(kElemThreads, 8)
     asm_element_kernel(int n_tets, const int4* __restrict__ tets, const double* __restrict__ coords,
                        const double* __restrict__ resp, long long stride, double* __restrict__ fe,
                        double* __restrict__ ke, unsigned long long* __restrict__ err) {
-  __shared__ double s_resp[kTetsPerCta][42];
-  __shared__ double s_x[kTetsPerCta][12];
+  __shared__ double s_resp[2][kTetsPerCta][42];
+  __shared__ double s_x[2][kTetsPerCta][12];
   __shared__ double s_geo[kTetsPerCta][14];  // grad[4][3], volume, finite flag
   __shared__ double s_ke[kTetsPerCta * kKeStride];
   const int le = threadIdx.x / 12, r = threadIdx.x % 12;
-  const long long e0 = static_cast<long long>(blockIdx.x) * kTetsPerCta;
-  const int n_here = static_cast<int>(min(static_cast<long long>(kTetsPerCta), n_tets - e0));
-  for (int i = threadIdx.x; i < n_here * 42; i += kElemThreads)
-    s_resp[i / 42][i % 42] = resp[(e0 + i / 42) * stride + i % 42];
-  const long long e = e0 + le;
-  const bool live = le < n_here;
-  if (live && r < 4) {  // node r's coordinates
-    const int* t = reinterpret_cast<const int*>(tets + e);
-    const int nd = t[r];
+  const long long n_tiles = (static_cast<long long>(n_tets) + kTetsPerCta - 1) / kTetsPerCta;
+  const long long step = gridDim.x;
+  // thread (le, r) fetches coordinate r % 3 of tet node r / 3
+  auto node_of = [&](long long tile) -> int {
+    const long long e = tile * kTetsPerCta + le;
+    return (tile < n_tiles && e < n_tets) ? reinterpret_cast<const int*>(tets + e)[r / 3] : -1;
+  };
+  auto issue = [&](long long tile, int st, int nd) {
+    if (tile >= n_tiles) return;
+    const long long e0 = tile * kTetsPerCta;
+    const int n_here = static_cast<int>(min(static_cast<long long>(kTetsPerCta), n_tets - e0));
+    for (int i = threadIdx.x; i < n_here * 42; i += kElemThreads)
+      cp_async8(&s_resp[st][i / 42][i % 42], resp + (e0 + i / 42) * stride + i % 42);
+    if (nd >= 0) cp_async8(&s_x[st][le][r], coords + 3LL * nd + r % 3);
+  };
+  long long tile = blockIdx.x;
+  int nd_next = node_of(tile + step);
+  issue(tile, 0, node_of(tile));
+  cp_async_commit();
+  for (int st = 0; tile < n_tiles; tile += step, st ^= 1) {
+    cp_async_wait_all();
+    __syncthreads();  // tile's stage landed; every thread is done with the previous tile
+    const int nd_after = node_of(tile + 2 * step);  // consumed next iteration
+    issue(tile + step, st ^ 1, nd_next);
+    cp_async_commit();
+    nd_next = nd_after;
+    const long long e0 = tile * kTetsPerCta;
+    const int n_here = static_cast<int>(min(static_cast<long long>(kTetsPerCta), n_tets - e0));
+    const long long e = e0 + le;
+    const bool live = le < n_here;
+    const double* sg = s_resp[st][le];  // SymTensor3 xx yy zz yz xz xy, then Mandel66
+    const double* cm = sg + 6;
+    if (live && r == 0) {  // b_matrix once per element, then the error order of :118-132
+      double grad[12], vol;
+      const double det = tet_geom(s_x[st][le], grad, &vol);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s_x[le][3 * r + k] = coords[3 * nd + k];
-  }
-  __syncthreads();
-  const double* sg = s_resp[le];  // SymTensor3 xx yy zz yz xz xy, then Mandel66 row-major
-  const double* cm = sg + 6;
-  if (live && r == 0) {  // b_matrix once per element, then the error order of :118-132
-    double grad[12], vol;
-    const double det = tet_geom(s_x[le], grad, &vol);
+      for (int i = 0; i < 12; ++i) s_geo[le][i] = grad[i];
+      s_geo[le][12] = vol;
+      const double m[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
+      bool fin = true;
 #pragma unroll
-    for (int i = 0; i < 12; ++i) s_geo[le][i] = grad[i];
-    s_geo[le][12] = vol;
-    const double m[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
-    bool fin = true;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) fin = fin && isfinite(m[i]);
-    const int code = !fin ? FIBRA_E_ASM_STRESS : (!(det > 0) ? FIBRA_E_KINEMATICS : 0);
-    if (code) atomicMin(err, (static_cast<unsigned long long>(e) << 8) | code);
-    bool cfin = fin;  // sigma and C finite: the structural-zero skip below is exact
-    for (int i = 0; i < 36; ++i) cfin = cfin && isfinite(cm[i]);
-    s_geo[le][13] = cfin ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // thread r owns column c = r = 3 b + bx of K_e: (C B)[:, c] stays in registers and the 12
-  // rows are produced from the register copy of grad (row indices unrolled)
-  const double* grad_s = s_geo[le];
-  double* kb = s_ke + le * kKeStride;
-  if (live) {
-    const int c = r, b = c / 3, bx = c % 3;
-    const double vol = grad_s[12];
-    double g[12];
-#pragma unroll
-    for (int i = 0; i < 12; ++i) g[i] = grad_s[i];
-    const double sig[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
-    const double sf[9] = {sg[0], sg[5], sg[4], sg[5], sg[1], sg[3], sg[4], sg[3], sg[2]};
-    const double gb[3] = {grad_s[3 * b], grad_s[3 * b + 1], grad_s[3 * b + 2]};
-    double gsg[4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      double t = 0;  // geometric part (:160-168), i = a, j = b
-#pragma unroll
-      for (int p = 0; p < 3; ++p)
-#pragma unroll
-        for (int q = 0; q < 3; ++q) t += g[3 * a + p] * sf[3 * p + q] * gb[q];
-      gsg[a] = t * vol;
+      for (int i = 0; i < 6; ++i) fin = fin && isfinite(m[i]);
+      const int code = !fin ? FIBRA_E_ASM_STRESS : (!(det > 0) ? FIBRA_E_KINEMATICS : 0);
+      if (code) atomicMin(err, (static_cast<unsigned long long>(e) << 8) | code);
+      bool cfin = fin;  // sigma and C finite: the structural-zero skip below is exact
+      for (int i = 0; i < 36; ++i) cfin = cfin && isfinite(cm[i]);
+      s_geo[le][13] = cfin ? 1.0 : 0.0;
     }
-    bool finite = grad_s[13] != 0.0;
-    double cb[6];
-    if (finite) {  // structural zeros of B skipped (exact, see b_column_sparse)
-      int rc_[3];
-      double vc[3];
-      b_column_sparse(grad_s, c, rc_, vc);
-      double s = 0;  // internal force (:137-142)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) s += vc[k] * sel6(sig, rc_[k]);
-      fe[e * 12 + c] = vol * s;
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {  // C B, column c (:145-150)
-        double t = 0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) t += cm[6 * p + rc_[k]] * vc[k];
-        cb[p] = t;
+    __syncthreads();
+    // thread r owns column c = r = 3 b + bx of K_e: (C B)[:, c] stays in registers and the
+    // 12 rows are produced from the register copy of grad (row indices unrolled)
+    const double* grad_s = s_geo[le];
+    double* kb = s_ke + le * kKeStride;
+    if (live) {
+      const int c = r, b = c / 3, bx = c % 3;
+      const double vol = grad_s[12];
+      double g[12];
+  #pragma unroll
+      for (int i = 0; i < 12; ++i) g[i] = grad_s[i];
+      const double sig[6] = {sg[0], sg[1], sg[2], kSqrt2 * sg[3], kSqrt2 * sg[4], kSqrt2 * sg[5]};
+      const double sf[9] = {sg[0], sg[5], sg[4], sg[5], sg[1], sg[3], sg[4], sg[3], sg[2]};
+      const double gb[3] = {grad_s[3 * b], grad_s[3 * b + 1], grad_s[3 * b + 2]};
+      double gsg[4];
+  #pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double t = 0;  // geometric part (:160-168), i = a, j = b
+  #pragma unroll
+        for (int p = 0; p < 3; ++p)
+  #pragma unroll
+          for (int q = 0; q < 3; ++q) t += g[3 * a + p] * sf[3 * p + q] * gb[q];
+        gsg[a] = t * vol;
       }
-#pragma unroll
-      for (int p = 0; p < 6; ++p) finite = finite && isfinite(cb[p]);
-    } else {
-      double bc[6];
-      b_column(grad_s, c, bc);
-      double s = 0;
-#pragma unroll
-      for (int p = 0; p < 6; ++p) s += bc[p] * sig[p];
-      fe[e * 12 + c] = vol * s;
-#pragma unroll
-      for (int p = 0; p < 6; ++p) {
-        double t = 0;
-#pragma unroll
-        for (int q = 0; q < 6; ++q) t += cm[6 * p + q] * bc[q];
-        cb[p] = t;
-      }
-    }
-    if (finite) {
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          // rows of B column 3a+ax (compile-time after unrolling): ax 0 -> 0,4,5 ...
-          const double gx = g[3 * a + ax];
-          const double h0 = ax == 0 ? g[3 * a + 2] : (ax == 1 ? g[3 * a + 2] : g[3 * a + 1]);
-          const double h1 = ax == 0 ? g[3 * a + 1] : g[3 * a];
-          const int p1 = ax == 0 ? 4 : 3, p2 = ax == 2 ? 4 : 5;
-          double t = 0;  // V B^T C B (:151-157)
-          t += (0.0 + gx) * cb[ax];
-          t += (0.0 + kSqrt2 * (0.0 + 0.5 * h0)) * cb[p1];
-          t += (0.0 + kSqrt2 * (0.0 + 0.5 * h1)) * cb[p2];
-          double k = vol * t;
-          if (bx == ax) k += gsg[a];
-          kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
-        }
-    } else {
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int ax = 0; ax < 3; ++ax) {
-          double br[6];
-          b_column(g, 3 * a + ax, br);
+      bool finite = grad_s[13] != 0.0;
+      double cb[6];
+      if (finite) {  // structural zeros of B skipped (exact, see b_column_sparse)
+        int rc_[3];
+        double vc[3];
+        b_column_sparse(grad_s, c, rc_, vc);
+        double s = 0;  // internal force (:137-142)
+  #pragma unroll
+        for (int k = 0; k < 3; ++k) s += vc[k] * sel6(sig, rc_[k]);
+        fe[e * 12 + c] = vol * s;
+  #pragma unroll
+        for (int p = 0; p < 6; ++p) {  // C B, column c (:145-150)
           double t = 0;
-#pragma unroll
-          for (int p = 0; p < 6; ++p) t += br[p] * cb[p];
-          double k = vol * t;
-          if (bx == ax) k += gsg[a];
-          kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+  #pragma unroll
+          for (int k = 0; k < 3; ++k) t += cm[6 * p + rc_[k]] * vc[k];
+          cb[p] = t;
         }
+  #pragma unroll
+        for (int p = 0; p < 6; ++p) finite = finite && isfinite(cb[p]);
+      } else {
+        double bc[6];
+        b_column(grad_s, c, bc);
+        double s = 0;
+  #pragma unroll
+        for (int p = 0; p < 6; ++p) s += bc[p] * sig[p];
+        fe[e * 12 + c] = vol * s;
+  #pragma unroll
+        for (int p = 0; p < 6; ++p) {
+          double t = 0;
+  #pragma unroll
+          for (int q = 0; q < 6; ++q) t += cm[6 * p + q] * bc[q];
+          cb[p] = t;
+        }
+      }
+      if (finite) {
+  #pragma unroll
+        for (int a = 0; a < 4; ++a)
+  #pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            // rows of B column 3a+ax (compile-time after unrolling): ax 0 -> 0,4,5 ...
+            const double gx = g[3 * a + ax];
+            const double h0 = ax == 0 ? g[3 * a + 2] : (ax == 1 ? g[3 * a + 2] : g[3 * a + 1]);
+            const double h1 = ax == 0 ? g[3 * a + 1] : g[3 * a];
+            const int p1 = ax == 0 ? 4 : 3, p2 = ax == 2 ? 4 : 5;
+            double t = 0;  // V B^T C B (:151-157)
+            t += (0.0 + gx) * cb[ax];
+            t += (0.0 + kSqrt2 * (0.0 + 0.5 * h0)) * cb[p1];
+            t += (0.0 + kSqrt2 * (0.0 + 0.5 * h1)) * cb[p2];
+            double k = vol * t;
+            if (bx == ax) k += gsg[a];
+            kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+          }
+      } else {
+  #pragma unroll
+        for (int a = 0; a < 4; ++a)
+  #pragma unroll
+          for (int ax = 0; ax < 3; ++ax) {
+            double br[6];
+            b_column(g, 3 * a + ax, br);
+            double t = 0;
+  #pragma unroll
+            for (int p = 0; p < 6; ++p) t += br[p] * cb[p];
+            double k = vol * t;
+            if (bx == ax) k += gsg[a];
+            kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+          }
+      }
     }
+    __syncthreads();
+    double* out = ke + e0 * 144;
+    for (int i = threadIdx.x; i < n_here * 144; i += kElemThreads)
+      out[i] = s_ke[(i / 144) * kKeStride + i % 144];
   }
-  __syncthreads();
-  double* out = ke + e0 * 144;
-  for (int i = threadIdx.x; i < n_here * 144; i += kElemThreads)
-    out[i] = s_ke[(i / 144) * kKeStride + i % 144];
+  cp_async_wait_all();
 }
 
 // one thread per node pair (A row node, B column node); contrib = e << 4 | a << 2 | b
@@ -319,7 +351,7 @@ struct fibra_assembly {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;
-  int n_tets = 0, n_nodes = 0, n_free = 0;
+  int n_tets = 0, n_nodes = 0, n_free = 0, n_sm = 148;
   long long nnz = 0, n_pairs = 0;
   std::vector<long long> col_ptr;
   std::vector<int> row_idx;
@@ -455,6 +487,7 @@ int fibra_cuda_assembly_create(int device, const int32_t* tets, int32_t n_tets, 
   as->n_pairs = static_cast<long long>(pa.size());
   int rc;
   if (cudaSetDevice(device) != cudaSuccess) { delete as; return FIBRA_E_CUDA; }
+  cudaDeviceGetAttribute(&as->n_sm, cudaDevAttrMultiProcessorCount, device);
   std::vector<int4> t4(n_tets);
   for (int e = 0; e < n_tets; ++e)
     t4[e] = make_int4(tets[4 * e], tets[4 * e + 1], tets[4 * e + 2], tets[4 * e + 3]);
@@ -515,7 +548,8 @@ int fibra_cuda_assemble_device(fibra_assembly* as, const double* coords_dev,
   AS_CUDA(as, cudaMemsetAsync(as->d_nonfinite, 0, sizeof(int), as->stream));
   cudaEventRecord(as->ev[0], as->stream);
   if (as->n_tets) {
-    const unsigned grid = (as->n_tets + kTetsPerCta - 1) / kTetsPerCta;
+    const long long tiles = (as->n_tets + kTetsPerCta - 1) / kTetsPerCta;
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(tiles, 8LL * as->n_sm));
     asm_element_kernel<<<grid, kElemThreads, 0, as->stream>>>(
         as->n_tets, as->d_tets, coords_dev, responses_dev, response_stride, as->d_fe, as->d_ke,
         as->d_err);
