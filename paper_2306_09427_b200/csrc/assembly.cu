@@ -13,11 +13,12 @@
 //   asm_element_kernel: 12 threads per tet (thread r owns row/column r of K_e), 8 tets per
 //     96-thread CTA; the response records (sigma + Mandel C, 42 doubles, any record stride,
 //     e.g. the fibra_point_result array a device solve left in HBM) are staged in shared
-//     memory, K_e is written as 16 contiguous 3x3 node blocks [a][b][ax][bx] so the gather
+//     memory, K_e is written as 16 contiguous 3x3 node blocks [b][a][ax][bx] (column node major) so the gather
 //     reads 72 contiguous bytes per (node pair, element).
-//   asm_pair_kernel: one thread per (row node A, column node B) pair with a free dof on both
-//     sides; it walks the elements shared by A and B in ascending order and writes the (up
-//     to) 9 folded values straight into their compressed-column slots.
+//   asm_pair_kernel: three threads (one per row axis) per (row node A, column node B) pair
+//     with a free dof on both sides; each walks the elements shared by A and B in ascending
+//     order and writes its (up to) 3 folded values straight into their compressed-column
+//     slots.
 //   asm_residual_kernel: one thread per node, the f_e entries of its elements in element
 //     order, then residual -= f_ext (:185).
 // Errors follow the reference's order: the first element (in element order) with a
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kElemThreads, 8)
             t += (0.0 + kSqrt2 * (0.0 + 0.5 * h1)) * cb[p2];
             double k = vol * t;
             if (bx == ax) k += gsg[a];
-            kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+            kb[((b * 4 + a) * 3 + ax) * 3 + bx] = k;
           }
       } else {
   #pragma unroll
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kElemThreads, 8)
             for (int p = 0; p < 6; ++p) t += br[p] * cb[p];
             double k = vol * t;
             if (bx == ax) k += gsg[a];
-            kb[((a * 4 + b) * 3 + ax) * 3 + bx] = k;
+            kb[((b * 4 + a) * 3 + ax) * 3 + bx] = k;
           }
       }
     }
@@ -283,40 +284,42 @@ __global__ void __launch_bounds__(kElemThreads, 8)
   cp_async_wait_all();
 }
 
-// one thread per node pair (A row node, B column node); contrib = e << 4 | a << 2 | b
+// one thread per (node pair, row axis): A row node, B column node, row dof 3 A + ax;
+// contrib = e << 4 | a << 2 | b.  Three threads per pair keep more block loads in flight.
 __global__ void asm_pair_kernel(long long n_pairs, const int* __restrict__ pair_a,
                                 const int* __restrict__ pair_b, const int* __restrict__ pair_rowoff,
                                 const long long* __restrict__ pair_ptr,
                                 const unsigned* __restrict__ contrib, const int* __restrict__ fod,
                                 const long long* __restrict__ col_ptr, const double* __restrict__ ke,
                                 double* __restrict__ values) {
-  const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long p = t / 3;
+  const int ax = static_cast<int>(t % 3);
   if (p >= n_pairs) return;
-  const int A = pair_a[p], B = pair_b[p];
-  double acc[9];
+  const int A = pair_a[p];
+  if (fod[3 * A + ax] < 0) return;
+  const int B = pair_b[p];
   const long long k0 = pair_ptr[p], k1 = pair_ptr[p + 1];
+  double acc[3];
   {
     const unsigned c = contrib[k0];
-    const double* blk = ke + (static_cast<long long>(c >> 4) * 16 + ((c >> 2) & 3) * 4 + (c & 3)) * 9;
+    const double* row = ke + (static_cast<long long>(c >> 4) * 16 + (c & 3) * 4 + ((c >> 2) & 3)) * 9 + 3 * ax;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[i] = blk[i];  // setFromTriplets: the first value as is
+    for (int i = 0; i < 3; ++i) acc[i] = row[i];  // setFromTriplets: the first value as is
   }
   for (long long k = k0 + 1; k < k1; ++k) {
     const unsigned c = contrib[k];
-    const double* blk = ke + (static_cast<long long>(c >> 4) * 16 + ((c >> 2) & 3) * 4 + (c & 3)) * 9;
+    const double* row = ke + (static_cast<long long>(c >> 4) * 16 + (c & 3) * 4 + ((c >> 2) & 3)) * 9 + 3 * ax;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) acc[i] = acc[i] + blk[i];  // collapseDuplicates, triplet order
+    for (int i = 0; i < 3; ++i) acc[i] = acc[i] + row[i];  // collapseDuplicates, triplet order
   }
-  const int fa[3] = {fod[3 * A], fod[3 * A + 1], fod[3 * A + 2]};
-  const int rowoff = pair_rowoff[p];
+  int before = 0;  // free row dofs of A ahead of this one in the column
+  for (int i = 0; i < ax; ++i) before += fod[3 * A + i] >= 0;
+  const long long off = pair_rowoff[p] + before;
 #pragma unroll
   for (int bx = 0; bx < 3; ++bx) {
     const int cf = fod[3 * B + bx];
-    if (cf < 0) continue;
-    long long pos = col_ptr[cf] + rowoff;
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax)
-      if (fa[ax] >= 0) values[pos++] = acc[3 * ax + bx];
+    if (cf >= 0) values[col_ptr[cf] + off] = acc[bx];
   }
 }
 
@@ -557,7 +560,7 @@ int fibra_cuda_assemble_device(fibra_assembly* as, const double* coords_dev,
   }
   cudaEventRecord(as->ev[1], as->stream);
   if (as->n_pairs) {
-    asm_pair_kernel<<<static_cast<unsigned>((as->n_pairs + 255) / 256), 256, 0, as->stream>>>(
+    asm_pair_kernel<<<static_cast<unsigned>((3 * as->n_pairs + 255) / 256), 256, 0, as->stream>>>(
         as->n_pairs, as->d_pair_a, as->d_pair_b, as->d_pair_rowoff, as->d_pair_ptr,
         as->d_contrib, as->d_fod, as->d_col_ptr, as->d_ke, values_dev);
     AS_CUDA(as, cudaGetLastError());
