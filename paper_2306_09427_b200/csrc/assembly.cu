@@ -135,7 +135,9 @@ __global__ void __launch_bounds__(kElemThreads, 8)
   __shared__ double s_x[2][kTetsPerCta][12];
   __shared__ double s_geo[kTetsPerCta][14];  // grad[4][3], volume, finite flag
   __shared__ double s_ke[kTetsPerCta * kKeStride];
+  __shared__ int s_cbad[2][kTetsPerCta];  // per stage: some C entry of the tet is not finite
   const int le = threadIdx.x / 12, r = threadIdx.x % 12;
+  if (threadIdx.x < 2 * kTetsPerCta) s_cbad[threadIdx.x / kTetsPerCta][threadIdx.x % kTetsPerCta] = 0;
   const long long n_tiles = (static_cast<long long>(n_tets) + kTetsPerCta - 1) / kTetsPerCta;
   const long long step = gridDim.x;
   // thread (le, r) fetches coordinate r % 3 of tet node r / 3
@@ -168,6 +170,9 @@ __global__ void __launch_bounds__(kElemThreads, 8)
     const bool live = le < n_here;
     const double* sg = s_resp[st][le];  // SymTensor3 xx yy zz yz xz xy, then Mandel66
     const double* cm = sg + 6;
+    if (r == 0) s_cbad[st ^ 1][le] = 0;  // next tile's flags (read after two barriers)
+    if (live && !(isfinite(cm[r]) && isfinite(cm[r + 12]) && isfinite(cm[r + 24])))
+      s_cbad[st][le] = 1;
     if (live && r == 0) {  // b_matrix once per element, then the error order of :118-132
       double grad[12], vol;
       const double det = tet_geom(s_x[st][le], grad, &vol);
@@ -180,9 +185,7 @@ __global__ void __launch_bounds__(kElemThreads, 8)
       for (int i = 0; i < 6; ++i) fin = fin && isfinite(m[i]);
       const int code = !fin ? FIBRA_E_ASM_STRESS : (!(det > 0) ? FIBRA_E_KINEMATICS : 0);
       if (code) atomicMin(err, (static_cast<unsigned long long>(e) << 8) | code);
-      bool cfin = fin;  // sigma and C finite: the structural-zero skip below is exact
-      for (int i = 0; i < 36; ++i) cfin = cfin && isfinite(cm[i]);
-      s_geo[le][13] = cfin ? 1.0 : 0.0;
+      s_geo[le][13] = fin ? 1.0 : 0.0;  // sigma finite (C: s_cbad, after the barrier)
     }
     __syncthreads();
     // thread r owns column c = r = 3 b + bx of K_e: (C B)[:, c] stays in registers and the
@@ -208,7 +211,8 @@ __global__ void __launch_bounds__(kElemThreads, 8)
           for (int q = 0; q < 3; ++q) t += g[3 * a + p] * sf[3 * p + q] * gb[q];
         gsg[a] = t * vol;
       }
-      bool finite = grad_s[13] != 0.0;
+      // sigma and C finite: the structural-zero skip below is exact
+    bool finite = grad_s[13] != 0.0 && !s_cbad[st][le];
       double cb[6];
       if (finite) {  // structural zeros of B skipped (exact, see b_column_sparse)
         int rc_[3];
