@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kElemThreads, 8)
   __shared__ double s_resp[2][kTetsPerCta][42];
   __shared__ double s_x[2][kTetsPerCta][12];
   __shared__ double s_geo[kTetsPerCta][14];  // grad[4][3], volume, finite flag
-  __shared__ double s_ke[kTetsPerCta * kKeStride];
+  __shared__ __align__(16) double s_ke[kTetsPerCta * kKeStride];
   __shared__ int s_cbad[2][kTetsPerCta];  // per stage: some C entry of the tet is not finite
   const int le = threadIdx.x / 12, r = threadIdx.x % 12;
   if (threadIdx.x < 2 * kTetsPerCta) s_cbad[threadIdx.x / kTetsPerCta][threadIdx.x % kTetsPerCta] = 0;
@@ -281,9 +281,10 @@ __global__ void __launch_bounds__(kElemThreads, 8)
       }
     }
     __syncthreads();
-    double* out = ke + e0 * 144;
-    for (int i = threadIdx.x; i < n_here * 144; i += kElemThreads)
-      out[i] = s_ke[(i / 144) * kKeStride + i % 144];
+    // 16-byte copy-out: K_e rows are 1152 B in HBM, 1168 B (padded) in shared memory
+    double2* out = reinterpret_cast<double2*>(ke + e0 * 144);
+    for (int i = threadIdx.x; i < n_here * 72; i += kElemThreads)
+      out[i] = *reinterpret_cast<const double2*>(&s_ke[(i / 72) * kKeStride + 2 * (i % 72)]);
   }
   cp_async_wait_all();
 }
