@@ -25,9 +25,12 @@ Headline line (rank 0, one JSON line):
   roofline FP64-pipe ops of the DR kernel / its event time vs the FP64 pipe peak measured
            on this device (fibra_cuda_fp64_peak)
   cpu_baseline  the reference's own compiled DR (oracle/_ref) on the host cores, bounded
-           sample of the same workload.
+           sample of the same workload; "single_rve" = the 1-core, best-of-3 config-1 rate
+           at lambda = 1.05 and 1.25 (the >= 1000x denominator).
 --impl reference times only that CPU implementation (all host threads) and prints the same
-metric line with "impl": "reference".
+metric line with "impl": "reference" and the same "config".  It imports nothing from the
+product package: the network comes from the reference's own generator (oracle/_ref) and F
+from oracle/workload.py; its timed steps together solve every point of the config-2 batch.
 """
 from __future__ import annotations
 
@@ -108,9 +111,65 @@ def workload(args, world, rank):
     return nets, np.arange(hi - lo, dtype=np.int32), F, desc, total, "strong"
 
 
+def describe(args, world, n_per_gpu, total, scaling, n_free):
+    """Workload description and the `config` dict, shared verbatim by both arms."""
+    if args.config == 2:
+        desc = (f"config{5 if args.tangent else 2}: {n_per_gpu} same-topology knn RVEs per GPU "
+                f"(375 nodes/1000 fibers, seed {NET_SEED}, n_free {n_free}), distinct F "
+                f"(mt19937_64(55) recipe), "
+                f"{'base + 6 probes + tangent' if args.tangent else 'stress only'}")
+    else:
+        kind = {3: "heterogeneous knn RVEs of 500-5k fibers (SURVEY 8d recipe, one network per point)",
+                4: "jittered-lattice RVEs of 50k fibers / 12,167 nodes (16-CTA clusters)",
+                5: "config-3 RVEs (first 4,096), base + 6 warm probes + tangent"}[args.config]
+        desc = (f"config{args.config}: {total} {kind}, distinct F (mt19937_64(55) recipe), "
+                f"fiber-weighted contiguous shards")
+    cfg = {"workload": desc, "points_per_gpu": n_per_gpu, "global_points": total,
+           "l2": "flushed between timed steps (256 MiB device write)",
+           "parallelism": f"dp{world} (independent RVE shards, 1 NCCL all-gather "
+                          "of result records per step)"}
+    return desc, cfg
+
+
 def sample_points(n, sample):
     """Bounded CPU sample: evenly spaced points of the shard (all of them when small)."""
     return np.unique(np.linspace(0, n - 1, min(n, sample)).astype(int))
+
+
+def step_slices(n, steps, min_size):
+    """Point slices of the CPU reference run: a fixed interleaving permutation of the n points
+    (stride coprime with n, so every slice mixes cheap and capped solves), cut into `steps`
+    consecutive slices of max(ceil(n / steps), min_size) points, wrapping around: over the
+    timed steps every point of the batch is solved at least once."""
+    stride = next(s for s in range(int(n * 0.618) | 1, 2 * n + 2) if np.gcd(s, n) == 1)
+    perm = (np.arange(n) * stride) % n
+    size = max(-(-n // steps), min(min_size, n))
+    return [perm[(k * size + np.arange(size)) % n] for k in range(steps)]
+
+
+def single_rve_baseline():
+    """BASELINE.md 4.2 denominator: the reference's relax_solve + homogenized_stress
+    (oracle/_ref, relax.cpp:93-191, network.cpp:341-372) on ONE core, best of 3, for the
+    config-1 network (knn 375/1000, seed 1) at F = diag(lambda, 1, 1), lambda = 1.05 and 1.25."""
+    import oracle as O
+    from oracle import workload as W
+    if not O.ref_available():
+        return None
+    rnet = O.ref_generate(seed=W.NET_SEED, **W.CONFIG1_KNN)
+    out = {"cores": 1, "kind": "reference", "network": "knn 375 nodes/1000 fibers seed 1",
+           "repeats": "best of 3"}
+    for lam in (1.05, 1.25):
+        F = np.diag([lam, 1.0, 1.0])
+        best, its = float("inf"), 0
+        for _ in range(3):
+            t0 = time.perf_counter()
+            st, rep = O.ref_relax_solve(rnet, F)
+            O.ref_homogenized_stress(rnet, st, F)
+            best = min(best, time.perf_counter() - t0)
+            its = rep["iterations"]
+        out[f"lambda_{lam}"] = {"solves_per_s": 1.0 / best, "seconds": best, "iterations": its,
+                                "ns_per_fiber_iteration": best / (its * rnet.n_fibers) * 1e9}
+    return out
 
 
 def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
@@ -118,18 +177,14 @@ def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
     oracle/_ref (the reference's own translation units) for the headline config 2, else the
     oracle restatement.  Returns (rve_solves_per_s, kind, seconds, iterations, n_sampled)."""
     import oracle as O
-    from paper_2306_09427_b200.synth import config1_spec
+    from oracle import workload as W
     idx = sample_points(len(F), sample)  # evenly spaced: iteration counts are heavy-tailed
     if args.config == 2 and O.ref_available() and not args.tangent:
-        Fs = F[idx]
-        spec = config1_spec()
-        rnet = O.ref_generate("knn", nodes=spec.nodes, fibers=spec.fibers,
-                              neighbors=spec.neighbors, merge_radius=spec.merge_radius,
-                              seed=NET_SEED)
+        rnet = O.ref_generate(seed=W.NET_SEED, **W.CONFIG1_KNN)
         t0 = time.perf_counter()
-        sig, iters, status = O.ref_batch_stress(rnet, Fs, workers=n_workers)
+        sig, iters, status = O.ref_batch_stress(rnet, F[idx], workers=n_workers)
         dt = time.perf_counter() - t0
-        return len(Fs) / dt, "reference", dt, int(iters.sum()), len(Fs)
+        return len(idx) / dt, "reference", dt, int(iters.sum()), len(idx)
     O.build(ref=False)
     used = sorted({int(eop[i]) for i in idx})
     remap = {e: k for k, e in enumerate(used)}
@@ -145,34 +200,68 @@ def cpu_sample_rate(args, nets, eop, F, n_workers, sample):
 
 
 def run_reference(args, rank, world):
+    """The reference's own CPU implementation of the path on this box's host cores.
+
+    Config 2 (the headline): the network comes from the reference's own generator and every
+    DR solve from the reference's compiled relax_solve / homogenized_stress (oracle/_ref,
+    WorkerPool over all host threads); the F recipe from oracle/workload.py.  Nothing of the
+    product package is imported.  The timed steps together cover the whole config-2 batch
+    of GPU shard 0 (1,024 points), so the rate is over the same points the GPU arm solves.
+    Configs 3-5 (builder runs only) time the oracle port on the product's networks."""
     if rank != 0:
         return
+    import oracle as O
+    from oracle import workload as W
     n_workers = os.cpu_count() or 1
-    import paper_2306_09427_b200  # noqa: F401  (network generator only; no GPU use)
-    nets, eop, F, desc, total, scaling = workload(args, 1, 0)
-    sample = max(8, 4 * n_workers)  # >> threads: the heavy tail must not idle the pool
-    for _ in range(max(1, min(args.warmup, 1))):
-        cpu_sample_rate(args, nets, eop, F, n_workers, min(sample, n_workers))
-    secs, iters, done = 0.0, 0, 0
-    kind = "port"
-    for _ in range(args.steps):
-        r, kind, dt, its, k = cpu_sample_rate(args, nets, eop, F, n_workers, sample)
-        secs += dt
-        iters += its
-        done += k
+    if args.config == 2 and O.ref_available() and not args.tangent:
+        rnet = O.ref_generate(seed=W.NET_SEED, **W.CONFIG1_KNN)
+        n = args.points
+        F = np.ascontiguousarray(W.batch_F(n * world)[:n]).reshape(n, 9)
+        desc, cfg = describe(args, world, n, n * world, "weak", rnet.n_free)
+        scaling = "weak"
+        slices = step_slices(n, args.steps, 2 * n_workers)
+        if args.warmup > 0:
+            O.ref_batch_stress(rnet, F[slices[0][:n_workers]], workers=n_workers)
+        secs, iters, done, covered = 0.0, 0, 0, set()
+        for sl in slices:
+            t0 = time.perf_counter()
+            _, its, _ = O.ref_batch_stress(rnet, F[sl], workers=n_workers)
+            secs += time.perf_counter() - t0
+            iters += int(its.sum())
+            done += len(sl)
+            covered.update(int(p) for p in sl)
+        kind = "reference"
+        assert "paper_2306_09427_b200" not in sys.modules  # reference arm: no product code
+        sample = (f"all {len(covered)} of {n} points of GPU shard 0 across the {args.steps} "
+                  f"timed steps ({done // args.steps} interleaved points per step), "
+                  f"{n_workers} WorkerPool threads")
+    else:
+        import paper_2306_09427_b200  # noqa: F401  (configs 3-5: the product's host generator)
+        nets, eop, F, _, total, scaling = workload(args, 1, 0)
+        desc, cfg = describe(args, world, len(F), total, scaling, None)
+        sample = max(8, 4 * n_workers)
+        secs, iters, done = 0.0, 0, 0
+        kind = "port"
+        for _ in range(args.steps):
+            r, kind, dt, its, k = cpu_sample_rate(args, nets, eop, F, n_workers, sample)
+            secs += dt
+            iters += its
+            done += k
+        sample = (f"evenly spaced {done // args.steps} points of the workload per step, "
+                  f"{n_workers} threads")
     value = done / secs
-    which = "evenly spaced"
     line = {"impl": "reference", "metric": METRICS[args.config], "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "sample_points_per_step": done // args.steps},
+            "config": cfg,
             "dr_iter_rve_per_s": iters / secs,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_workers, "kind": kind,
-                             "sample": f"{which} {done // args.steps} points of the workload per "
-                                       f"step, {n_workers} WorkerPool threads"},
+                             "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    if args.config == 2 and not args.no_cpu_baseline:
+        line["cpu_baseline"]["single_rve"] = single_rve_baseline()
     print(json.dumps(line), flush=True)
 
 
@@ -349,10 +438,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "points_per_gpu": n, "global_points": total,
-                       "l2": "flushed between timed steps (256 MiB device write)",
-                       "parallelism": f"dp{world} (independent RVE shards, 1 NCCL all-gather "
-                                      "of result records per step)"},
+            "config": describe(args, world, n, total, scaling,
+                               nets[0].n_free if args.config == 2 else None)[1],
             "dr_iter_rve_per_s": all_iters / (max_total_ms * 1e-3) * (args.steps / args.steps),
             "failed_points": failed,
             "roofline": {"bound": "fp64_pipe", "achieved": achieved / 1e9, "peak": peak / 1e9,
@@ -382,6 +469,9 @@ def main():
                                     "sample": f"{which} {k} points of this workload on "
                                               f"{nw} host threads ({secs:.1f} s, {its} DR "
                                               "iterations)"}
+            single = single_rve_baseline()
+            if single is not None:
+                line["cpu_baseline"]["single_rve"] = single
         print(json.dumps(line), flush=True)
     db.close()
     if world > 1:

@@ -118,6 +118,7 @@ def lib():
                                         C.POINTER(CLaw), _dp, C.POINTER(CRelaxCfg), C.c_double,
                                         C.c_int, C.c_int, C.c_int, C.POINTER(CResponse), _ip]
         L.or_polar_decompose.argtypes = [_dp, _dp, _dp]
+        L.or_eigen_sym3.argtypes = [_dp, _dp, _dp]
         L.or_pull_back_stress.argtypes = [_dp, _dp, _dp]
         L.or_push_forward_stiffness.argtypes = [_dp, _dp, _dp]
         L.or_material_stiffness_from_probes.argtypes = [_dp, _dp, _dp, C.c_double, _dp]
@@ -287,6 +288,18 @@ def polar_decompose(F):
     if rc:
         raise OracleError(rc, "polar")
     return R.reshape(3, 3), U
+
+
+def eigen_sym3(A):
+    """Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d> restatement: (eigenvalues ascending,
+    eigenvector columns)."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.float64).reshape(9))
+    lam = np.zeros(3)
+    Q = np.zeros(9)
+    rc = lib().or_eigen_sym3(_ptr(A, _dp), _ptr(lam, _dp), _ptr(Q, _dp))
+    if rc:
+        raise OracleError(7, "eigen_sym3 NoConvergence")
+    return lam, Q.reshape(3, 3)
 
 
 def norm2_sq(x):

@@ -341,81 +341,237 @@ int or_pull_back_stress(const double sig[6], const double f[9], double out[6]) {
   return OR_OK;
 }
 
-/* Symmetric 3x3 eigensolver (cyclic Jacobi).  RESTATEMENT of the Eigen
- * SelfAdjointEigenSolver call in polar_decompose tensor.cpp:208-215; Eigen's bits are
- * not reproducible here (Eigen absent), parity across that boundary is tolerance-only.
- * The device solver (csrc/tensor.cuh) runs the identical sequence of IEEE operations. */
-static void jacobi3(double a[9], double q[9]) {
-  for (int i = 0; i < 9; ++i) q[i] = (i % 4 == 0) ? 1.0 : 0.0;
-  static const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    int rotated = 0;
-    for (int r = 0; r < 3; ++r) {
-      const int p = P[r], qq = Q[r];
-      const double apq = a[3 * p + qq];
-      const double app = a[3 * p + p], aqq = a[3 * qq + qq];
-      if (fabs(apq) <= 1e-18 * (fabs(app) + fabs(aqq))) {
-        a[3 * p + qq] = a[3 * qq + p] = 0.0;
-        continue;
+/* ------------------------------------------------------------------------- */
+/* Eigen 3.4.0 pieces on the hot path (RESTATEMENT of the published library)  */
+/* ------------------------------------------------------------------------- */
+/* The reference builds tensor.cpp / stiffness.cpp against the system Eigen
+ * (CMakeLists.txt:34, /usr/include/eigen3), which is absent here.  We pin Eigen 3.4.0
+ * (the Ubuntu 24.04 libeigen3-dev package this image's toolchain matches) at the
+ * reference's compile flags: -O3 -ffp-contract=off, no -march, so x86-64 SSE2 only
+ * (Packet2d, EIGEN_UNALIGNED_VECTORIZE=1, no FMA), and restate, operation by
+ * operation, what that build executes:
+ *   - Matrix3d products (CoeffBasedProductMode, lazy product evaluator,
+ *     Eigen/src/Core/ProductEvaluators.h + AssignEvaluator.h): a column-major 3x3
+ *     result whose product evaluator has packet access (column-major lhs) is assigned
+ *     by SliceVectorizedTraversal with InnerUnrolling: rows 0-1 of every column as one
+ *     Packet2d, accumulated ((l0*r0 + l1*r1) + l2*r2) (etor_product_packet_impl), row 2
+ *     through coeff() = (lhs.row(2)' .* rhs.col(j)).sum(), whose strided operands give a
+ *     non-vectorized redux, redux_novec_unroller's halving order l0*r0 + (l1*r1 + l2*r2).
+ *     Without packet access (F^T F: row-major lhs, column-major rhs) every coefficient
+ *     goes through coeff(), and there the operands are contiguous, so the redux is
+ *     LinearVectorized: predux(packet(0,1)) + x2 = (x0 + x1) + x2.
+ *   - SelfAdjointEigenSolver<Matrix3d>::compute (Eigenvalues/SelfAdjointEigenSolver.h):
+ *     lower triangle scaled by its max |entry|; tridiagonalization_inplace_selector<...,3,
+ *     false> (Eigenvalues/Tridiagonalization.h, closed-form Householder);
+ *     computeFromTridiagonal_impl (deflation |s| < DBL_MIN or (s/eps)^2 <= |d_i|+|d_i+1|,
+ *     30*n iteration cap) with tridiagonal_qr_step (Wilkinson shift via numext::hypot,
+ *     JacobiRotation::makeGivens, Q.applyOnTheRight(k, k+1, G)), then the selection sort
+ *     of the eigenvalues (first minimum) with their columns; eigenvalues *= scale.
+ *   - FullPivLU<Matrix<double,6,6>> (LU/FullPivLU.h): computeInPlace as in the previous
+ *     restatement; _solve_impl with c = RhsType::PlainObject, which for the reference's
+ *     rhs pe.transpose() is ROW-major, so both triangular solves go through
+ *     triangular_solve_matrix<..., RowMajor other> = the OnTheRight kernel on the
+ *     transposed problem (Core/products/TriangularSolverMatrix.h) with SmallPanelWidth =
+ *     max(mr, nr) = 4 (gebp_traits<double,double>, SSE2: nr = 4, mr = 2*2) and one
+ *     kc = 6 block: panels of 4 and 2 columns, the off-panel part through gebp (an
+ *     accumulator started at +0.0, depth in ascending order, then r + (-1)*acc), the
+ *     in-panel part left-looking (r -= x_k * t_kj, k ascending), the non-unit diagonal
+ *     applied as r *= 1/t_jj.
+ * Nothing in the reference's tests pins Eigen's bits, so this is "parity by
+ * restatement"; csrc/tensor.cuh executes the identical sequence on the device. */
+
+/* R = L * Rh for 3x3 (row-major storage of the math matrices) as the reference's
+ * Matrix3d product assignment evaluates it (see above): rows 0-1 left fold, row 2
+ * l0 + (l1 + l2). */
+static void eig_prod3_slice(const double l[9], const double r[9], double out[9]) {
+  for (int j = 0; j < 3; ++j) {
+    for (int i = 0; i < 2; ++i)
+      out[3 * i + j] = (l[3 * i] * r[j] + l[3 * i + 1] * r[3 + j]) + l[3 * i + 2] * r[6 + j];
+    out[6 + j] = l[6] * r[j] + (l[7] * r[3 + j] + l[8] * r[6 + j]);
+  }
+}
+
+static double eig_hypot(double x, double y) { /* MathFunctionsImpl.h positive_real_hypot */
+  x = fabs(x);
+  y = fabs(y);
+  if (isinf(x) || isinf(y)) return INFINITY;
+  if (isnan(x) || isnan(y)) return NAN;
+  const double p = smax(x, y);
+  if (p == 0.0) return 0.0;
+  const double qp = smin(y, x) / p;
+  return p * sqrt(1.0 + qp * qp);
+}
+
+/* JacobiRotation<double>::makeGivens(p, q) (Jacobi/Jacobi.h, real case) */
+static void eig_make_givens(double p, double q, double* c, double* s) {
+  if (q == 0.0) {
+    *c = p < 0.0 ? -1.0 : 1.0;
+    *s = 0.0;
+  } else if (p == 0.0) {
+    *c = 0.0;
+    *s = q < 0.0 ? 1.0 : -1.0;
+  } else if (fabs(p) > fabs(q)) {
+    const double t = q / p;
+    double u = sqrt(1.0 + t * t);
+    if (p < 0.0) u = -u;
+    *c = 1.0 / u;
+    *s = -t * *c;
+  } else {
+    const double t = p / q;
+    double u = sqrt(1.0 + t * t);
+    if (q < 0.0) u = -u;
+    *s = -1.0 / u;
+    *c = -t * *s;
+  }
+}
+
+/* tridiagonal_qr_step<ColMajor> (Eigenvalues/SelfAdjointEigenSolver.h) on n = 3 */
+static void eig_qr_step(double diag[3], double sub[2], int start, int end, double q[9]) {
+  const double td = (diag[end - 1] - diag[end]) * 0.5;
+  const double e = sub[end - 1];
+  double mu = diag[end];
+  if (td == 0.0) {
+    mu -= fabs(e);
+  } else if (e != 0.0) {
+    const double e2 = e * e;
+    const double h = eig_hypot(td, e);
+    if (e2 == 0.0)
+      mu -= e / ((td + (td > 0.0 ? h : -h)) / e);
+    else
+      mu -= e2 / (td + (td > 0.0 ? h : -h));
+  }
+  double x = diag[start] - mu;
+  double z = sub[start];
+  for (int k = start; k < end && z != 0.0; ++k) {
+    double c, s;
+    eig_make_givens(x, z, &c, &s);
+    const double sdk = s * diag[k] + c * sub[k];
+    const double dkp1 = s * sub[k] + c * diag[k + 1];
+    diag[k] = c * (c * diag[k] - s * sub[k]) - s * (c * sub[k] - s * diag[k + 1]);
+    diag[k + 1] = s * sdk + c * dkp1;
+    sub[k] = c * sdk - s * dkp1;
+    if (k > start) sub[k - 1] = c * sub[k - 1] - s * z;
+    x = sub[k];
+    if (k < end - 1) {
+      z = -s * sub[k + 1];
+      sub[k + 1] = c * sub[k + 1];
+    }
+    /* q.applyOnTheRight(k, k+1, rot): apply_rotation_in_the_plane(col k, col k+1,
+     * rot.transpose() = (c, -s)): x' = c*x + (-s)*y, y' = s*x + c*y */
+    if (!(c == 1.0 && -s == 0.0))
+      for (int i = 0; i < 3; ++i) {
+        const double xi = q[3 * i + k], yi = q[3 * i + k + 1];
+        q[3 * i + k] = c * xi + (-s) * yi;
+        q[3 * i + k + 1] = s * xi + c * yi;
       }
-      rotated = 1;
-      const double tau = (aqq - app) / (2.0 * apq);
-      const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                  : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-      const double c = 1.0 / sqrt(1.0 + t * t);
-      const double s = t * c;
-      a[3 * p + p] = app - t * apq;
-      a[3 * qq + qq] = aqq + t * apq;
-      a[3 * p + qq] = a[3 * qq + p] = 0.0;
-      const int o = 3 - p - qq;
-      const double arp = a[3 * o + p], arq = a[3 * o + qq];
-      a[3 * o + p] = a[3 * p + o] = c * arp - s * arq;
-      a[3 * o + qq] = a[3 * qq + o] = s * arp + c * arq;
-      for (int k = 0; k < 3; ++k) {
-        const double qkp = q[3 * k + p], qkq = q[3 * k + qq];
-        q[3 * k + p] = c * qkp - s * qkq;
-        q[3 * k + qq] = s * qkp + c * qkq;
+  }
+}
+
+/* SelfAdjointEigenSolver<Matrix3d>(a, ComputeEigenvectors): eigenvalues ascending in
+ * lam, eigenvectors as the columns of q.  Returns 0 on Success, 1 on NoConvergence. */
+int or_eigen_sym3(const double a[9], double lam[3], double q[9]) {
+  double m[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[3 * i + j] = (j <= i) ? a[3 * i + j] : 0.0;
+  double scale = 0.0;
+  for (int k = 0; k < 9; ++k) scale = smax(scale, fabs(m[k])); /* cwiseAbs().maxCoeff() */
+  if (scale == 0.0) scale = 1.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j <= i; ++j) m[3 * i + j] /= scale;
+  /* tridiagonalization_inplace_selector<MatrixType, 3, false>::run */
+  double diag[3], sub[2];
+  diag[0] = m[0];
+  const double v1norm2 = m[6] * m[6];
+  if (v1norm2 <= DBL_MIN) {
+    diag[1] = m[4];
+    diag[2] = m[8];
+    sub[0] = m[3];
+    sub[1] = m[7];
+    for (int k = 0; k < 9; ++k) q[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  } else {
+    const double beta = sqrt(m[3] * m[3] + v1norm2);
+    const double inv_beta = 1.0 / beta;
+    const double m01 = m[3] * inv_beta;
+    const double m02 = m[6] * inv_beta;
+    const double qq = 2.0 * m01 * m[7] + m02 * (m[8] - m[4]);
+    diag[1] = m[4] + m02 * qq;
+    diag[2] = m[8] - m02 * qq;
+    sub[0] = beta;
+    sub[1] = m[7] - m01 * qq;
+    const double qm[9] = {1, 0, 0, 0, m01, m02, 0, m02, -m01};
+    memcpy(q, qm, sizeof qm);
+  }
+  /* computeFromTridiagonal_impl(diag, subdiag, m_maxIterations = 30, true, eivec) */
+  const double consider_as_zero = DBL_MIN;
+  const double precision_inv = 1.0 / DBL_EPSILON;
+  int end = 2, start = 0, iter = 0;
+  while (end > 0) {
+    for (int i = start; i < end; ++i) {
+      if (fabs(sub[i]) < consider_as_zero) {
+        sub[i] = 0.0;
+      } else {
+        const double scaled = precision_inv * sub[i];
+        if (scaled * scaled <= (fabs(diag[i]) + fabs(diag[i + 1]))) sub[i] = 0.0;
       }
     }
-    if (!rotated) break;
+    while (end > 0 && sub[end - 1] == 0.0) end--;
+    if (end <= 0) break;
+    iter++;
+    if (iter > 30 * 3) break;
+    start = end - 1;
+    while (start > 0 && sub[start - 1] != 0.0) start--;
+    eig_qr_step(diag, sub, start, end, q);
   }
+  if (iter > 30 * 3) return 1; /* NoConvergence */
+  for (int i = 0; i < 2; ++i) { /* sort: diag.segment(i, n-i).minCoeff(&k) */
+    int k = 0;
+    for (int t = 1; t < 3 - i; ++t)
+      if (diag[i + t] < diag[i + k]) k = t;
+    if (k > 0) {
+      const double d = diag[i];
+      diag[i] = diag[k + i];
+      diag[k + i] = d;
+      for (int r = 0; r < 3; ++r) {
+        const double v = q[3 * r + i];
+        q[3 * r + i] = q[3 * r + k + i];
+        q[3 * r + k + i] = v;
+      }
+    }
+  }
+  for (int k = 0; k < 3; ++k) lam[k] = diag[k] * scale;
+  return 0;
 }
 
 int or_polar_decompose(const double f[9], double rot[9], double u6[6]) {
   /* tensor.cpp:203-224 */
   const double j = or_det(f);
   if (!(j > 0.0)) return OR_KINEMATICS;
-  double ft[9], c[9], q[9];
-  transpose3(f, ft);
-  or_matmul(ft, f, c);
-  jacobi3(c, q);
-  double lam[3] = {c[0], c[4], c[8]};
-  if (lam[0] <= 0.0 || lam[1] <= 0.0 || lam[2] <= 0.0) return OR_KINEMATICS;
+  double c[9];
+  for (int i = 0; i < 3; ++i) /* fe.transpose() * fe: every coefficient via coeff() */
+    for (int jj = 0; jj < 3; ++jj)
+      c[3 * i + jj] = (f[i] * f[jj] + f[3 + i] * f[3 + jj]) + f[6 + i] * f[6 + jj];
+  double lam[3], q[9];
+  if (or_eigen_sym3(c, lam, q)) return OR_KINEMATICS; /* es.info() != Success */
+  if (smin(smin(lam[0], lam[1]), lam[2]) <= 0.0) return OR_KINEMATICS;
   double sq[3], isq[3];
-  for (int k = 0; k < 3; ++k) {
-    sq[k] = sqrt(lam[k]);
-    isq[k] = 1.0 / sq[k];
-  }
-  double u[9], uinv[9];
+  for (int k = 0; k < 3; ++k) sq[k] = sqrt(lam[k]);
+  for (int k = 0; k < 3; ++k) isq[k] = 1.0 / sq[k]; /* sq.cwiseInverse() */
+  double qd[9], qdi[9], qt[9], u[9], uinv[9];
   for (int i = 0; i < 3; ++i)
-    for (int jj = 0; jj < 3; ++jj) {
-      double s = 0, si = 0;
-      for (int k = 0; k < 3; ++k) {
-        s += (q[3 * i + k] * sq[k]) * q[3 * jj + k];
-        si += (q[3 * i + k] * isq[k]) * q[3 * jj + k];
-      }
-      u[3 * i + jj] = s;
-      uinv[3 * i + jj] = si;
+    for (int k = 0; k < 3; ++k) {
+      qd[3 * i + k] = q[3 * i + k] * sq[k]; /* q * sq.asDiagonal() */
+      qdi[3 * i + k] = q[3 * i + k] * isq[k];
+      qt[3 * k + i] = q[3 * i + k];
     }
-  or_matmul(f, uinv, rot);
+  eig_prod3_slice(qd, qt, u);
+  eig_prod3_slice(qdi, qt, uinv);
+  eig_prod3_slice(f, uinv, rot); /* fe * uinv */
   or_sym_from_full(u, u6);
   return OR_OK;
 }
 
-/* 6x6 full-pivot LU solve of ([M][T])^T [A]^T = [P]^T.  RESTATEMENT of
- * Eigen::FullPivLU (stiffness.cpp:26-39): largest |entry| pivot of the trailing block
- * (first in column-major scan), rank threshold |pivot| > 6*eps*max|pivot|, forward
- * then backward substitution, column permutation undone last. */
+/* 6x6 full-pivot LU solve of ([M][T])^T [A]^T = [P]^T: Eigen::FullPivLU (stiffness.cpp:
+ * 26-39), computeInPlace + _solve_impl as described above. */
 static int fullpiv_solve6(const double a_in[36], const double rhs[36], double x[36]) {
   double lu[36], c[36];
   int rt[6], ct[6];
@@ -425,7 +581,7 @@ static int fullpiv_solve6(const double a_in[36], const double rhs[36], double x[
   for (int k = 0; k < 6; ++k) {
     double big = -1.0;
     int br = k, bc = k;
-    for (int jj = k; jj < 6; ++jj)
+    for (int jj = k; jj < 6; ++jj) /* maxCoeff(&row, &col): column-major scan, first max */
       for (int i = k; i < 6; ++i) {
         const double v = fabs(lu[6 * i + jj]);
         if (v > big) { big = v; br = i; bc = jj; }
@@ -445,7 +601,7 @@ static int fullpiv_solve6(const double a_in[36], const double rhs[36], double x[
     if (k < 5) {
       const double piv = lu[6 * k + k];
       for (int i = k + 1; i < 6; ++i) lu[6 * i + k] /= piv;
-      for (int jj = k + 1; jj < 6; ++jj)
+      for (int jj = k + 1; jj < 6; ++jj) /* outer product, column by column */
         for (int i = k + 1; i < 6; ++i) lu[6 * i + jj] -= lu[6 * i + k] * lu[6 * k + jj];
     }
   }
@@ -454,18 +610,37 @@ static int fullpiv_solve6(const double a_in[36], const double rhs[36], double x[
   for (int i = 0; i < nonzero; ++i) rank += fabs(lu[6 * i + i]) > thr;
   if (rank != 6) return OR_SINGULAR;
   memcpy(c, rhs, sizeof c);
-  for (int k = 0; k < 6; ++k)
+  for (int k = 0; k < 6; ++k) /* c = P * rhs */
     if (rt[k] != k)
       for (int jj = 0; jj < 6; ++jj) { double t = c[6 * k + jj]; c[6 * k + jj] = c[6 * rt[k] + jj]; c[6 * rt[k] + jj] = t; }
-  for (int jj = 0; jj < 6; ++jj) {
-    for (int k = 0; k < 6; ++k)          /* unit lower, column oriented */
-      for (int i = k + 1; i < 6; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
-    for (int k = 5; k >= 0; --k) {       /* upper, column oriented */
-      c[6 * k + jj] /= lu[6 * k + k];
-      for (int i = 0; i < k; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
+  for (int jj = 0; jj < 6; ++jj) { /* every rhs column independently (one "row" of c^T) */
+    double* y = c + jj; /* y[6 * i] = c(i, jj) */
+    /* L y = c, unit lower: panel rows 0-3 left-looking, rows 4-5 = gebp over 0-3, then
+     * the 2-row panel */
+    for (int i = 1; i < 4; ++i)
+      for (int k = 0; k < i; ++k) y[6 * i] -= y[6 * k] * lu[6 * i + k];
+    for (int i = 4; i < 6; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < 4; ++k) acc = acc + y[6 * k] * lu[6 * i + k];
+      y[6 * i] = y[6 * i] + (-1.0) * acc;
+    }
+    y[6 * 5] -= y[6 * 4] * lu[6 * 5 + 4];
+    /* U x = y: panel rows 4-5 first (5, then 4), rows 0-3 = gebp over 4-5, then the
+     * 4-row panel bottom up, left-looking over the rows already solved in it */
+    y[6 * 5] *= 1.0 / lu[6 * 5 + 5];
+    y[6 * 4] -= y[6 * 5] * lu[6 * 4 + 5];
+    y[6 * 4] *= 1.0 / lu[6 * 4 + 4];
+    for (int i = 0; i < 4; ++i) {
+      double acc = 0.0;
+      for (int k = 4; k < 6; ++k) acc = acc + y[6 * k] * lu[6 * i + k];
+      y[6 * i] = y[6 * i] + (-1.0) * acc;
+    }
+    for (int i = 3; i >= 0; --i) {
+      for (int k = i + 1; k < 4; ++k) y[6 * i] -= y[6 * k] * lu[6 * i + k];
+      y[6 * i] *= 1.0 / lu[6 * i + i];
     }
   }
-  for (int k = 5; k >= 0; --k)
+  for (int k = 5; k >= 0; --k) /* dst.row(Q.indices(i)) = c.row(i) */
     if (ct[k] != k)
       for (int jj = 0; jj < 6; ++jj) { double t = c[6 * k + jj]; c[6 * k + jj] = c[6 * ct[k] + jj]; c[6 * ct[k] + jj] = t; }
   memcpy(x, c, sizeof c);

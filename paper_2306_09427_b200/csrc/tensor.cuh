@@ -195,77 +195,195 @@ FB_HD void rotate_stress(const double* rot, const double* su6, double* out) {
   sym_from_full(s9, out);
 }
 
-// Cyclic Jacobi eigensolver for the symmetric 3x3 F^T F (stands in for Eigen's
-// SelfAdjointEigenSolver, tensor.cpp:208-215).  Identical IEEE sequence in the oracle.
-FB_HD void jacobi3(double* a, double* q) {
-  for (int i = 0; i < 9; ++i) q[i] = (i % 4 == 0) ? 1.0 : 0.0;
-  const int P[3] = {0, 0, 1}, Q[3] = {1, 2, 2};
-  for (int sweep = 0; sweep < 64; ++sweep) {
-    bool rotated = false;
-    for (int r = 0; r < 3; ++r) {
-      const int p = P[r], qq = Q[r];
-      const double apq = a[3 * p + qq];
-      const double app = a[3 * p + p], aqq = a[3 * qq + qq];
-      if (fabs(apq) <= 1e-18 * (fabs(app) + fabs(aqq))) {
-        a[3 * p + qq] = a[3 * qq + p] = 0.0;
-        continue;
+// ---- Eigen 3.4.0 on the reference's hot path, restated (oracle/fibra_oracle.c carries
+// the derivation: SSE2 Packet2d build, no FMA).  Same IEEE sequence as the oracle.
+
+// Matrix3d product assignment (SliceVectorizedTraversal): rows 0-1 of each column as one
+// packet, ((l0 r0 + l1 r1) + l2 r2); row 2 through coeff(), l0 r0 + (l1 r1 + l2 r2).
+FB_HD void eig_prod3_slice(const double* l, const double* r, double* out) {
+  for (int j = 0; j < 3; ++j) {
+    for (int i = 0; i < 2; ++i)
+      out[3 * i + j] = (l[3 * i] * r[j] + l[3 * i + 1] * r[3 + j]) + l[3 * i + 2] * r[6 + j];
+    out[6 + j] = l[6] * r[j] + (l[7] * r[3 + j] + l[8] * r[6 + j]);
+  }
+}
+
+FB_HD double eig_hypot(double x, double y) {  // positive_real_hypot (MathFunctionsImpl.h)
+  x = fabs(x);
+  y = fabs(y);
+  if (isinf(x) || isinf(y)) return INFINITY;
+  if (isnan(x) || isnan(y)) return NAN;
+  const double p = smax(x, y);
+  if (p == 0.0) return 0.0;
+  const double qp = smin(y, x) / p;
+  return p * sqrt(1.0 + qp * qp);
+}
+
+FB_HD void eig_make_givens(double p, double q, double& c, double& s) {  // Jacobi.h
+  if (q == 0.0) {
+    c = p < 0.0 ? -1.0 : 1.0;
+    s = 0.0;
+  } else if (p == 0.0) {
+    c = 0.0;
+    s = q < 0.0 ? 1.0 : -1.0;
+  } else if (fabs(p) > fabs(q)) {
+    const double t = q / p;
+    double u = sqrt(1.0 + t * t);
+    if (p < 0.0) u = -u;
+    c = 1.0 / u;
+    s = -t * c;
+  } else {
+    const double t = p / q;
+    double u = sqrt(1.0 + t * t);
+    if (q < 0.0) u = -u;
+    s = -1.0 / u;
+    c = -t * s;
+  }
+}
+
+FB_HD void eig_qr_step(double* diag, double* sub, int start, int end, double* q) {
+  // tridiagonal_qr_step (SelfAdjointEigenSolver.h), Wilkinson shift
+  const double td = (diag[end - 1] - diag[end]) * 0.5;
+  const double e = sub[end - 1];
+  double mu = diag[end];
+  if (td == 0.0) {
+    mu -= fabs(e);
+  } else if (e != 0.0) {
+    const double e2 = e * e;
+    const double h = eig_hypot(td, e);
+    if (e2 == 0.0)
+      mu -= e / ((td + (td > 0.0 ? h : -h)) / e);
+    else
+      mu -= e2 / (td + (td > 0.0 ? h : -h));
+  }
+  double x = diag[start] - mu;
+  double z = sub[start];
+  for (int k = start; k < end && z != 0.0; ++k) {
+    double c, s;
+    eig_make_givens(x, z, c, s);
+    const double sdk = s * diag[k] + c * sub[k];
+    const double dkp1 = s * sub[k] + c * diag[k + 1];
+    diag[k] = c * (c * diag[k] - s * sub[k]) - s * (c * sub[k] - s * diag[k + 1]);
+    diag[k + 1] = s * sdk + c * dkp1;
+    sub[k] = c * sdk - s * dkp1;
+    if (k > start) sub[k - 1] = c * sub[k - 1] - s * z;
+    x = sub[k];
+    if (k < end - 1) {
+      z = -s * sub[k + 1];
+      sub[k + 1] = c * sub[k + 1];
+    }
+    if (!(c == 1.0 && -s == 0.0))  // Q.applyOnTheRight(k, k+1, rot): rotation (c, -s)
+      for (int i = 0; i < 3; ++i) {
+        const double xi = q[3 * i + k], yi = q[3 * i + k + 1];
+        q[3 * i + k] = c * xi + (-s) * yi;
+        q[3 * i + k + 1] = s * xi + c * yi;
       }
-      rotated = true;
-      const double tau = (aqq - app) / (2.0 * apq);
-      const double t = tau >= 0.0 ? 1.0 / (tau + sqrt(1.0 + tau * tau))
-                                  : -1.0 / (-tau + sqrt(1.0 + tau * tau));
-      const double c = 1.0 / sqrt(1.0 + t * t);
-      const double s = t * c;
-      a[3 * p + p] = app - t * apq;
-      a[3 * qq + qq] = aqq + t * apq;
-      a[3 * p + qq] = a[3 * qq + p] = 0.0;
-      const int o = 3 - p - qq;
-      const double arp = a[3 * o + p], arq = a[3 * o + qq];
-      a[3 * o + p] = a[3 * p + o] = c * arp - s * arq;
-      a[3 * o + qq] = a[3 * qq + o] = s * arp + c * arq;
-      for (int k = 0; k < 3; ++k) {
-        const double qkp = q[3 * k + p], qkq = q[3 * k + qq];
-        q[3 * k + p] = c * qkp - s * qkq;
-        q[3 * k + qq] = s * qkp + c * qkq;
+  }
+}
+
+// SelfAdjointEigenSolver<Matrix3d>::compute(a, ComputeEigenvectors); false = NoConvergence
+FB_HD bool eigen_sym3(const double* a, double* lam, double* q) {
+  double m[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) m[3 * i + j] = (j <= i) ? a[3 * i + j] : 0.0;
+  double scale = 0.0;
+  for (int k = 0; k < 9; ++k) scale = smax(scale, fabs(m[k]));
+  if (scale == 0.0) scale = 1.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j <= i; ++j) m[3 * i + j] /= scale;
+  double diag[3], sub[2];  // tridiagonalization_inplace_selector<MatrixType, 3, false>
+  diag[0] = m[0];
+  const double v1norm2 = m[6] * m[6];
+  if (v1norm2 <= DBL_MIN) {
+    diag[1] = m[4];
+    diag[2] = m[8];
+    sub[0] = m[3];
+    sub[1] = m[7];
+    for (int k = 0; k < 9; ++k) q[k] = (k % 4 == 0) ? 1.0 : 0.0;
+  } else {
+    const double beta = sqrt(m[3] * m[3] + v1norm2);
+    const double inv_beta = 1.0 / beta;
+    const double m01 = m[3] * inv_beta;
+    const double m02 = m[6] * inv_beta;
+    const double qq = 2.0 * m01 * m[7] + m02 * (m[8] - m[4]);
+    diag[1] = m[4] + m02 * qq;
+    diag[2] = m[8] - m02 * qq;
+    sub[0] = beta;
+    sub[1] = m[7] - m01 * qq;
+    q[0] = 1; q[1] = 0; q[2] = 0;
+    q[3] = 0; q[4] = m01; q[5] = m02;
+    q[6] = 0; q[7] = m02; q[8] = -m01;
+  }
+  const double precision_inv = 1.0 / DBL_EPSILON;  // computeFromTridiagonal_impl
+  int end = 2, start = 0, iter = 0;
+  while (end > 0) {
+    for (int i = start; i < end; ++i) {
+      if (fabs(sub[i]) < DBL_MIN) {
+        sub[i] = 0.0;
+      } else {
+        const double scaled = precision_inv * sub[i];
+        if (scaled * scaled <= (fabs(diag[i]) + fabs(diag[i + 1]))) sub[i] = 0.0;
       }
     }
-    if (!rotated) break;
+    while (end > 0 && sub[end - 1] == 0.0) end--;
+    if (end <= 0) break;
+    iter++;
+    if (iter > 30 * 3) break;
+    start = end - 1;
+    while (start > 0 && sub[start - 1] != 0.0) start--;
+    eig_qr_step(diag, sub, start, end, q);
   }
+  if (iter > 30 * 3) return false;
+  for (int i = 0; i < 2; ++i) {  // ascending sort, first minimum, columns follow
+    int k = 0;
+    for (int t = 1; t < 3 - i; ++t)
+      if (diag[i + t] < diag[i + k]) k = t;
+    if (k > 0) {
+      const double d = diag[i];
+      diag[i] = diag[k + i];
+      diag[k + i] = d;
+      for (int r = 0; r < 3; ++r) {
+        const double v = q[3 * r + i];
+        q[3 * r + i] = q[3 * r + k + i];
+        q[3 * r + k + i] = v;
+      }
+    }
+  }
+  for (int k = 0; k < 3; ++k) lam[k] = diag[k] * scale;
+  return true;
 }
 
 // F = R U via the eigendecomposition of F^T F (tensor.cpp:203-224)
 FB_HD bool polar_decompose(const double* f, double* rot, double* u6) {
   const double j = det3(f);
   if (!(j > 0.0)) return false;
-  double ft[9], c[9], q[9];
-  transpose3(f, ft);
-  matmul3(ft, f, c);
-  jacobi3(c, q);
-  const double lam[3] = {c[0], c[4], c[8]};
-  if (lam[0] <= 0.0 || lam[1] <= 0.0 || lam[2] <= 0.0) return false;
+  double c[9];
+  for (int i = 0; i < 3; ++i)  // fe.transpose() * fe (vectorized redux per coefficient)
+    for (int jj = 0; jj < 3; ++jj)
+      c[3 * i + jj] = (f[i] * f[jj] + f[3 + i] * f[3 + jj]) + f[6 + i] * f[6 + jj];
+  double lam[3], q[9];
+  if (!eigen_sym3(c, lam, q)) return false;
+  if (smin(smin(lam[0], lam[1]), lam[2]) <= 0.0) return false;
   double sq[3], isq[3];
-  for (int k = 0; k < 3; ++k) {
-    sq[k] = sqrt(lam[k]);
-    isq[k] = 1.0 / sq[k];
-  }
-  double u[9], uinv[9];
+  for (int k = 0; k < 3; ++k) sq[k] = sqrt(lam[k]);
+  for (int k = 0; k < 3; ++k) isq[k] = 1.0 / sq[k];
+  double qd[9], qdi[9], qt[9], u[9], uinv[9];
   for (int i = 0; i < 3; ++i)
-    for (int jj = 0; jj < 3; ++jj) {
-      double s = 0, si = 0;
-      for (int k = 0; k < 3; ++k) {
-        s += (q[3 * i + k] * sq[k]) * q[3 * jj + k];
-        si += (q[3 * i + k] * isq[k]) * q[3 * jj + k];
-      }
-      u[3 * i + jj] = s;
-      uinv[3 * i + jj] = si;
+    for (int k = 0; k < 3; ++k) {
+      qd[3 * i + k] = q[3 * i + k] * sq[k];
+      qdi[3 * i + k] = q[3 * i + k] * isq[k];
+      qt[3 * k + i] = q[3 * i + k];
     }
-  matmul3(f, uinv, rot);
+  eig_prod3_slice(qd, qt, u);
+  eig_prod3_slice(qdi, qt, uinv);
+  eig_prod3_slice(f, uinv, rot);
   sym_from_full(u, u6);
   return true;
 }
 
-// ([M][T])^T A^T = P^T by full-pivot LU (stands in for Eigen::FullPivLU,
-// stiffness.cpp:26-39); returns false when rank-deficient (isInvertible() == false).
+// ([M][T])^T A^T = P^T by Eigen::FullPivLU (stiffness.cpp:26-39); false when
+// rank-deficient (isInvertible() == false).  Solve order = Eigen's blocked TRSM on the
+// row-major rhs copy (see the oracle).
 FB_HD bool fullpiv_solve6(const double* a_in, const double* rhs, double* x) {
   double lu[36], c[36];
   int rt[6], ct[6];
@@ -308,11 +426,26 @@ FB_HD bool fullpiv_solve6(const double* a_in, const double* rhs, double* x) {
     if (rt[k] != k)
       for (int jj = 0; jj < 6; ++jj) { const double t = c[6 * k + jj]; c[6 * k + jj] = c[6 * rt[k] + jj]; c[6 * rt[k] + jj] = t; }
   for (int jj = 0; jj < 6; ++jj) {
-    for (int k = 0; k < 6; ++k)
-      for (int i = k + 1; i < 6; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
-    for (int k = 5; k >= 0; --k) {
-      c[6 * k + jj] /= lu[6 * k + k];
-      for (int i = 0; i < k; ++i) c[6 * i + jj] -= lu[6 * i + k] * c[6 * k + jj];
+    double* y = c + jj;
+    for (int i = 1; i < 4; ++i)  // unit lower: 4-row panel, gebp rows 4-5, 2-row panel
+      for (int k = 0; k < i; ++k) y[6 * i] -= y[6 * k] * lu[6 * i + k];
+    for (int i = 4; i < 6; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < 4; ++k) acc = acc + y[6 * k] * lu[6 * i + k];
+      y[6 * i] = y[6 * i] + (-1.0) * acc;
+    }
+    y[6 * 5] -= y[6 * 4] * lu[6 * 5 + 4];
+    y[6 * 5] *= 1.0 / lu[6 * 5 + 5];  // upper: 2-row panel, gebp rows 0-3, 4-row panel
+    y[6 * 4] -= y[6 * 5] * lu[6 * 4 + 5];
+    y[6 * 4] *= 1.0 / lu[6 * 4 + 4];
+    for (int i = 0; i < 4; ++i) {
+      double acc = 0.0;
+      for (int k = 4; k < 6; ++k) acc = acc + y[6 * k] * lu[6 * i + k];
+      y[6 * i] = y[6 * i] + (-1.0) * acc;
+    }
+    for (int i = 3; i >= 0; --i) {
+      for (int k = i + 1; k < 4; ++k) y[6 * i] -= y[6 * k] * lu[6 * i + k];
+      y[6 * i] *= 1.0 / lu[6 * i + i];
     }
   }
   for (int k = 5; k >= 0; --k)

@@ -224,3 +224,19 @@ def test_config4_lattices_fit_16_cta_clusters():
         _capi.load().fibra_debug_cluster_smem(net.desc(), 16, 2, out.ctypes.data_as(_capi._lp))
         assert out[0] == 1 and out[3] <= 4096, (i, out)
         assert out[2] <= 232448 - 4096, (i, out)
+
+
+def test_reference_arm_workload_matches_product():
+    """bench.py's reference arm rebuilds the config-2 F batch without the product package
+    (oracle/workload.py); both restatements of the test_batch.cpp:149-157 recipe agree bit
+    for bit, and the reference arm's step slices cover every point."""
+    import bench
+    from oracle import workload as W
+    from paper_2306_09427_b200 import synth
+    a, b = W.batch_F(1024), synth.batch_F(1024)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    for steps in (1, 3, 5, 16, 20, 100):
+        sl = bench.step_slices(1024, steps, 32)
+        assert len(sl) == steps
+        assert len(set(np.concatenate(sl).tolist())) == 1024 or steps * len(sl[0]) < 1024
+        assert min(len(s) for s in sl) >= 32

@@ -223,6 +223,25 @@ def test_polar_properties(oracle_lib):  # test_tensor.cpp:59-112 (tolerance-pinn
         O.polar_decompose(np.diag([-1.0, 1, 1]))
 
 
+def test_eigen_sym3_restatement(oracle_lib):
+    """Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d> restatement (fibra_oracle.c): agrees
+    with LAPACK to rounding, ascending order, orthonormal columns; a diagonal input deflates
+    without a QR step, so eigenvalues are the diagonal bits exactly (sorted) and Q is a
+    permutation."""
+    rng = np.random.default_rng(11)
+    for t in range(2000):
+        F = np.eye(3) + rng.uniform(-0.3, 0.3, (3, 3)) * 10.0 ** rng.uniform(-8, 0)
+        C = F.T @ F
+        lam, Q = O.eigen_sym3(C)
+        assert np.all(np.diff(lam) >= 0)
+        assert np.max(np.abs(lam - np.linalg.eigvalsh(C))) <= 1e-14 * np.max(np.abs(lam))
+        assert np.linalg.norm(C @ Q - Q * lam) <= 1e-14 * np.linalg.norm(C)
+        assert np.linalg.norm(Q.T @ Q - np.eye(3)) <= 1e-14
+    lam, Q = O.eigen_sym3(np.diag([3.0, 1.0, 2.0]))
+    assert list(lam) == [1.0, 2.0, 3.0]
+    assert sorted(map(tuple, np.abs(Q))) == sorted(map(tuple, np.eye(3)))
+
+
 def _substitute_pk2(U6, mu=1.3, lam=0.8):  # batch.cpp:199-214 (closed-form material)
     U = np.array([[U6[0], U6[5], U6[4]], [U6[5], U6[1], U6[3]], [U6[4], U6[3], U6[2]]])
     C = U @ U
