@@ -111,6 +111,12 @@ int fibra_debug_cluster_forces(const fibra_net_desc* net, int C, int shape, int 
                                const double* u, double* f_emul, double* f_direct);
 int fibra_debug_resident_forces(const fibra_net_desc* net, int shape, const double* u,
                                 double* f_emul, double* f_direct);
+/* Diagnostics (no CUDA): one node-centric force pass (csrc/dr_node.cuh) emulated on the host
+ * from the uploaded incidence tables, linear law with ea_scale 1, f_emul in packed order;
+ * report[4] = {half-warp gather steps, excess bank wavefronts before / after the placement
+ * search, incidence rows}.  shape indexes the node shapes. */
+int fibra_debug_node_forces(const fibra_net_desc* net, int shape, const double* u,
+                            double* f_emul, int64_t* report);
 /* Diagnostics (no CUDA): out[4] = {plan found, mirror mode, dynamic shared bytes, static
  * control-block bytes} of the cluster plan of `net` on C CTAs of cluster shape `shape`. */
 int fibra_debug_cluster_smem(const fibra_net_desc* net, int C, int shape, int64_t* out);

@@ -415,6 +415,10 @@ def ref():
                                           _dp, _dp]
         L.ref_batch_stress.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, C.c_double, C.c_double,
                                        C.c_int, C.POINTER(CRelaxCfg), C.c_int, _dp, _lp, _ip]
+        L.ref_batch_response.argtypes = [C.POINTER(C.c_void_p), _ip, C.c_int, _dp, C.c_int,
+                                         C.c_double, C.c_double, C.c_int,
+                                         C.POINTER(CRelaxCfg), C.c_double, C.c_int, C.c_int,
+                                         C.c_int, _dp, _dp, _lp, _lp, _ip, _ip, _ip]
         L.ref_last_error.restype = C.c_char_p
         _ref = L
     return _ref
@@ -536,6 +540,35 @@ def ref_batch_stress(rnet: RefNetwork, F, cfg: RelaxConfig = None, law: Law = No
     if rc:
         raise OracleError(rc, ref().ref_last_error().decode())
     return sig, iters, status
+
+
+def ref_batch_response(rnets, entry_of_point, F, cfg: RelaxConfig = None, law: Law = None,
+                       fd_rel_step=1e-5, reuse_warm=True, want_tangent=True, workers=1):
+    """constitutive_response per point (stiffness.cpp:153-175) with every DR solve and
+    homogenized stress from the reference's compiled code (ref_shim.cpp), fresh states.
+    Returns a dict of arrays: sigma (n,6), spatial_c (n,36), base_iterations,
+    relax_iterations, solves, failed_probe, status."""
+    cfg = cfg or RelaxConfig()
+    law = law or Law()
+    F = np.ascontiguousarray(F, dtype=np.float64).reshape(-1, 9)
+    n = len(F)
+    eop = np.ascontiguousarray(entry_of_point, dtype=np.int32)
+    handles = (C.c_void_p * len(rnets))(*[r.h.value for r in rnets])
+    out = {"sigma": np.zeros((n, 6)), "spatial_c": np.zeros((n, 36)),
+           "base_iterations": np.zeros(n, np.int64), "relax_iterations": np.zeros(n, np.int64),
+           "solves": np.zeros(n, np.int32), "failed_probe": np.zeros(n, np.int32),
+           "status": np.zeros(n, np.int32)}
+    rc = ref().ref_batch_response(handles, _ptr(eop, _ip), n, _ptr(F, _dp), law.kind,
+                                  law.ea_scale, law.nonlinearity, int(law.buckling_off),
+                                  C.byref(cfg.c()), fd_rel_step, int(reuse_warm),
+                                  int(want_tangent), workers,
+                                  *(_ptr(out[k], t) for k, t in
+                                    (("sigma", _dp), ("spatial_c", _dp),
+                                     ("base_iterations", _lp), ("relax_iterations", _lp),
+                                     ("solves", _ip), ("failed_probe", _ip), ("status", _ip))))
+    if rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    return out
 
 
 def network_from_ref(rnet: RefNetwork, box_half=0.5, tol_bnd=1e-6) -> Network:

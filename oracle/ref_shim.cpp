@@ -358,4 +358,125 @@ int ref_batch_stress(void* h, int n_points, const double* F, int law_kind, doubl
   }
 }
 
+
+// Full constitutive_response (stiffness.cpp:153-175: solve_base :66-83, probe_pk2s :86-123,
+// material_stiffness_from_probes :15-41, push_forward_stiffness tensor.cpp:286-300) per
+// point through the reference WorkerPool: every one of the 7 DR solves and every
+// homogenized stress is the reference's compiled relax_solve / homogenized_stress; the
+// Eigen/tensor.cpp steps (polar, pull-back, probing, FullPivLU, push-forward) come from the
+// oracle restatement.  Fresh states (init_batch).  Per point: sigma[6], spatial C[36],
+// base iterations, relax_iterations (all solves), solves, failed_probe, status.
+int ref_batch_response(void* const* nets, const int32_t* entry_of_point, int n_points,
+                       const double* F, int law_kind, double ea_scale, double nonlin,
+                       int buckling_off, const or_relax_cfg* cfg, double fd_rel_step,
+                       int reuse_warm, int want_tangent, int workers, double* sigma_out,
+                       double* c_out, int64_t* base_iters, int64_t* relax_iters,
+                       int32_t* solves, int32_t* failed_probe, int32_t* status) {
+  const FiberLaw law = make_law(law_kind, ea_scale, nonlin, buckling_off);
+  const RelaxConfig rc = make_cfg(cfg);
+  struct Buf {
+    std::vector<double> b;
+    double t = 0;
+    std::int64_t it = 0;
+    std::uint8_t conv = 0;
+    RveStateView view(std::size_t nd, int n_free) {
+      b.assign(7 * nd, 0.0);
+      RveStateView s;
+      s.u = std::span<double>(b.data(), nd);
+      s.v = std::span<double>(b.data() + nd, nd);
+      s.a = std::span<double>(b.data() + 2 * nd, nd);
+      s.f_int = std::span<double>(b.data() + 3 * nd, nd);
+      s.f_damp = std::span<double>(b.data() + 4 * nd, nd);
+      s.mass = std::span<double>(b.data() + 5 * nd, nd);
+      s.inv_mass = std::span<double>(b.data() + 6 * nd, nd);
+      s.t = &t;
+      s.iters = &it;
+      s.converged = &conv;
+      s.n_free = n_free;
+      return s;
+    }
+  };
+  try {
+    WorkerPool pool(workers);
+    pool.run(n_points, [&](int p) {
+      const FiberNetwork& net = *static_cast<const FiberNetwork*>(nets[entry_of_point[p]]);
+      const std::size_t nd = static_cast<std::size_t>(net.n_dof());
+      double* sig = sigma_out + 6 * p;
+      double* cc = c_out + 36 * p;
+      std::memset(sig, 0, 6 * sizeof(double));
+      std::memset(cc, 0, 36 * sizeof(double));
+      base_iters[p] = relax_iters[p] = 0;
+      solves[p] = 0;
+      failed_probe[p] = -1;
+      status[p] = 0;
+      Buf base, scratch;
+      RveStateView s = base.view(nd, net.n_free());
+      double R[9], U[6], fu9[9], su6[6], pk2[6];
+      int rc2 = or_polar_decompose(F + 9 * p, R, U);
+      if (rc2) { status[p] = rc2; return; }
+      or_sym_full(U, fu9);
+      try {
+        const RelaxReport r = relax_solve(net, law, def_of(fu9), rc, s, WarmStart::reuse);
+        base_iters[p] = r.iterations;
+        if (!r.converged) { status[p] = OR_NOT_CONVERGED; return; }
+        const HomogenizedStress hs = homogenized_stress(net, s, def_of(fu9), net.box());
+        const double a6[6] = {hs.sigma.xx, hs.sigma.yy, hs.sigma.zz,
+                              hs.sigma.yz, hs.sigma.xz, hs.sigma.xy};
+        std::memcpy(su6, a6, sizeof a6);
+        if ((rc2 = or_pull_back_stress(su6, fu9, pk2))) { status[p] = rc2; return; }
+        solves[p] = 1;
+        relax_iters[p] = r.iterations;
+      } catch (const SolverError& e) {
+        status[p] = classify(e);
+        return;
+      } catch (const KinematicsError& e) {
+        status[p] = classify(e);
+        return;
+      }
+      if (want_tangent) {
+        const double h = fd_rel_step * std::sqrt(U[0] * U[0] + U[1] * U[1] + U[2] * U[2] +
+                                                 2.0 * (U[3] * U[3] + U[4] * U[4] + U[5] * U[5]));
+        RveStateView sc = scratch.view(nd, net.n_free());
+        double probes[36];
+        for (int q = 0; q < 6; ++q) {
+          double dir[6], up[6], fq[9];
+          or_probing_direction(q, dir);
+          for (int i = 0; i < 6; ++i) up[i] = U[i] + dir[i] * h;
+          or_sym_full(up, fq);
+          if (!(or_det(fq) > 0)) { status[p] = OR_PROBE_FAILED; return; }
+          if (reuse_warm) std::copy(s.u.begin(), s.u.end(), sc.u.begin());
+          try {
+            const RelaxReport pr = relax_solve(net, law, def_of(fq), rc, sc,
+                                               reuse_warm ? WarmStart::reuse : WarmStart::zero_interior);
+            ++solves[p];
+            relax_iters[p] += pr.iterations;
+            if (!pr.converged) { failed_probe[p] = q; status[p] = OR_PROBE_FAILED; return; }
+            const HomogenizedStress hq = homogenized_stress(net, sc, def_of(fq), net.box());
+            const double q6[6] = {hq.sigma.xx, hq.sigma.yy, hq.sigma.zz,
+                                  hq.sigma.yz, hq.sigma.xz, hq.sigma.xy};
+            if ((rc2 = or_pull_back_stress(q6, fq, probes + 6 * q))) { status[p] = rc2; return; }
+          } catch (const SolverError& e) {
+            failed_probe[p] = q;
+            status[p] = OR_PROBE_FAILED;
+            return;
+          }
+        }
+        double a[36];
+        if ((rc2 = or_material_stiffness_from_probes(U, pk2, probes, h, a))) { status[p] = rc2; return; }
+        if ((rc2 = or_push_forward_stiffness(a, F + 9 * p, cc))) { status[p] = rc2; return; }
+      }
+      double su[9], rt[9], t1[9], s9[9];
+      or_sym_full(su6, su);
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) rt[3 * i + j] = R[3 * j + i];
+      or_matmul(R, su, t1);
+      or_matmul(t1, rt, s9);
+      or_sym_from_full(s9, sig);
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
 }  // extern "C"

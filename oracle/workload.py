@@ -66,3 +66,35 @@ def batch_F(n: int, seed: int = 55) -> np.ndarray:
         F[p, 1, 1] -= u(0.0, 0.02)
         F[p, 0, 1] += u(0.0, 0.02)
     return F
+
+
+CONFIG3_POINTS = 16384
+
+
+def splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def config3_spec(p: int):
+    """Config-3 RVE p: M = 500 + splitmix64(p) mod 4501 fibers, N = round(M / r)
+    nodes with r = 2.67 up to 1,500 fibers and 4 above; knn, neighbors 10, merge 0.05,
+    seed p + 1 (advanced by 16,384 on ConfigError)."""
+    m = 500 + splitmix64(p) % 4501
+    r = 2.67 if m <= 1500 else 4.0
+    return dict(style="knn", nodes=int(round(m / r)), fibers=m, neighbors=10,
+                merge_radius=0.05), p + 1
+
+
+def config3_ref_network(p: int):
+    """Config-3 RVE p built by the REFERENCE generator (oracle/_ref)."""
+    import oracle as O
+    spec, seed = config3_spec(p)
+    for _ in range(64):
+        try:
+            return O.ref_generate(seed=seed, **spec), seed
+        except O.OracleError:
+            seed += CONFIG3_POINTS
+    raise RuntimeError(f"config-3 RVE {p}: no valid seed")

@@ -29,7 +29,7 @@ EXPORTS = [
     "fibra_network_write", "fibra_network_describe", "fibra_network_free",
     "fibra_host_last_error", "fibra_assign_random", "fibra_schedule_report",
     "fibra_cluster_report", "fibra_schedule_slots", "fibra_debug_cluster_forces",
-    "fibra_debug_resident_forces", "fibra_debug_cluster_smem",
+    "fibra_debug_resident_forces", "fibra_debug_cluster_smem", "fibra_debug_node_forces",
     "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
     "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel", "fibra_cuda_orientation",
@@ -139,6 +139,7 @@ def load(build_if_missing: bool = True):
                                                  _dp, _dp, _dp]),
         "fibra_debug_cluster_smem": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, _lp]),
         "fibra_debug_resident_forces": (C.c_int, [C.POINTER(NetDesc), C.c_int, _dp, _dp, _dp]),
+        "fibra_debug_node_forces": (C.c_int, [C.POINTER(NetDesc), C.c_int, _dp, _dp, _lp]),
         "fibra_schedule_slots": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, _ip,
                                            C.c_int32]),
         "fibra_cuda_open": (C.c_int, [C.c_int, pp]),

@@ -25,15 +25,19 @@ SOURCES = [
     os.path.join(HERE, "csrc", "fibra_cuda.cu"),
     os.path.join(HERE, "csrc", "kernels_resident.cu"),
     os.path.join(HERE, "csrc", "kernels_cluster.cu"),
+    os.path.join(HERE, "csrc", "kernels_node.cu"),
     os.path.join(HERE, "csrc", "assembly.cu"),
     os.path.join(HERE, "csrc", "host", "network.cpp"),
     os.path.join(HERE, "csrc", "host", "netgen.cpp"),
     os.path.join(HERE, "csrc", "host", "schedule.cpp"),
     os.path.join(HERE, "csrc", "host", "cluster_schedule.cpp"),
+    os.path.join(HERE, "csrc", "host", "node_schedule.cpp"),
 ]
 DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "dr_kernel.cuh"),
     os.path.join(HERE, "csrc", "dr_cluster.cuh"),
+    os.path.join(HERE, "csrc", "dr_node.cuh"),
+    os.path.join(HERE, "csrc", "host", "node_schedule.hpp"),
     os.path.join(HERE, "csrc", "variants.hpp"),
     os.path.join(HERE, "csrc", "host", "cluster_schedule.hpp"),
     os.path.join(HERE, "csrc", "tensor.cuh"),

@@ -31,6 +31,7 @@
 #include "dr_cluster.cuh"
 #include "dr_kernel.cuh"
 #include "host/cluster_schedule.hpp"
+#include "host/node_schedule.hpp"
 #include "host/schedule.hpp"
 #include "fibra_cuda.h"
 #include "tensor.cuh"
@@ -267,6 +268,14 @@ __global__ void fastmath_selftest_kernel(unsigned long long n, unsigned long lon
     double q = div_fast(a, b, ok);
     if (!ok) q = a / b;
     local += !same_bits(q, a / b);
+    q = div_fast_i(a, b, ok);  // integer-predicate variant of the DR kernels
+    if (!ok) q = a / b;
+    local += !same_bits(q, a / b);
+    const double zq = (mode == 3 ? 0.0 : a);  // zero numerators through the escape
+    q = div_fast_i(zq, b, ok);
+    if (!ok) q = zq / b;
+    local += !same_bits(q, zq / b);
+    local += le_nonneg_bits(fabs(a), fabs(b)) != (fabs(a) <= fabs(b)) && !isnan(a) && !isnan(b);
     const double x = mode == 2 ? a : fabs(a);
     double s = sqrt_fast(x, ok);
     if (!ok) s = sqrt(x);
@@ -295,9 +304,11 @@ constexpr int kMaxClasses = 16;  // 4 bits of the schedule key
 
 struct DeviceEntry {
   EntryDev dev;           // resident-kernel entry
+  NodeEntryDev ndev;      // node-centric kernel entry
   ClusterEntryDev cdev;   // cluster-kernel entry
   OrientDev orient;       // reference-order fibres + packed reference (orientation_p2)
   Schedule sched;
+  NodeSchedule nsched;
   std::vector<void*> allocs;
   int cls = -1;           // kernel class
   float log_its = 0;      // topology term of the schedule cost model (upload_library)
@@ -311,12 +322,14 @@ struct DeviceEntry {
 // own ticket queue; classes of one call run concurrently on forked streams.
 struct KClass {
   bool cluster = false;
+  bool node = false;      // node-centric resident kernel (dr_node.cuh)
   int vi = 0, C = 1;
   int x_bytes = 0, g_bytes = 0, ts = 0, csr_cap = 0, push_cap = 0, ck_stride = 0;
   int max_halo = 0;  // cluster: halo slots per bank (two banks, dr_cluster.cuh)
   long long scratch_stride = 0;
   bool uniform_ea = true;
   EntryDev* d_entries = nullptr;          // [n_entries] (resident)
+  NodeEntryDev* d_nentries = nullptr;     // [n_entries] (node)
   ClusterEntryDev* d_centries = nullptr;  // [n_entries] (cluster)
   int n_points = 0, point_off = 0;        // bound points of the class, offset in the order
   cudaStream_t stream = nullptr;   // head launch (several classes) or the class's only launch
@@ -327,7 +340,14 @@ struct KClass {
   size_t ckpt_cap = 0;
   double* d_scratch = nullptr;
   size_t scratch_cap = 0;
+  // node classes: x double buffer + incidence tables (x offsets, (l0, 1/l0), EA when not
+  // uniform, reduced mass for the nonlinear law)
+  size_t node_smem(bool nonlinear) const {
+    return 2ull * x_bytes + ((4ull * csr_cap + 15) & ~15ull) + 16ull * csr_cap +
+           (uniform_ea ? 0ull : 8ull * csr_cap) + (nonlinear ? 8ull * csr_cap : 0ull);
+  }
   size_t smem() const {
+    if (node) return node_smem(true);
     if (cluster)
       return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 8ull * csr_cap + 4ull * push_cap;
     return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 4ull * (ts + 1) + 4ull * csr_cap;
@@ -469,6 +489,7 @@ void free_library(fibra_ctx* c) {
   c->entries.clear();
   for (auto& k : c->classes) {
     cudaFree(k.d_entries);
+    cudaFree(k.d_nentries);
     cudaFree(k.d_centries);
     cudaFree(k.d_ckpt);
     cudaFree(k.d_scratch);
@@ -551,6 +572,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
 
   DrParams P;
   P.entries = nullptr;
+  P.nentries = nullptr;
   P.entry_of_point = c->d_entry_of_point;
   P.offsets = c->d_offsets;
   P.u = c->d_state[0];
@@ -623,7 +645,8 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   std::vector<double> class_work(c->classes.size(), 0.0), class_cost(c->classes.size(), 0.0);
   for (int p = 0; p < n; ++p) {
     const DeviceEntry& de = c->entries[c->entry_of_point[p]];
-    const int m = c->classes[de.cls].cluster ? de.cdev.n_fibers : de.dev.n_fibers;
+    const KClass& Kc = c->classes[de.cls];
+    const int m = Kc.cluster ? de.cdev.n_fibers : (Kc.node ? de.ndev.n_fibers : de.dev.n_fibers);
     class_work[de.cls] += m;
     class_cost[de.cls] += std::exp(static_cast<double>(de.log_its)) * m;
   }
@@ -652,7 +675,18 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
     const size_t smem = K.smem();
     int cap = 0;  // co-resident CTAs (resident) or clusters (cluster) on the device
-    if (!K.cluster) {
+    if (K.node) {
+      const NodeVariant& v = kNodeVariants[K.vi];
+      KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      const size_t nsm = K.node_smem(law->kind != 0);
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(nsm)));
+      int per_sm = 0;
+      FB_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, v.T, nsm));
+      if (per_sm < 1) return set_err(c, FIBRA_E_ARG, "node DR kernel does not fit on an SM");
+      cap = per_sm * c->n_sm;
+      plan[ci].per_unit = per_sm;
+    } else if (!K.cluster) {
       const Variant& v = kVariants[K.vi];
       KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -708,7 +742,19 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     P.csr_cap = K.csr_cap;
     P.ck_stride = K.ck_stride;
     const size_t smem = K.smem();
-    if (!K.cluster) {
+    if (K.node) {
+      const NodeVariant& v = kNodeVariants[K.vi];
+      KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      const size_t nsm = K.node_smem(law->kind != 0);
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(nsm)));
+      P.first_wave_sms = (!heads && plan[ci].per_unit == 2 && units == 2 * c->n_sm) ? c->n_sm : 0;
+      P.entries = nullptr;
+      P.nentries = K.d_nentries;
+      P.ckpt = K.d_ckpt + static_cast<size_t>(slot0) * 12 * K.ck_stride;
+      P.phase_prof = nullptr;
+      fn<<<units, v.T, nsm, sm>>>(P);
+    } else if (!K.cluster) {
       const Variant& v = kVariants[K.vi];
       KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       // (several classes may share a kernel function: its shared-memory limit is set per launch)
@@ -937,6 +983,96 @@ void merge_caps(KClass& K, const Caps& e) {
   K.push_cap = std::max(K.push_cap, e.push_cap);
   K.max_halo = std::max(K.max_halo, e.max_halo);
   K.scratch_stride = std::max(K.scratch_stride, e.scratch_stride);
+}
+
+// node-centric kernel: shared-memory components of an entry for shape v (Caps fields:
+// x_bytes = one x buffer, csr_cap = incidence entries); the footprint is checked for the
+// nonlinear law (the largest) and must hold the exit scratch (f, x, m v^2, strain energy).
+int node_search_moves() {
+  const char* e = getenv("FIBRA_NODE_SEARCH");  // diagnostics: placement search moves
+  return e ? atoi(e) : 20000;
+}
+
+bool node_fits(const fibra_ctx* c, const PackedNet& P, const NodeVariant& v, bool uniform_ea,
+               NodeSchedule& S) {
+  const int TS = v.NPT * v.T;
+  if (P.N > TS || 24 * TS >= 65536) return false;  // 16-bit x offsets
+  if (!build_node_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.NPT,
+                           node_search_moves(), S))
+    return false;
+  KClass K;
+  K.node = true;
+  K.uniform_ea = uniform_ea;
+  K.x_bytes = static_cast<int>(align16(24ull * TS));
+  K.csr_cap = 32 * std::max(S.n_rows, 1);
+  const size_t region = K.node_smem(false) - 2ull * K.x_bytes;
+  const size_t exit_need = 8ull * (3 * P.N + 3 * P.NFN + P.M);
+  if (region < exit_need) K.csr_cap = static_cast<int>((exit_need + 19) / 20 + 32);
+  return K.node_smem(true) <= static_cast<size_t>(c->max_smem);
+}
+
+// node-kernel entry: slot arrays and the step-major incidence tables
+void build_node_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc& d,
+                      const NodeVariant& v, Arena& A, Caps& K) {
+  const NodeSchedule& S = de.nsched;
+  const int TS = v.NPT * v.T;
+  const int G = TS / 32;
+  std::vector<int> slot_pn(TS, -1), slot_deg(TS, 0);
+  std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
+  for (int sl = 0; sl < TS; ++sl) {
+    const int pn = S.pn_of_slot[sl];
+    slot_pn[sl] = pn;
+    slot_deg[sl] = S.deg[sl];
+    if (pn < 0) continue;
+    for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
+    slot_lump[sl] = P.lump[pn];
+  }
+  const size_t ninc = 32ull * S.n_rows;
+  std::vector<int> inc_x(ninc, 0);
+  std::vector<double> inc_l0(ninc, 1.0), inc_ea(ninc, 1.0), inc_lump(ninc, 1.0);
+  for (int g = 0; g < G; ++g)
+    for (int l = 0; l < 32; ++l) {
+      const int sl = 32 * g + l;
+      for (int st = 0; st < S.deg[sl]; ++st) {
+        const size_t ix = 32ull * (S.group_row0[g] + st) + l;
+        const int f = S.inc_fiber[sl][st], o = S.inc_other[sl][st];
+        inc_x[ix] = 24 * S.slot_of_pn[o];
+        inc_l0[ix] = P.l0[f];
+        inc_ea[ix] = P.ea[f];
+        inc_lump[ix] = P.lump[o];
+      }
+    }
+  NodeEntryDev& E = de.ndev;
+  E = NodeEntryDev{};
+  E.n_nodes = P.N;
+  E.n_fibers = P.M;
+  E.n_free_nodes = P.NFN;
+  E.n_fix_nodes = P.N - P.NFN;
+  E.f0 = S.f0;
+  E.node_slots = TS;
+  E.n_rows = S.n_rows;
+  E.max_lump = P.max_lump;
+  E.max_ea = d.max_ea;
+  E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
+  A.add(&E.slot_pn, slot_pn);
+  A.add(&E.slot_ref, slot_ref);
+  A.add(&E.slot_lump, slot_lump);
+  A.add(&E.slot_deg, slot_deg);
+  A.add(&E.group_row0, S.group_row0);
+  A.add(&E.inc_x, inc_x);
+  A.add(&E.inc_l0, inc_l0);
+  A.add(&E.inc_ea, inc_ea);
+  A.add(&E.inc_lump, inc_lump);
+  A.add(&E.fib_a, P.a);
+  A.add(&E.fib_b, P.b);
+  A.add(&E.fib_l0, P.l0);
+  A.add(&E.fib_ea, P.ea);
+  K.ts = TS;
+  K.x_bytes = static_cast<int>(align16(24ull * TS));
+  K.csr_cap = 32 * std::max(S.n_rows, 1);
+  const size_t region = 2ull * 0 + ((4ull * K.csr_cap + 15) & ~15ull) + 16ull * K.csr_cap;
+  const size_t exit_need = 8ull * (3 * P.N + 3 * P.NFN + P.M);
+  if (region < exit_need) K.csr_cap = static_cast<int>((exit_need + 19) / 20 + 32);
 }
 
 // resident-kernel entry: slot arrays, g*d record colouring, step-major CSR pairs
@@ -1307,7 +1443,13 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   c->entries.resize(n);
   std::vector<PackedNet> nets(n);
   std::vector<ClusterPlan> plans(n);
-  std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1);
+  std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1), kind_node(n, 0);
+  // FIBRA_KERNEL=node: the node-centric kernel (dr_node.cuh) for the entries it holds.
+  // Opt-in: it removes the fiber -> node barrier but evaluates every fibre twice, and on
+  // config 2 it issues 13.0k instructions per RVE-iteration against the fiber/node kernel's
+  // 6.2k, with warps waiting on the highest-degree warp (profiles/r02_node_*).
+  const char* kern_env = getenv("FIBRA_KERNEL");
+  const bool allow_node = kern_env && kern_env[0] == 'n';
   std::vector<Caps> est(n);  // the entry's shared-memory components (exact, = the build's)
   // diagnostics: FIBRA_FORCE_CLUSTER=C places every entry on a C-CTA cluster (kernel timing)
   const char* force_env = getenv("FIBRA_FORCE_CLUSTER");
@@ -1334,6 +1476,24 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       const double r = P.N ? static_cast<double>(P.M) / P.N : 0.0;
       de.log_its = static_cast<float>(7.2 * fd2 - 3.3 * r + 1.75 * std::log(std::max(P.M, 1)));
     }
+    // diagnostics: FIBRA_NODE_SHAPE=i restricts the node kernel to kNodeVariants[i]
+    const char* nshape_env = getenv("FIBRA_NODE_SHAPE");
+    const int force_nshape = nshape_env ? atoi(nshape_env) : -1;
+    for (int v = 0; v < kNumNodeVariants && kind_vi[i] < 0 && !force_c && allow_node; ++v)
+      if ((force_nshape < 0 || v == force_nshape) &&
+          node_fits(c, P, kNodeVariants[v], false, de.nsched)) {
+        kind_vi[i] = v;
+        kind_node[i] = 1;
+        const NodeVariant& nv = kNodeVariants[v];
+        const int TS = nv.NPT * nv.T;
+        est[i].ts = TS;
+        est[i].x_bytes = static_cast<int>(align16(24ull * TS));
+        int capn = 32 * std::max(de.nsched.n_rows, 1);
+        const size_t region = ((4ull * capn + 15) & ~15ull) + 16ull * capn;
+        const size_t exit_need = 8ull * (3 * P.N + 3 * P.NFN + P.M);
+        if (region < exit_need) capn = static_cast<int>((exit_need + 19) / 20 + 32);
+        est[i].csr_cap = capn;
+      }
     for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
       if (resident_fits(c, P, kVariants[v], mp, de.sched)) {
         kind_vi[i] = v;
@@ -1374,22 +1534,26 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
                                          std::to_string(nets[i].N) +
                                          " nodes) exceeds a 16-CTA cluster");
     const bool cl = kind_cl[i] != 0;
+    const bool nd = kind_node[i] != 0;
     // a class's footprint is the per-component maximum over its entries: join the first
     // class of this kernel shape that still fits the device with this entry, else open one
     auto fits_with = [&](const KClass& K) {
       KClass T = K;
+      T.uniform_ea = false;
       merge_caps(T, est[i]);
       return T.smem() <= static_cast<size_t>(c->max_smem - (cl ? kClusterCtlExtra : 0));
     };
     int k = 0;
     const int nk = static_cast<int>(c->classes.size());
-    while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].vi == kind_vi[i] &&
+    while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].node == nd &&
+                       c->classes[k].vi == kind_vi[i] &&
                        c->classes[k].C == kind_C[i] && fits_with(c->classes[k])))
       ++k;
     if (k == nk) {
       if (nk == kMaxClasses) return set_err(c, FIBRA_E_ARG, "too many kernel classes in one library");
       KClass K;
       K.cluster = cl;
+      K.node = nd;
       K.vi = kind_vi[i];
       K.C = kind_C[i];
       c->classes.push_back(K);
@@ -1419,6 +1583,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       if (K.cluster)
         build_cluster_entry(de, nets[i], entries[i], plans[i], kClusterVariants[K.vi],
                             arenas[i - lo], parts[i - lo], parts_off[i - lo], caps[i - lo]);
+      else if (K.node)
+        build_node_entry(de, nets[i], entries[i], kNodeVariants[K.vi], arenas[i - lo],
+                         caps[i - lo]);
       else
         build_resident_entry(de, nets[i], entries[i], kVariants[K.vi], arenas[i - lo],
                              caps[i - lo]);
@@ -1440,7 +1607,14 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   for (KClass& K : c->classes) {
     if (K.smem() > static_cast<size_t>(c->max_smem - (K.cluster ? kClusterCtlExtra : 0)))
       return set_err(c, FIBRA_E_ARG, "library shared-memory footprint exceeds the device limit");
-    if (K.cluster) {
+    if (K.node) {
+      std::vector<NodeEntryDev> host(n, NodeEntryDev{});
+      for (int i = 0; i < n; ++i)
+        if (&c->classes[c->entries[i].cls] == &K) host[i] = c->entries[i].ndev;
+      FB_CUDA(c, cudaMalloc(&K.d_nentries, sizeof(NodeEntryDev) * n));
+      FB_CUDA(c, cudaMemcpy(K.d_nentries, host.data(), sizeof(NodeEntryDev) * n,
+                            cudaMemcpyHostToDevice));
+    } else if (K.cluster) {
       std::vector<ClusterEntryDev> host(n, ClusterEntryDev{});
       for (int i = 0; i < n; ++i)
         if (&c->classes[c->entries[i].cls] == &K) host[i] = c->entries[i].cdev;
@@ -1538,7 +1712,10 @@ int fibra_cuda_orientation(fibra_ctx* c, const int32_t* points, int32_t n, const
 int fibra_cuda_entry_kernel(const fibra_ctx* c, int32_t entry, int32_t* out) {
   if (!c || !out || entry < 0 || entry >= static_cast<int>(c->entries.size())) return FIBRA_E_ARG;
   const KClass& K = c->classes[c->entries[entry].cls];
-  if (K.cluster) {
+  if (K.node) {  // fibres per thread: 0 marks the node-centric kernel
+    const NodeVariant& v = kNodeVariants[K.vi];
+    out[0] = 1, out[1] = v.T, out[2] = 0, out[3] = v.NPT;
+  } else if (K.cluster) {
     const ClusterVariant& v = kClusterVariants[K.vi];
     out[0] = K.C, out[1] = v.T, out[2] = v.FPT, out[3] = v.NPT;
   } else {
@@ -1724,9 +1901,11 @@ int fibra_cuda_last_stats(fibra_ctx* c, fibra_solve_stats* s) {
       float t = -1;
       cudaEventElapsedTime(&t, c->ev[1], K.done_t);
       std::fprintf(stderr, "class %zu: %s %s C=%d points=%d done at %.1f ms\n", k,
-                   K.cluster ? "cluster" : "resident",
+                   K.cluster ? "cluster" : (K.node ? "node" : "resident"),
                    K.cluster ? (std::to_string(kClusterVariants[K.vi].T) + "/" +
                                 std::to_string(kClusterVariants[K.vi].FPT)).c_str()
+                   : K.node  ? (std::to_string(kNodeVariants[K.vi].T) + "/" +
+                                std::to_string(kNodeVariants[K.vi].NPT)).c_str()
                              : (std::to_string(kVariants[K.vi].T) + "/" +
                                 std::to_string(kVariants[K.vi].FPT)).c_str(),
                    K.C, K.n_points, t);
@@ -1894,6 +2073,63 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
       f_direct[3 * P.b[f] + c] += g * dx[c];
       f_direct[3 * P.a[f] + c] -= g * dx[c];
     }
+  }
+  return FIBRA_OK;
+}
+
+// Diagnostics (no CUDA): one force pass of the node-centric kernel emulated on the host from
+// the uploaded arrays (x records by slot, step-major incidence tables, d' = x_other - x_own,
+// f -= g d' from +0.0), linear law with ea_scale 1, into f_emul (packed node order).  The
+// reference's force loop (network.cpp:275-311) must give the same bits.
+// report[4] = {half-warp gather steps, excess wavefronts before / after the placement
+// search, incidence rows}.
+int fibra_debug_node_forces(const fibra_net_desc* d, int shape, const double* u, double* f_emul,
+                            int64_t* report) {
+  if (!d || !u || !f_emul || shape < 0 || shape >= kNumNodeVariants) return FIBRA_E_ARG;
+  const PackedNet P = pack(*d);
+  const NodeVariant& v = kNodeVariants[shape];
+  DeviceEntry de;
+  if (!build_node_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.NPT,
+                           node_search_moves(), de.nsched))
+    return FIBRA_E_CONFIG;
+  Arena A;
+  Caps K;
+  build_node_entry(de, P, *d, v, A, K);
+  for (auto& f : A.fixes) {
+    const void* addr = A.host.data() + f.second;
+    std::memcpy(f.first, &addr, sizeof addr);
+  }
+  const NodeEntryDev& E = de.ndev;
+  const int TS = E.node_slots;
+  std::vector<double> X(3 * static_cast<size_t>(TS), 0.0);
+  for (int sl = 0; sl < TS; ++sl)
+    for (int c = 0; c < 3; ++c)
+      X[3 * sl + c] = E.slot_ref[3 * sl + c] + (E.slot_pn[sl] >= 0 ? u[3 * E.slot_pn[sl] + c] : 0.0);
+  for (int i = 0; i < 3 * P.N; ++i) f_emul[i] = 0.0;
+  for (int sl = 0; sl < TS; ++sl) {
+    const int pn = E.slot_pn[sl];
+    if (pn < 0) continue;
+    const int g = sl / 32, lane = sl % 32;
+    double f[3] = {0.0, 0.0, 0.0};
+    for (int st = 0; st < E.slot_deg[sl]; ++st) {
+      const int ix = 32 * (E.group_row0[g] + st) + lane;
+      const int o = E.inc_x[ix] / 8;
+      const double dx = X[o] - X[3 * sl], dy = X[o + 1] - X[3 * sl + 1], dz = X[o + 2] - X[3 * sl + 2];
+      const double len = std::sqrt(dx * dx + dy * dy + dz * dz);
+      const double l0 = E.inc_l0[ix];
+      const double stretch = len / l0;
+      const double gg = (1.0 * E.inc_ea[ix]) * (stretch - 1.0) / len;
+      f[0] = f[0] - gg * dx;
+      f[1] = f[1] - gg * dy;
+      f[2] = f[2] - gg * dz;
+    }
+    for (int c = 0; c < 3; ++c) f_emul[3 * pn + c] = f[c];
+  }
+  if (report) {
+    report[0] = de.nsched.steps;
+    report[1] = de.nsched.excess_initial;
+    report[2] = de.nsched.excess;
+    report[3] = de.nsched.n_rows;
   }
   return FIBRA_OK;
 }

@@ -4,6 +4,7 @@
 
 #include "dr_cluster.cuh"
 #include "dr_kernel.cuh"
+#include "dr_node.cuh"
 
 namespace fibra_b200 {
 
@@ -20,7 +21,14 @@ struct ClusterVariant {  // cluster kernel: one cluster of C CTAs per RVE (per-C
   ClusterFn fn[4][2];
 };
 
+struct NodeVariant {  // node-centric kernel: one CTA per RVE, NPT node slots per thread
+  int T, NPT, MINB;
+  KernelFn fn[4][2];
+};
+
 extern const Variant kVariants[];
+extern const NodeVariant kNodeVariants[];
+extern const int kNumNodeVariants;
 extern const int kNumVariants;
 extern const ClusterVariant kClusterVariants[];
 extern const int kNumClusterVariants;

@@ -224,11 +224,14 @@ def test_config3_regressions(oracle_lib, p, force):
     check_states(st, ost, points=[p_ for p_ in range(1) if not status[p_]])
 
 
-def test_multiclass_head_launches_tangent(oracle_lib):
-    """Four config-3 networks in four kernel classes (two resident shapes, a large resident
-    shape, a 2-CTA cluster) with the tangent: the multi-class path launches a head and a body
-    grid per class on one ticket queue, and probes follow base completion across both
-    launches -- records and states bitwise."""
+@pytest.mark.parametrize("kernel", ["edge", "node"])
+def test_multiclass_head_launches_tangent(oracle_lib, monkeypatch, kernel):
+    """Four config-3 networks in several kernel classes (edge kernel: two resident shapes, a
+    large resident shape, a 2-CTA cluster; node kernel: two node shapes and a 2-CTA cluster)
+    with the tangent: the multi-class path launches a head and a body grid per class on one
+    ticket queue, and probes follow base completion across both launches -- records and
+    states bitwise."""
+    monkeypatch.setenv("FIBRA_KERNEL", kernel)
     pairs = [config3_pair(p) for p in (1439, 27, 0, 5)]
     pn, on = [q[0] for q in pairs], [q[1] for q in pairs]
     eop = [0, 1, 2, 3, 3, 2, 1, 0]
@@ -236,7 +239,7 @@ def test_multiclass_head_launches_tangent(oracle_lib):
     relax = P.RelaxConfig(tolerance=1e-4)
     br, st, shapes = run(pn, eop, F, tangent=True, relax=relax)
     kinds = {(s["cluster"], s["threads"], s["fibers_per_thread"]) for s in shapes}
-    assert len(kinds) == 4, shapes
+    assert len(kinds) == (4 if kernel == "edge" else 3), shapes
     resp, status, ost = oracle_batch(on, eop, F, tangent=True,
                                      relax=O.RelaxConfig(tolerance=1e-4))
     assert not any(status), status

@@ -1,0 +1,99 @@
+"""GPU parity against the REFERENCE build at batch scale, every bit of every point.
+
+The fixtures (tests/golden/config*_*.json) were made on the CPU by
+tests/golden/make_golden_batches.py: the reference's own network generator, and every DR
+solve and homogenized stress from the reference's compiled relax_solve /
+homogenized_stress (oracle/_ref, WorkerPool over all cores), with the Eigen steps from the
+oracle's Eigen 3.4.0 restatement.  Here the same batches run through the C-ABI on the B200:
+  * config 2: all 1,024 points (non-symmetric F, so the polar step is on the path), stress
+    only -- status, failed set (the 45 points at the 500k-iteration cap included), base
+    iteration count and sigma bits;                                    batch.cpp:155-187
+  * config 5: 64 config-3 networks with base + 6 warm probes + tangent -- status,
+    iterations of all 7 solves, sigma and spatial C bits;             stiffness.cpp:153-175
+  * config 3: every point the GPU batch fails (140, all at the cap) plus 64 converged
+    ones, stress only.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2306_09427_b200 as P
+from paper_2306_09427_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def fixture(name):
+    path = os.path.join(HERE, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated (tests/golden/make_golden_batches.py)")
+    with open(path) as fh:
+        return json.load(fh)
+
+
+def hexbits(lst):
+    return np.array([float.fromhex(x) for x in lst]).view(np.uint64)
+
+
+def run(nets, eop, F, tangent):
+    lib = P.RveLibrary(list(nets), policy="explicit", explicit_assignment=[int(e) for e in eop])
+    st, assign = P.init_batch(np.zeros(len(eop), np.int32), lib, 0)
+    return P.batch_response(lib, assign, st, P.FiberLaw(), F, P.RelaxConfig(),
+                            P.StiffnessConfig(), want_tangent=tangent)
+
+
+def compare(br, pts, tangent):
+    bad = []
+    for i, fx in enumerate(pts):
+        r = br.records[i]
+        ok = int(r["status"] != 0) == int(fx["status"] != 0)
+        if fx["status"] == 0:
+            ok &= int(r["base_report"]["iterations"]) == fx["base_iterations"]
+            ok &= np.array_equal(np.asarray(r["sigma"]).view(np.uint64), hexbits(fx["sigma"]))
+            if tangent:
+                ok &= int(r["relax_iterations"]) == fx["relax_iterations"]
+                ok &= int(r["solves"]) == fx["solves"] == 7
+                ok &= np.array_equal(np.asarray(r["spatial_c"]).reshape(36).view(np.uint64),
+                                     hexbits(fx["spatial_c"]))
+        elif not tangent or fx["solves"] == 0:  # base failure: the cap, as the reference
+            ok &= int(r["base_report"]["iterations"]) == fx["base_iterations"]
+        if not ok:
+            bad.append(fx["p"])
+    return bad
+
+
+def test_config2_full_batch_vs_reference():
+    fx = fixture("config2_full.json")
+    pts = fx["points"]
+    net = P.generate_network(synth.config1_spec(), 1)
+    F = synth.batch_F(len(pts))
+    br = run([net], np.zeros(len(pts), np.int32), F, tangent=False)
+    assert br.failed == [q["p"] for q in pts if q["status"] != 0]
+    assert len(br.failed) == 45
+    assert compare(br, pts, tangent=False) == []
+
+
+def test_config5_sample_vs_reference():
+    fx = fixture("config5_sample.json")
+    pts = fx["points"]
+    ids = [q["p"] for q in pts]
+    nets = synth.parallel_networks(synth.config3_network, ids)
+    F = synth.batch_F(max(ids) + 1).reshape(-1, 9)[ids]
+    br = run(nets, np.arange(len(ids)), F, tangent=True)
+    assert [ids[i] for i in br.failed] == [q["p"] for q in pts if q["status"] != 0]
+    assert compare(br, pts, tangent=True) == []
+
+
+def test_config3_sample_vs_reference():
+    fx = fixture("config3_sample.json")
+    pts = fx["points"]
+    ids = [q["p"] for q in pts]
+    nets = synth.parallel_networks(synth.config3_network, ids)
+    F = synth.batch_F(synth.CONFIG3_POINTS).reshape(-1, 9)[ids]
+    br = run(nets, np.arange(len(ids)), F, tangent=False)
+    assert [ids[i] for i in br.failed] == [q["p"] for q in pts if q["status"] != 0]
+    assert compare(br, pts, tangent=False) == []

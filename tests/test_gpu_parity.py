@@ -238,3 +238,23 @@ def test_cpp_dropin_shim_bitwise():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "OK" in r.stdout
+
+
+def test_node_kernel_config1_batch_bitwise(oracle_lib, monkeypatch):
+    """The opt-in node-centric kernel (FIBRA_KERNEL=node, csrc/dr_node.cuh): every fibre
+    evaluated at both ends with d' = x_other - x_own, one barrier per iteration -- records
+    and PackedStates bitwise against the oracle on 8 config-1 RVEs, with the tangent."""
+    monkeypatch.setenv("FIBRA_KERNEL", "node")
+    pn, on = knn(375, 1000, 1)
+    F = batch_F(8)
+    br, gst = gpu_batch([pn], [0] * 8, F, tangent=True)
+    resp, status, ost = oracle_batch([on], [0] * 8, F, tangent=True)
+    assert list(np.nonzero(status)[0]) == br.failed
+    for p in range(8):
+        if status[p]:
+            continue
+        r = br.records[p]
+        assert r["relax_iterations"] == resp[p]["relax_iterations"]
+        assert same_bits(r["sigma"], resp[p]["sigma"])
+        assert same_bits(r["spatial_c"].reshape(6, 6), resp[p]["spatial_c"])
+    check_states(gst, ost)

@@ -240,3 +240,33 @@ def test_reference_arm_workload_matches_product():
         assert len(sl) == steps
         assert len(set(np.concatenate(sl).tolist())) == 1024 or steps * len(sl[0]) < 1024
         assert min(len(s) for s in sl) >= 32
+
+
+def test_node_kernel_force_emulation_bitwise():
+    """Node-centric kernel tables (fibra_debug_node_forces, host emulation of one force pass
+    from the uploaded incidence tables with d' = x_other - x_own, f -= g d' from +0.0): the
+    same bits as the reference force loop (oracle internal_forces, network.cpp:275-311) on
+    config-1 and small knn networks, for every node shape that holds them."""
+    import oracle as O
+    from paper_2306_09427_b200 import _capi, synth
+    lib = _capi.load()
+    O.build(ref=False)
+    for spec, seed in ((synth.config1_spec(), 1),
+                       (P.NetGenSpec(style="knn", nodes=20, fibers=56, neighbors=10), 31)):
+        net = P.generate_network(spec, seed)
+        on = O.Network(net.coords, net.fiber_nodes[:, 0], net.fiber_nodes[:, 1],
+                       net.fiber_area, net.fiber_modulus)
+        checked = 0
+        for sh in range(5):
+            u = np.random.default_rng(sh).normal(0, 0.01, net.n_dof)
+            fe = np.zeros(net.n_dof)
+            rep = np.zeros(4, np.int64)
+            r = lib.fibra_debug_node_forces(net.desc(), sh, u.ctypes.data_as(_capi._dp),
+                                            fe.ctypes.data_as(_capi._dp),
+                                            rep.ctypes.data_as(_capi._lp))
+            if r:
+                continue
+            checked += 1
+            assert np.array_equal(fe.view(np.uint64), O.internal_forces(on, u).view(np.uint64))
+            assert rep[2] <= rep[1]  # the placement search never adds bank conflicts
+        assert checked >= 3

@@ -357,3 +357,34 @@ def test_batch_threads_bitwise_equal_sequential(oracle_lib):  # test_batch.cpp:1
         assert np.array_equal(a["sigma"], b["sigma"]) and np.array_equal(a["spatial_c"], b["spatial_c"])
     for k in ("u", "v", "f_int"):
         assert np.array_equal(st1.arrays[k], st4.arrays[k])
+
+
+def test_config2_fixture_pins_polar_and_solves(oracle_lib):
+    """tests/golden/config2_full.json (reference build, make_golden_batches.py): the oracle's
+    Eigen 3.4.0 polar restatement reproduces the fixture's U bits for all 1,024 config-2 F,
+    and the oracle's relax reproduces the reference's iterations and sigma on the cheapest
+    points (the GPU suite checks all of them)."""
+    import json
+    import os
+    from oracle import workload as W
+    path = os.path.join(os.path.dirname(__file__), "golden", "config2_full.json")
+    with open(path) as fh:
+        pts = json.load(fh)["points"]
+    F = W.batch_F(len(pts))
+    for q in pts:
+        R, U = O.polar_decompose(F[q["p"]])
+        assert list(U.view(np.uint64)) == [np.float64(float.fromhex(x)).view(np.uint64)
+                                           for x in q["U"]], q["p"]
+    cheap = sorted((q for q in pts if q["status"] == 0), key=lambda q: q["base_iterations"])[:4]
+    import paper_2306_09427_b200 as P
+    from paper_2306_09427_b200 import synth
+    pn = P.generate_network(synth.config1_spec(), 1)
+    on = O.Network(pn.coords, pn.fiber_nodes[:, 0], pn.fiber_nodes[:, 1], pn.fiber_area,
+                   pn.fiber_modulus, pn.box_half)
+    ids = [q["p"] for q in cheap]
+    st = O.PackedStates.fresh([on], [0] * len(ids))
+    resp, status = O.batch_response([on], [0] * len(ids), st, F[ids], want_tangent=False)
+    for i, q in enumerate(cheap):
+        assert status[i] == 0
+        assert resp[i]["base_report"]["iterations"] == q["base_iterations"]
+        assert [float(x).hex() for x in resp[i]["sigma"]] == q["sigma"]

@@ -1,42 +1,47 @@
-"""Aggregate an ncu 'source' page (cuda,sass CSV) per CUDA source line."""
+"""Per-CUDA-line totals from an ncu 'source' page (cuda,sass CSV), normalised per unit.
+
+usage: ncu_lines2.py <csv> <units> [min_instr_per_unit]
+"""
 import csv
 import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
+N = float(sys.argv[2])
+lim = float(sys.argv[3]) if len(sys.argv) > 3 else 8
 hdr = None
-agg = defaultdict(lambda: defaultdict(float))
+fname = "?"
+agg = defaultdict(lambda: [0.0, 0.0, 0.0])
 src = {}
 cur = None
 for r in rows:
+    if r and r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
     if len(r) > 4 and r[0] == "Line No":
         hdr = r
         continue
     if hdr is None or len(r) != len(hdr):
         continue
     if r[0]:
-        cur = int(r[0])
-        src[cur] = r[1][:90]
+        cur = (fname, int(r[0]))
+        src[cur] = r[1][:80]
         continue
     d = dict(zip(hdr, r))
-    for k in ("Warp Stall Sampling (All Samples)", "Instructions Executed",
-              "L1 Wavefronts Shared", "L1 Wavefronts Shared Ideal", "stall_barrier",
-              "stall_short_sb", "stall_long_sb", "stall_math", "stall_mio", "stall_wait",
-              "stall_lg", "stall_not_selected", "stall_selected", "stall_branch_resolving",
-              "stall_dispatch", "stall_no_inst"):
+
+    def f(k):
         try:
-            agg[cur][k] += float(d.get(k, 0) or 0)
+            return float(d.get(k, 0) or 0)
         except ValueError:
-            pass
-tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
-toti = sum(v["Instructions Executed"] for v in agg.values())
-print(f"total samples {tot:.0f} instructions {toti:.3g}")
-keys = ["stall_barrier", "stall_short_sb", "stall_long_sb", "stall_math", "stall_mio",
-        "stall_wait", "stall_lg", "stall_not_selected", "stall_selected", "stall_branch_resolving",
-        "stall_dispatch", "stall_no_inst"]
-top = sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:int(sys.argv[2]) if len(sys.argv) > 2 else 30]
-for line, v in top:
-    s = v["Warp Stall Sampling (All Samples)"]
-    st = ", ".join(f"{k[6:]}={v[k]/max(s,1)*100:.0f}%" for k in keys if v[k] / max(s, 1) > 0.08)
-    print(f"{line:4d} {s/tot*100:5.1f}% inst {v['Instructions Executed']/toti*100:5.1f}% "
-          f"wf {v['L1 Wavefronts Shared']:.3g}/{v['L1 Wavefronts Shared Ideal']:.3g} | {src.get(line,'')} | {st}")
+            return 0.0
+    a = agg[cur]
+    a[0] += f("Instructions Executed") / N
+    a[1] += f("Warp Stall Sampling (All Samples)")
+    a[2] += f("L1 Wavefronts Shared") / N
+tots = sum(v[1] for v in agg.values()) or 1
+tot_i = sum(v[0] for v in agg.values())
+print(f"total instructions/unit {tot_i:.1f}")
+for k in sorted(k for k in agg if k):
+    v = agg[k]
+    if v[0] >= lim or v[1] / tots > 0.004:
+        print(f"{k[0][:10]:>10}:{k[1]:<4} {v[0]:7.1f} st={v[1]/tots*100:5.1f}% wf={v[2]:6.1f}  {src.get(k, '')}")
