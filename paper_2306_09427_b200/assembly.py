@@ -184,9 +184,23 @@ class MacroAssembler:
             responses[:, :6] = np.asarray(sigma, dtype=np.float64).reshape(n, 6)
             responses[:, 6:] = np.asarray(spatial_c, dtype=np.float64).reshape(n, 36)
             stride = 42
-        resp = np.ascontiguousarray(responses).view(np.float64).reshape(-1)
+        responses = np.asarray(responses)
+        if responses.dtype.names is not None:  # record array (e.g. RESULT_DTYPE): raw bytes
+            if responses.dtype.itemsize % 8:
+                raise ValueError("response records must be a whole number of doubles")
+            resp = np.ascontiguousarray(responses).view(np.float64).reshape(-1)
+        else:  # numeric input is converted, never reinterpreted
+            resp = np.ascontiguousarray(responses, dtype=np.float64).reshape(-1)
+        if stride < 42 or resp.size < stride * n:
+            raise ValueError(f"responses hold {resp.size} doubles, {n} elements x stride "
+                             f"{stride} (>= 42) needed")
         x = np.ascontiguousarray(coords, dtype=np.float64)
+        if x.size != 3 * self.mesh.n_nodes:
+            raise ValueError(f"coords must be ({self.mesh.n_nodes}, 3)")
+        x = x.reshape(-1)
         fe = None if f_ext_free is None else np.ascontiguousarray(f_ext_free, dtype=np.float64)
+        if fe is not None and fe.size != self.numbering.n_free:
+            raise ValueError(f"f_ext_free must have n_free = {self.numbering.n_free} entries")
         if out is None:
             res, vals = np.zeros(self.numbering.n_free), np.zeros(self.nnz)
         else:

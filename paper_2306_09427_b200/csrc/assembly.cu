@@ -418,8 +418,19 @@ int fibra_cuda_assembly_create(int device, const int32_t* tets, int32_t n_tets, 
   if (static_cast<long long>(n_tets) >= (1LL << 28)) return FIBRA_E_ARG;  // contrib encoding
   for (long long i = 0; i < 4LL * n_tets; ++i)
     if (tets[i] < 0 || tets[i] >= n_nodes) return FIBRA_E_ARG;
-  for (long long d = 0; d < 3LL * n_nodes; ++d)
-    if (free_of_dof[d] >= n_free) return FIBRA_E_ARG;
+  // the compressed column pattern below assumes the free slots are exactly 0..n_free-1 in
+  // ascending DOF order (build_numbering, macrofem.cpp:22-38): rows then ascend in every
+  // column and no two DOFs share a slot
+  {
+    int32_t next = 0;
+    for (long long d = 0; d < 3LL * n_nodes; ++d) {
+      const int32_t f = free_of_dof[d];
+      if (f < 0) continue;
+      if (f != next) return FIBRA_E_ARG;
+      ++next;
+    }
+    if (next != n_free) return FIBRA_E_ARG;
+  }
   auto* as = new fibra_assembly();
   as->device = device;
   as->n_tets = n_tets, as->n_nodes = n_nodes, as->n_free = n_free;

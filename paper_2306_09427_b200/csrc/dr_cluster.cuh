@@ -434,10 +434,10 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
             dz[jj] = xb_[2] - xa_[2];
             bool o1, o2, o3 = true;
             const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
-            collapsed |= le_nonneg_bits(len, 1e-8 * fl0[j]);  // len <= 1e-8 l0, network.cpp:291
-            const double stretch = div_fast_i(len, fl0[j], o2);
+            collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
+            const double stretch = div_fast(len, fl0[j], o2);
             if (LAW == 0) {
-              g[jj] = div_fast_i(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+              g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
             } else {
               g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
               const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));

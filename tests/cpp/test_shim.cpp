@@ -9,33 +9,15 @@
 
 #include "fibra/netgen.hpp"
 #include "fibra_b200/batch_response.hpp"
+#include "fibra_b200/network_batch_provider.hpp"
 #include "fibra_oracle.h"
 
 using namespace fibra;
 
 static double u01(std::mt19937_64& r) { return static_cast<double>(r() >> 11) * 0x1.0p-53; }
 
-int main() {
-  RveLibrary lib;
-  NetGenSpec spec;
-  spec.style = NetGenSpec::Style::knn;
-  spec.nodes = 14;
-  spec.fibers = 38;
-  spec.neighbors = 9;
-  lib.entries.push_back(generate_network(spec, 101));
-  spec.nodes = 12;
-  spec.fibers = 32;
-  lib.entries.push_back(generate_network(spec, 102));
-  // a 1,900-fibre network: one CTA of a large resident shape (8-byte record offsets)
-  spec.nodes = 712;
-  spec.fibers = 1900;
-  spec.neighbors = 10;
-  lib.entries.push_back(generate_network(spec, 7));
-  const int n_entries = 3;
-  const int n = 8;
-  BatchAssignment assign;
-  std::mt19937_64 pick(7);
-  for (int p = 0; p < n; ++p) assign.entry_of_point.push_back(static_cast<int32_t>(pick() % n_entries));
+static PackedStates fresh_states(const RveLibrary& lib, const BatchAssignment& assign) {
+  const int n = static_cast<int>(assign.entry_of_point.size());
   PackedStates st;  // init_batch (batch.cpp:94-145) without the Eigen-dependent TU
   st.offsets.assign(n + 1, 0);
   for (int p = 0; p < n; ++p) {
@@ -48,6 +30,10 @@ int main() {
   st.t.assign(n, 0.0);
   st.iters.assign(n, 0);
   st.converged.assign(n, 0);
+  return st;
+}
+
+static std::vector<Def3> batch_defs(int n) {
   std::vector<Def3> fs;
   std::mt19937_64 rng(55);  // test_batch.cpp:149-157
   for (int p = 0; p < n; ++p) {
@@ -57,6 +43,19 @@ int main() {
     f(0, 1) += 0.0 + 0.02 * u01(rng);
     fs.push_back(f);
   }
+  return fs;
+}
+
+// batch_response through the drop-in vs the oracle on `lib`: sigma, C, stats, PackedStates
+static int run_case(RveLibrary& lib, uint64_t pick_seed) {
+  const int n_entries = static_cast<int>(lib.entries.size());
+  const int n = 8;
+  BatchAssignment assign;
+  std::mt19937_64 pick(pick_seed);
+  for (int p = 0; p < n; ++p) assign.entry_of_point.push_back(static_cast<int32_t>(pick() % n_entries));
+  PackedStates st = fresh_states(lib, assign);
+  const size_t tot = st.offsets.back();
+  const std::vector<Def3> fs = batch_defs(n);
   WorkerPool pool(1);
   const BatchResult br = fibra_b200::batch_response(lib, assign, st, FiberLaw{}, fs, RelaxConfig{},
                                                     StiffnessConfig{}, pool);
@@ -104,7 +103,94 @@ int main() {
   bad += !br.failed.empty();
   bad += std::memcmp(st.u.data(), u.data(), tot * 8) != 0;
   bad += std::memcmp(st.f_int.data(), fi.data(), tot * 8) != 0;
-  std::printf("%s: %d mismatches over %d points (sigma, C, stats, PackedStates)\n",
-              bad ? "FAIL" : "OK", bad, n);
+  for (auto& o : onets) or_network_free(&o);
+  return bad;
+}
+
+static RveLibrary make_library(bool large) {
+  RveLibrary lib;
+  NetGenSpec spec;
+  spec.style = NetGenSpec::Style::knn;
+  spec.nodes = 14;
+  spec.fibers = 38;
+  spec.neighbors = 9;
+  lib.entries.push_back(generate_network(spec, 101));
+  spec.nodes = 12;
+  spec.fibers = 32;
+  lib.entries.push_back(generate_network(spec, 102));
+  if (large) {  // a 1,900-fibre network: one CTA of a large resident shape
+    spec.nodes = 712;
+    spec.fibers = 1900;
+    spec.neighbors = 10;
+    lib.entries.push_back(generate_network(spec, 7));
+  } else {
+    spec.nodes = 20;
+    spec.fibers = 56;
+    spec.neighbors = 10;
+    lib.entries.push_back(generate_network(spec, 31));
+  }
+  return lib;
+}
+
+int main() {
+  int bad = 0;
+  // 1. the drop-in against the oracle
+  RveLibrary lib = make_library(true);
+  int b = run_case(lib, 7);
+  std::printf("batch_response: %d mismatches\n", b);
+  bad += b;
+  // 2. the same RveLibrary object edited in place: the content-keyed context re-uploads
+  lib.entries = make_library(false).entries;
+  b = run_case(lib, 9);
+  std::printf("library edited in place: %d mismatches\n", b);
+  bad += b;
+  // 3. a PackedStates that does not match the library is a ConfigError, before any copy
+  {
+    BatchAssignment assign;
+    assign.entry_of_point = {0, 1};
+    PackedStates st = fresh_states(lib, assign);
+    st.u.resize(st.u.size() - 3);
+    const std::vector<Def3> fs = batch_defs(2);
+    WorkerPool pool(1);
+    bool threw = false;
+    try {
+      fibra_b200::batch_response(lib, assign, st, FiberLaw{}, fs, RelaxConfig{}, StiffnessConfig{}, pool);
+    } catch (const ConfigError&) {
+      threw = true;
+    }
+    std::printf("state layout mismatch throws ConfigError: %s\n", threw ? "yes" : "NO");
+    bad += !threw;
+  }
+  // 4. device-resident provider over two Newton-like calls == batch_response on host states
+  {
+    BatchAssignment assign;
+    assign.entry_of_point = {0, 1, 2, 0, 2, 1};
+    const int n = 6;
+    std::vector<Def3> f1 = batch_defs(n), f2 = f1;
+    for (auto& f : f2) f(0, 0) += 0.002;
+    fibra_b200::NetworkBatchProvider prov(lib, fresh_states(lib, assign), assign, FiberLaw{},
+                                          RelaxConfig{}, StiffnessConfig{});
+    PackedStates host = fresh_states(lib, assign);
+    WorkerPool pool(1);
+    int pb = 0;
+    for (const auto* fs : {&f1, &f2}) {
+      const ProviderResult pr = prov.respond(*fs);
+      const BatchResult br = fibra_b200::batch_response(lib, assign, host, FiberLaw{}, *fs,
+                                                        RelaxConfig{}, StiffnessConfig{}, pool);
+      pb += pr.failed_points != br.failed;
+      for (int p = 0; p < n; ++p) {
+        pb += std::memcmp(&pr.responses[p].sigma, &br.responses[p].sigma, sizeof(SymTensor3)) != 0;
+        pb += std::memcmp(&pr.responses[p].spatial_c, &br.responses[p].spatial_c, sizeof(Mandel66)) != 0;
+      }
+    }
+    PackedStates& ps = prov.states();
+    pb += std::memcmp(ps.u.data(), host.u.data(), host.u.size() * 8) != 0;
+    pb += std::memcmp(ps.f_int.data(), host.f_int.data(), host.f_int.size() * 8) != 0;
+    pb += ps.iters != host.iters;
+    std::printf("device-resident provider (2 calls): %d mismatches, warm iterations %lld\n", pb,
+                static_cast<long long>(ps.iters[0]));
+    bad += pb;
+  }
+  std::printf("%s: %d mismatches (sigma, C, stats, PackedStates, provider)\n", bad ? "FAIL" : "OK", bad);
   return bad ? 1 : 0;
 }

@@ -151,3 +151,21 @@ def test_error_order(oracle_lib):  # macrofem.cpp:118-132: first failing element
         O.assemble(mesh.tets, mesh.coords.ravel(), np.zeros((n, 6)), cm, num.free_of_dof,
                    num.n_free, f)
     assert ei.value.code == 11
+
+
+def test_assembly_create_rejects_bad_numbering():
+    """fibra_cuda_assembly_create validates the DOF numbering before any device work: free
+    slots must be 0..n_free-1 in ascending DOF order (build_numbering, macrofem.cpp:22-38),
+    else FIBRA_E_ARG (a shared or out-of-order slot would break the CSC pattern)."""
+    import ctypes as C
+    from paper_2306_09427_b200 import _capi
+    L = _capi.load()
+    tets = np.array([0, 1, 2, 3], np.int32)
+    h = C.c_void_p()
+    for fod in ([0, 1, 2, -1, -1, -1, 3, 4, 5, -1, -1, 5],   # slot 5 twice
+                [1, 0, 2, -1, -1, -1, 3, 4, 5, -1, -1, -1],  # descending
+                [0, 1, 2, -1, -1, -1, 3, 4, 6, -1, -1, -1]):  # gap
+        f = np.array(fod, np.int32)
+        rc = L.fibra_cuda_assembly_create(0, tets.ctypes.data_as(_capi._ip), 1, 4,
+                                          f.ctypes.data_as(_capi._ip), 6, C.byref(h))
+        assert rc == 21, fod  # FIBRA_E_ARG
