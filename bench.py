@@ -69,6 +69,10 @@ def parse():
     ap.add_argument("--tangent", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--single-process", action="store_true",
+                    help="one process drives all --gpus through the library's multi-device "
+                         "context (fibra_cuda_open_devices: LPT shards, one ncclAllGather); "
+                         "run without torchrun")
     a = ap.parse_args()
     if a.points is None:
         a.points = DEFAULT_POINTS[a.config]
@@ -77,17 +81,28 @@ def parse():
     return a
 
 
-def workload(args, world, rank):
+def proxy_cost(m, n):
+    """The library's schedule cost model without the network-specific degree term (computable
+    from the config-3 recipe alone, so every rank plans without building all networks)."""
+    return np.exp(-3.3 * m / n + 1.75 * np.log(m)) * m
+
+
+def workload(args, world, rank, full=False):
     """(networks, entry_of_point, F (n, 9), description, global point count, scaling) of
-    this rank's shard."""
+    this rank's shard (``full``: the whole batch of all ``world`` GPUs, for one process).
+    Configs 3-5 shard by longest-processing-time on the cost model (shard.plan_shards)."""
     import paper_2306_09427_b200 as P
     from paper_2306_09427_b200 import synth
-    from paper_2306_09427_b200.shard import shard_ranges
+    from paper_2306_09427_b200.shard import plan_shards
     tangent = args.tangent
     if args.config == 2:
         points = args.points
         net = P.generate_network(synth.config1_spec(), NET_SEED)
         F_all = synth.batch_F(points * world)
+        if full:
+            F = np.ascontiguousarray(F_all).reshape(points * world, 9)
+            desc = describe(args, world, points, points * world, "weak", net.n_free)[0]
+            return [net], np.zeros(points * world, np.int32), F, desc, points * world, "weak"
         F = np.ascontiguousarray(F_all[rank * points:(rank + 1) * points]).reshape(points, 9)
         desc = (f"config{5 if tangent else 2}: {points} same-topology knn RVEs per GPU "
                 f"(375 nodes/1000 fibers, seed {NET_SEED}, n_free {net.n_free}), distinct F "
@@ -95,20 +110,21 @@ def workload(args, world, rank):
         return [net], np.zeros(points, np.int32), F, desc, points * world, "weak"
     total = args.points
     if args.config == 4:
-        sizes = np.full(total, 50000)
+        cost = np.full(total, 50000.0)
         make = synth.config4_network
     else:
-        sizes = np.array([synth.config3_size(p)[0] for p in range(total)])
+        mn = np.array([synth.config3_size(p) for p in range(total)], dtype=np.float64)
+        cost = proxy_cost(mn[:, 0], mn[:, 1])
         make = synth.config3_network
-    lo, hi = shard_ranges(sizes, world)[rank]
-    nets = synth.parallel_networks(make, range(lo, hi))
-    F = np.ascontiguousarray(synth.batch_F(total)[lo:hi]).reshape(hi - lo, 9)
+    pts = np.arange(total) if full else plan_shards(cost, world)[rank]
+    nets = synth.parallel_networks(make, [int(p) for p in pts])
+    F = np.ascontiguousarray(synth.batch_F(total)[pts]).reshape(len(pts), 9)
     kind = {3: "heterogeneous knn RVEs of 500-5k fibers (SURVEY 8d recipe, one network per point)",
             4: "jittered-lattice RVEs of 50k fibers / 12,167 nodes (16-CTA clusters)",
             5: "config-3 RVEs (first 4,096), base + 6 warm probes + tangent"}[args.config]
     desc = (f"config{args.config}: {total} {kind}, distinct F (mt19937_64(55) recipe), "
-            f"fiber-weighted contiguous shards")
-    return nets, np.arange(hi - lo, dtype=np.int32), F, desc, total, "strong"
+            f"longest-processing-time shards on the cost model")
+    return nets, np.arange(len(pts), dtype=np.int32), F, desc, total, "strong"
 
 
 def describe(args, world, n_per_gpu, total, scaling, n_free):
@@ -123,7 +139,7 @@ def describe(args, world, n_per_gpu, total, scaling, n_free):
                 4: "jittered-lattice RVEs of 50k fibers / 12,167 nodes (16-CTA clusters)",
                 5: "config-3 RVEs (first 4,096), base + 6 warm probes + tangent"}[args.config]
         desc = (f"config{args.config}: {total} {kind}, distinct F (mt19937_64(55) recipe), "
-                f"fiber-weighted contiguous shards")
+                f"longest-processing-time shards on the cost model")
     cfg = {"workload": desc, "points_per_gpu": n_per_gpu, "global_points": total,
            "l2": "flushed between timed steps (256 MiB device write)",
            "parallelism": f"dp{world} (independent RVE shards, 1 NCCL all-gather "
@@ -330,16 +346,25 @@ def main():
     import torch.distributed as dist
     import paper_2306_09427_b200 as P
 
+    sp = args.single_process and args.gpus > 1  # one process, the library's multi-device path
+    devices = list(range(args.gpus)) if sp else None
+    ngpu = args.gpus if sp else world
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    nets, eop, F, desc, total, scaling = workload(args, world, rank)
+    if sp:
+        nets, eop, F, desc, total, scaling = workload(args, args.gpus, 0, full=True)
+    else:
+        nets, eop, F, desc, total, scaling = workload(args, world, rank)
     n = len(F)
     lib = P.RveLibrary(nets, policy="explicit", explicit_assignment=[int(e) for e in eop])
     assign = P.BatchAssignment(eop)
     stream = torch.cuda.Stream(device=local)  # explicit stream shared by torch and the solver
     torch.cuda.set_stream(stream)
-    db = P.DeviceBatch(lib, assign, device=local, stream=stream.cuda_stream)
+    if sp:
+        db = P.DeviceBatch(lib, assign, device=0, devices=devices)
+    else:
+        db = P.DeviceBatch(lib, assign, device=local, stream=stream.cuda_stream)
     peak = db.fp64_peak()  # FP64-pipe roofline denominator, measured while the GPU is idle
     rec_bytes = P.RESULT_DTYPE.itemsize
     F_dev = torch.from_numpy(F).to(f"cuda:{local}")
@@ -378,8 +403,12 @@ def main():
         step()
         ev1.record(stream)
         torch.cuda.synchronize()
-        total_ms += ev0.elapsed_time(ev1)
         s = db.last_stats()
+        if sp:  # the devices run on the library's streams: its events on device 0 span the
+            db.synchronize()  # F gather, every device's solve, the all-gather and the permute
+            total_ms += s["total_ms"]
+        else:
+            total_ms += ev0.elapsed_time(ev1)
         dr_ms += s["dr_kernel_ms"]
         iters += s["iterations"]
         pipe_ops += s["pipe_ops"]
@@ -414,7 +443,7 @@ def main():
             dist.barrier()
         t0 = time.perf_counter()
         br = P.batch_response(lib, assign, st_host, law, F, rcfg, scfg,
-                              want_tangent=args.tangent, device=local)
+                              want_tangent=args.tangent, device=local, devices=devices)
         if world > 1:
             g = torch.zeros(n_pad * rec_bytes, dtype=torch.uint8, device=f"cuda:{local}")
             g[:n * rec_bytes] = torch.from_numpy(br.records.view(np.uint8).copy()).to(f"cuda:{local}")
@@ -432,14 +461,19 @@ def main():
     d2h = n * rec_bytes + 7 * tot * 8 + n * (8 + 8 + 1)
 
     if rank == 0:
-        achieved = all_pipe / world / (max_dr_ms * 1e-3)  # per-GPU FP64-pipe lane-ops/s
+        achieved = all_pipe / ngpu / (max_dr_ms * 1e-3)  # per-GPU FP64-pipe lane-ops/s
+        cfg = describe(args, ngpu, n // ngpu if sp and args.config == 2 else n, total, scaling,
+                       nets[0].n_free if args.config == 2 else None)[1]
+        if sp:
+            cfg["parallelism"] = (f"dp{ngpu} in one process (fibra_cuda_open_devices: "
+                                  "longest-processing-time shards, 1 ncclAllGather of the "
+                                  "result records per step)")
         line = {
-            "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRICS[args.config], "value": value, "unit": UNIT, "n_gpus": ngpu,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": max_total_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": describe(args, world, n, total, scaling,
-                               nets[0].n_free if args.config == 2 else None)[1],
+            "config": cfg,
             "dr_iter_rve_per_s": all_iters / (max_total_ms * 1e-3) * (args.steps / args.steps),
             "failed_points": failed,
             "roofline": {"bound": "fp64_pipe", "achieved": achieved / 1e9, "peak": peak / 1e9,
@@ -449,9 +483,9 @@ def main():
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
-            "alg_flops": {"achieved_tflops": all_flops / world / (max_dr_ms * 1e-3) / 1e12,
+            "alg_flops": {"achieved_tflops": all_flops / ngpu / (max_dr_ms * 1e-3) / 1e12,
                           "fma_peak_tflops": 2 * peak / 1e12,
-                          "frac": all_flops / world / (max_dr_ms * 1e-3) / (2 * peak),
+                          "frac": all_flops / ngpu / (max_dr_ms * 1e-3) / (2 * peak),
                           "model": "F_alg = 28 M + 12 n_free + 2 n_fix flops per RVE-iteration "
                                    "(div and sqrt count 1; SURVEY 8d); peak = 2 x the measured "
                                    "DADD lane-op rate (FMA-counted)"},

@@ -163,14 +163,20 @@ inline void check_layout(const Ctx& c, const fibra::PackedStates& st) {
     throw fibra::ConfigError("state layout does not match the network");
 }
 
+// open one device, or several GPUs of this process (fibra_cuda_open_devices)
+inline int open_ctx(const std::vector<int32_t>& devices, fibra_ctx** out) {
+  if (devices.size() == 1) return fibra_cuda_open(devices[0], out);
+  return fibra_cuda_open_devices(devices.data(), static_cast<int32_t>(devices.size()), out);
+}
+
 inline Ctx& context(const fibra::RveLibrary& library, const fibra::BatchAssignment& a,
-                    int device) {
-  thread_local std::map<int, std::unique_ptr<Ctx>> cache;
-  auto& slot = cache[device];
+                    const std::vector<int32_t>& devices) {
+  thread_local std::map<std::vector<int32_t>, std::unique_ptr<Ctx>> cache;
+  auto& slot = cache[devices];
   const uint64_t key = library_key(library);
   if (!slot || slot->key != key) {
     slot = std::make_unique<Ctx>();
-    check(fibra_cuda_open(device, &slot->ctx), nullptr);
+    check(open_ctx(devices, &slot->ctx), nullptr);
     upload(*slot, library);
     slot->key = key;
     slot->eop.clear();
@@ -250,13 +256,14 @@ inline fibra::BatchResult batch_response(const fibra::RveLibrary& library,
                                          const fibra::RelaxConfig& relax_cfg,
                                          const fibra::StiffnessConfig& stiff_cfg,
                                          fibra::WorkerPool& /*pool: the GPU grid replaces it*/,
-                                         int device = 0) {
+                                         const std::vector<int32_t>& devices) {
   const int n = states.n_points();
+  if (devices.empty()) throw fibra::ConfigError("no device");
   if (static_cast<int>(deformation.size()) != n)
     throw fibra::ConfigError("one deformation gradient per point is required");
   if (static_cast<int>(assignment.entry_of_point.size()) != n)
     throw fibra::ConfigError("assignment does not match the packed states");
-  detail::Ctx& c = detail::context(library, assignment, device);
+  detail::Ctx& c = detail::context(library, assignment, devices);
   detail::check_layout(c, states);
   detail::check(fibra_cuda_upload_states(c.ctx, states.u.data(), states.t.data(),
                                          states.iters.data(), states.converged.data()),
@@ -275,6 +282,18 @@ inline fibra::BatchResult batch_response(const fibra::RveLibrary& library,
                                            states.converged.data()),
                 c.ctx);
   return detail::to_result(out);
+}
+
+// one B200 (device index) -- the reference signature plus an optional device
+inline fibra::BatchResult batch_response(const fibra::RveLibrary& library,
+                                         const fibra::BatchAssignment& assignment,
+                                         fibra::PackedStates& states, const fibra::FiberLaw& law,
+                                         std::span<const fibra::Def3> deformation,
+                                         const fibra::RelaxConfig& relax_cfg,
+                                         const fibra::StiffnessConfig& stiff_cfg,
+                                         fibra::WorkerPool& pool, int device = 0) {
+  return batch_response(library, assignment, states, law, deformation, relax_cfg, stiff_cfg,
+                        pool, std::vector<int32_t>{device});
 }
 
 }  // namespace fibra_b200

@@ -16,7 +16,8 @@
 // before the next respond().  The next respond() also starts the points that relaxed longest
 // in this one first (fibra_cuda_set_schedule, FIBRA_SCHED_HINT); results do not depend on
 // the order.  `workers` is accepted for signature compatibility: the GPU grid replaces the
-// WorkerPool.
+// WorkerPool.  `devices` lists the GPUs (several: fibra_cuda_open_devices, points sharded
+// across them, the warm states staying on the device that solves their point).
 #pragma once
 
 #include <cstdint>
@@ -35,18 +36,18 @@ class NetworkBatchProvider final : public fibra::ConstitutiveProvider {
  public:
   NetworkBatchProvider(std::span<const std::int32_t> region_of_point, fibra::RveLibrary library,
                        std::uint64_t seed, fibra::FiberLaw law, fibra::RelaxConfig relax_cfg,
-                       fibra::StiffnessConfig stiff_cfg, int /*workers*/, int device = 0)
+                       fibra::StiffnessConfig stiff_cfg, int /*workers*/, std::vector<int32_t> devices = {0})
       : library_(std::move(library)), law_(law), relax_cfg_(relax_cfg), stiff_cfg_(stiff_cfg),
-        device_(device) {
+        devices_(std::move(devices)) {
     auto [states, assignment] = fibra::init_batch(region_of_point, library_, seed);
     states_ = std::move(states);
     assignment_ = std::move(assignment);
   }
   NetworkBatchProvider(const fibra::MacroMesh& mesh, fibra::RveLibrary library, std::uint64_t seed,
                        fibra::FiberLaw law, fibra::RelaxConfig relax_cfg,
-                       fibra::StiffnessConfig stiff_cfg, int /*workers*/, int device = 0)
+                       fibra::StiffnessConfig stiff_cfg, int /*workers*/, std::vector<int32_t> devices = {0})
       : library_(std::move(library)), law_(law), relax_cfg_(relax_cfg), stiff_cfg_(stiff_cfg),
-        device_(device) {
+        devices_(std::move(devices)) {
     auto [states, assignment] = fibra::init_batch(mesh, library_, seed);
     states_ = std::move(states);
     assignment_ = std::move(assignment);
@@ -55,10 +56,10 @@ class NetworkBatchProvider final : public fibra::ConstitutiveProvider {
   NetworkBatchProvider(fibra::RveLibrary library, fibra::PackedStates states,
                        fibra::BatchAssignment assignment, fibra::FiberLaw law,
                        fibra::RelaxConfig relax_cfg, fibra::StiffnessConfig stiff_cfg,
-                       int device = 0)
+                       std::vector<int32_t> devices = {0})
       : library_(std::move(library)), states_(std::move(states)),
         assignment_(std::move(assignment)), law_(law), relax_cfg_(relax_cfg),
-        stiff_cfg_(stiff_cfg), device_(device) {}
+        stiff_cfg_(stiff_cfg), devices_(std::move(devices)) {}
   ~NetworkBatchProvider() override { fibra_cuda_close(ctx_); }
   NetworkBatchProvider(const NetworkBatchProvider&) = delete;
   NetworkBatchProvider& operator=(const NetworkBatchProvider&) = delete;
@@ -139,7 +140,7 @@ class NetworkBatchProvider final : public fibra::ConstitutiveProvider {
   void ensure_device() {
     if (!ctx_) {
       detail::Ctx c;  // owns the context until the library is on the device
-      detail::check(fibra_cuda_open(device_, &c.ctx), nullptr);
+      detail::check(detail::open_ctx(devices_, &c.ctx), nullptr);
       detail::upload(c, library_);
       detail::bind(c, library_, assignment_);
       detail::check_layout(c, states_);
@@ -161,7 +162,7 @@ class NetworkBatchProvider final : public fibra::ConstitutiveProvider {
   fibra::FiberLaw law_;
   fibra::RelaxConfig relax_cfg_;
   fibra::StiffnessConfig stiff_cfg_;
-  int device_ = 0;
+  std::vector<int32_t> devices_;  // one GPU, or several of this process
   fibra_ctx* ctx_ = nullptr;
   bool device_newer_ = false;  // HBM holds states the host copy has not seen
   bool host_newer_ = true;     // the host copy may hold edits the device has not seen

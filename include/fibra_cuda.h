@@ -183,6 +183,22 @@ typedef struct {          /* per-call counters for reporting                    
 typedef struct fibra_ctx fibra_ctx;
 
 int fibra_cuda_open(int device, fibra_ctx** out);
+/* One context over several GPUs of this process (the reference's single-process
+ * batch_response, batch.cpp:155-187, on 1/2/4/8 B200).  The library is replicated on every
+ * device; bind_points splits the points into per-device shards by longest-processing-time
+ * on the per-point cost (fibra_plan_shards: the entry's topology cost at bind time, the
+ * caller's FIBRA_SCHED_HINT costs afterwards -- a new hint re-plans and moves the warm
+ * states of the points that change device); every call solves the shards concurrently and
+ * returns the 760-byte records with ONE ncclAllGather over NVLink (NCCL loaded at run time)
+ * plus a permutation into point order on the first device.  All other calls behave as on
+ * a single-device context; F_dev / out_dev of solve_device live on devices[0]. */
+int fibra_cuda_open_devices(const int32_t* devices, int32_t n_dev, fibra_ctx** out);
+/* Host only: devices of n points by longest-processing-time on cost[] (descending cost,
+ * each point to the least-loaded device, ties to the lower index; deterministic). */
+int fibra_plan_shards(const double* cost, int32_t n, int32_t n_dev, int32_t* dev_of_point);
+/* Host only: the schedule cost model's work estimate of one network, exp(log iterations)
+ * x fibres, with the topology term of the input-only model. */
+int fibra_network_cost(const fibra_net_desc* net, double* cost);
 int fibra_cuda_close(fibra_ctx* ctx);
 const char* fibra_cuda_last_error(const fibra_ctx* ctx);
 /* use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = own */

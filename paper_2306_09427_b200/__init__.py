@@ -363,11 +363,21 @@ class DeviceBatch:
     """
 
     def __init__(self, library: RveLibrary, assignment: BatchAssignment, device: int = 0,
-                 stream: Optional[int] = None):
+                 stream: Optional[int] = None, devices: Optional[Sequence[int]] = None):
+        """``devices``: several GPUs of this process (fibra_cuda_open_devices): the library
+        is replicated, the points are sharded by longest-processing-time on their cost, and
+        the records come back through one NCCL all-gather; device pointers of
+        ``solve_device`` then live on ``devices[0]``."""
         L = _capi.load()
         self._L = L
         self._ctx = C.c_void_p()
-        self._check(L.fibra_cuda_open(device, C.byref(self._ctx)), ctx=False)
+        self.devices = [int(d) for d in devices] if devices else [int(device)]
+        if len(self.devices) > 1:
+            devs = np.ascontiguousarray(self.devices, dtype=np.int32)
+            self._check(L.fibra_cuda_open_devices(_ptr(devs, _capi._ip), len(devs),
+                                                  C.byref(self._ctx)), ctx=False)
+        else:
+            self._check(L.fibra_cuda_open(self.devices[0], C.byref(self._ctx)), ctx=False)
         if stream:
             self._check(L.fibra_cuda_set_stream(self._ctx, C.c_void_p(stream)))
         self.library = library
@@ -486,24 +496,38 @@ _CTX_CACHE: Dict[tuple, DeviceBatch] = {}
 def batch_response(library: RveLibrary, assignment: BatchAssignment, states: PackedStates,
                    law: FiberLaw, deformation, relax_cfg: RelaxConfig,
                    stiff_cfg: StiffnessConfig, pool=None, *, want_tangent: bool = True,
-                   device: int = 0) -> BatchResult:
+                   device: int = 0, devices: Optional[Sequence[int]] = None) -> BatchResult:
     """batch_response (batch.hpp:73-77, batch.cpp:155-187) on the B200.
 
     ``states`` is mutated in place exactly like the reference (warm start in, base solution
     out).  ``pool`` is accepted for signature parity and ignored: the GPU grid replaces
     the WorkerPool.  ``want_tangent=False`` runs the base solves only (sigma; C = 0).
+    ``devices``: several GPUs of this process (DeviceBatch(devices=...)).
     """
     F = np.ascontiguousarray(deformation, dtype=np.float64).reshape(-1, 9)
     if len(F) != states.n_points():
         raise ConfigError("one deformation gradient per point is required")
-    key = (id(library), device, assignment.entry_of_point.tobytes())
+    if len(assignment.entry_of_point) != states.n_points():
+        raise ConfigError("assignment does not match the packed states")
+    devs = tuple(int(d) for d in devices) if devices else (int(device),)
+    # keyed on the library's entries (immutable networks), so an edited library re-uploads
+    key = (id(library), tuple(id(e) for e in library.entries), devs,
+           assignment.entry_of_point.tobytes())
     db = _CTX_CACHE.get(key)
     if db is None or db.library is not library:
         for k in list(_CTX_CACHE):
-            if k[0] == id(library) and k[1] == device:
+            if k[0] == id(library) and k[2] == devs:
                 _CTX_CACHE.pop(k).close()
-        db = DeviceBatch(library, assignment, device)
+        db = DeviceBatch(library, assignment, devs[0], devices=devs)
+        db.entries_ref = list(library.entries)  # keep the keyed entries alive
         _CTX_CACHE[key] = db
+    tot = int(np.sum([library.entries[e].n_dof for e in assignment.entry_of_point]))
+    n = db.n_points
+    if (states.offsets.size != n + 1 or states.total_dofs() != tot
+            or any(getattr(states, k).size != tot
+                   for k in ("u", "v", "a", "f_int", "f_damp", "mass", "inv_mass"))
+            or any(getattr(states, k).size != n for k in ("t", "iters", "converged"))):
+        raise ConfigError("state layout does not match the network")  # relax.cpp:99-100
     db.upload_states(states)
     rec = db.solve(F, law, relax_cfg, stiff_cfg, want_tangent)
     db.download_states(states)
@@ -523,13 +547,13 @@ class NetworkBatchProvider:
 
     def __init__(self, region_of_point, library: RveLibrary, seed: int, law: FiberLaw = None,
                  relax_cfg: RelaxConfig = None, stiff_cfg: StiffnessConfig = None,
-                 workers: int = 1, device: int = 0):
+                 workers: int = 1, device: int = 0, devices: Optional[Sequence[int]] = None):
         self.library = library
         self.law = law or FiberLaw()
         self.relax_cfg = relax_cfg or RelaxConfig()
         self.stiff_cfg = stiff_cfg or StiffnessConfig()
         self._states, self.assignment = init_batch(region_of_point, library, seed)
-        self._db = DeviceBatch(library, self.assignment, device)
+        self._db = DeviceBatch(library, self.assignment, device, devices=devices)
         self._dirty = False
         self.total_solves = 0
 

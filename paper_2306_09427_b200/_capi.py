@@ -30,7 +30,8 @@ EXPORTS = [
     "fibra_host_last_error", "fibra_assign_random", "fibra_schedule_report",
     "fibra_cluster_report", "fibra_schedule_slots", "fibra_debug_cluster_forces",
     "fibra_debug_resident_forces", "fibra_debug_cluster_smem", "fibra_debug_node_forces",
-    "fibra_cuda_open", "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
+    "fibra_cuda_open", "fibra_cuda_open_devices", "fibra_plan_shards", "fibra_network_cost",
+    "fibra_cuda_close", "fibra_cuda_last_error", "fibra_cuda_set_stream",
     "fibra_cuda_upload_library", "fibra_cuda_bind_points", "fibra_cuda_reset_states",
     "fibra_cuda_set_schedule", "fibra_cuda_entry_kernel", "fibra_cuda_orientation",
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
@@ -143,6 +144,9 @@ def load(build_if_missing: bool = True):
         "fibra_schedule_slots": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, _ip,
                                            C.c_int32]),
         "fibra_cuda_open": (C.c_int, [C.c_int, pp]),
+        "fibra_cuda_open_devices": (C.c_int, [_ip, C.c_int32, pp]),
+        "fibra_plan_shards": (C.c_int, [_dp, C.c_int32, C.c_int32, _ip]),
+        "fibra_network_cost": (C.c_int, [C.POINTER(NetDesc), _dp]),
         "fibra_cuda_close": (C.c_int, [vp]),
         "fibra_cuda_last_error": (C.c_char_p, [vp]),
         "fibra_cuda_set_stream": (C.c_int, [vp, vp]),

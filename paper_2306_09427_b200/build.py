@@ -83,7 +83,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc build of libfibra_b200.so failed")
         if verbose:
             sys.stderr.write(r.stderr)
-    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs],
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-ldl"],
                        capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -14,6 +14,8 @@
 //   post_kernel   per point: A from probes (stiffness.cpp:15-41), C = push-forward(A, F)
 //                 (tensor.cpp:286-300), sigma = R sigma_U R^T (stiffness.cpp:171-173)
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -409,6 +411,30 @@ struct fibra_ctx {
   size_t phase_prof_n = 0;
   unsigned long long* d_trace = nullptr;  // FIBRA_TRACE diagnostics: [solve][4]
   size_t trace_cap = 0, trace_n = 0;
+  // ---- multi-device context (fibra_cuda_open_devices): one sub-context per device over a
+  // shard of the points; this context then holds no device state of its own ----
+  std::vector<fibra_ctx*> subs;
+  std::vector<ncclComm_t> comms;
+  std::vector<double> entry_cost;               // fibra_network_cost per library entry
+  std::vector<float> entry_log_its;             // its topology term (schedule cost model)
+  std::vector<int> entry_fibers, entry_ndof;
+  bool plan_pending = false;                    // bound, shards not yet planned
+  bool staged = false;                          // states uploaded before the plan
+  std::vector<double> stage_u, stage_t;
+  std::vector<int64_t> stage_iters;
+  std::vector<uint8_t> stage_conv;
+  std::vector<int32_t> dev_of_point, local_of_point;
+  std::vector<std::vector<int32_t>> shard;      // global point ids per device, ascending
+  int block = 0;                                // records per device block (largest shard)
+  std::vector<fibra_point_result*> d_block;     // per device: its block of records
+  std::vector<fibra_point_result*> d_gather;    // per device: n_dev blocks (all-gather)
+  std::vector<double*> d_Fsh;                   // per device: its shard's F
+  std::vector<int32_t*> d_Fidx;                 // device 0: global point ids per shard
+  int* d_src = nullptr;                         // device 0: point -> gathered record index
+  fibra_point_result* d_out0 = nullptr;         // device 0: records in point order (host path)
+  double* d_F0 = nullptr;                       // device 0: F of the host path
+  int cap0 = 0;
+  float last_gather_ms = 0;
 };
 
 namespace {
@@ -888,6 +914,19 @@ PackedNet pack(const fibra_net_desc& d) {
   return P;
 }
 
+// Input-only schedule cost model, topology term: floppy networks (many nodes of degree <= 2,
+// few fibres per node) relax slowest; fitted on config-3 knn networks (Spearman 0.83 on
+// held-out points vs 0.08 for strain alone, tools/trace_solve.py); only orders / places work
+float topology_log_its(const PackedNet& P) {
+  std::vector<int> deg(P.N, 0);
+  for (int f = 0; f < P.M; ++f) ++deg[P.a[f]], ++deg[P.b[f]];
+  int low = 0;
+  for (int d : deg) low += d <= 2;
+  const double fd2 = P.N ? static_cast<double>(low) / P.N : 0.0;
+  const double r = P.N ? static_cast<double>(P.M) / P.N : 0.0;
+  return static_cast<float>(7.2 * fd2 - 3.3 * r + 1.75 * std::log(std::max(P.M, 1)));
+}
+
 // largest CSR list of a network in entry pairs (incident fibers per node, padded to even)
 int max_pairs_of(const PackedNet& P) {
   std::vector<int> deg(P.N, 0);
@@ -1350,6 +1389,353 @@ int commit_entry(fibra_ctx* c, DeviceEntry& de, Arena& A, std::vector<PartDev>& 
 
 }  // namespace
 
+// ---------------------------------------------------------------------------------
+// multi-device contexts (fibra_cuda_open_devices): one sub-context per GPU, each a full
+// single-device context over its shard of the points; NCCL (resolved at run time, so a
+// process that already holds torch's libnccl.so.2 shares it) gathers the result records
+// ---------------------------------------------------------------------------------
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r.err = "libnccl.so.2 not found";
+      return r;
+    }
+    r.comm_init_all = reinterpret_cast<decltype(r.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+    r.all_gather = reinterpret_cast<decltype(r.all_gather)>(dlsym(h, "ncclAllGather"));
+    r.group_start = reinterpret_cast<decltype(r.group_start)>(dlsym(h, "ncclGroupStart"));
+    r.group_end = reinterpret_cast<decltype(r.group_end)>(dlsym(h, "ncclGroupEnd"));
+    r.comm_destroy = reinterpret_cast<decltype(r.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    r.error_string = reinterpret_cast<decltype(r.error_string)>(dlsym(h, "ncclGetErrorString"));
+    r.ok = r.comm_init_all && r.all_gather && r.group_start && r.group_end && r.comm_destroy &&
+           r.error_string;
+    if (!r.ok) r.err = "libnccl.so.2 lacks the collective entry points";
+    return r;
+  }();
+  return api;
+}
+
+#define FB_NCCL(ctx, call)                                                                  \
+  do {                                                                                      \
+    const ncclResult_t r_ = (call);                                                         \
+    if (r_ != ncclSuccess)                                                                  \
+      return set_err(ctx, FIBRA_E_CUDA, std::string(#call) + ": " + nccl_api().error_string(r_)); \
+  } while (0)
+
+__global__ void gather_F_kernel(int n, const int32_t* idx, const double* F, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 9 * n) return;
+  out[i] = F[9 * idx[i / 9] + i % 9];
+}
+
+// records in point order from the gathered device blocks; one thread per 8-byte word
+__global__ void permute_records_kernel(int n, const int* src, const fibra_point_result* in,
+                                       fibra_point_result* out) {
+  constexpr int W = sizeof(fibra_point_result) / 8;
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<long long>(W) * n) return;
+  const int p = static_cast<int>(i / W), w = static_cast<int>(i % W);
+  reinterpret_cast<unsigned long long*>(out + p)[w] =
+      reinterpret_cast<const unsigned long long*>(in + src[p])[w];
+}
+
+template <class Fn>
+int for_each_sub(fibra_ctx* c, Fn fn) {  // one host thread per device, first error wins
+  const int nd = static_cast<int>(c->subs.size());
+  std::vector<int> rc(nd, FIBRA_OK);
+  std::vector<std::thread> th;
+  for (int i = 0; i < nd; ++i) th.emplace_back([&, i] { rc[i] = fn(i, c->subs[i]); });
+  for (auto& t : th) t.join();
+  for (int i = 0; i < nd; ++i)
+    if (rc[i] != FIBRA_OK)
+      return set_err(c, rc[i], "device " + std::to_string(c->subs[i]->device) + ": " +
+                                   c->subs[i]->err);
+  return FIBRA_OK;
+}
+
+void free_multi_points(fibra_ctx* c) {
+  for (size_t i = 0; i < c->subs.size(); ++i) {
+    cudaSetDevice(c->subs[i]->device);
+    if (i < c->d_block.size()) cudaFree(c->d_block[i]);
+    if (i < c->d_gather.size()) cudaFree(c->d_gather[i]);
+    if (i < c->d_Fsh.size()) cudaFree(c->d_Fsh[i]);
+  }
+  if (!c->subs.empty()) {
+    cudaSetDevice(c->subs[0]->device);
+    for (int32_t* p : c->d_Fidx) cudaFree(p);
+    cudaFree(c->d_src);
+    cudaFree(c->d_out0);
+    cudaFree(c->d_F0);
+  }
+  c->d_block.clear();
+  c->d_gather.clear();
+  c->d_Fsh.clear();
+  c->d_Fidx.clear();
+  c->d_src = nullptr;
+  c->d_out0 = nullptr;
+  c->d_F0 = nullptr;
+  c->cap0 = 0;
+}
+
+// (re)bind every device to its shard and size the gather buffers
+int multi_bind_shards(fibra_ctx* c) {
+  const int nd = static_cast<int>(c->subs.size());
+  const int n = c->n_points;
+  c->shard.assign(nd, {});
+  c->local_of_point.assign(n, 0);
+  for (int p = 0; p < n; ++p) {
+    c->local_of_point[p] = static_cast<int32_t>(c->shard[c->dev_of_point[p]].size());
+    c->shard[c->dev_of_point[p]].push_back(p);
+  }
+  int rc = for_each_sub(c, [&](int i, fibra_ctx* sc) {
+    std::vector<int32_t> eop(c->shard[i].size());
+    for (size_t k = 0; k < eop.size(); ++k) eop[k] = c->entry_of_point[c->shard[i][k]];
+    return fibra_cuda_bind_points(sc, eop.data(), static_cast<int32_t>(eop.size()));
+  });
+  if (rc) return rc;
+  free_multi_points(c);
+  c->block = 1;
+  for (const auto& sh : c->shard) c->block = std::max(c->block, static_cast<int>(sh.size()));
+  c->d_block.assign(nd, nullptr);
+  c->d_gather.assign(nd, nullptr);
+  c->d_Fsh.assign(nd, nullptr);
+  const size_t rb = sizeof(fibra_point_result);
+  for (int i = 0; i < nd; ++i) {
+    FB_CUDA(c, cudaSetDevice(c->subs[i]->device));
+    FB_CUDA(c, cudaMalloc(&c->d_block[i], rb * c->block));
+    FB_CUDA(c, cudaMemset(c->d_block[i], 0, rb * c->block));  // padding rows: zero records
+    FB_CUDA(c, cudaMalloc(&c->d_gather[i], rb * c->block * nd));
+    FB_CUDA(c, cudaMalloc(&c->d_Fsh[i], 9 * sizeof(double) * c->block));
+  }
+  FB_CUDA(c, cudaSetDevice(c->subs[0]->device));
+  c->d_Fidx.assign(nd, nullptr);
+  for (int i = 0; i < nd; ++i) {
+    FB_CUDA(c, cudaMalloc(&c->d_Fidx[i], sizeof(int32_t) * std::max<size_t>(c->shard[i].size(), 1)));
+    // device i's F is gathered on device 0 into its own staging rows (device i's slot in
+    // d_gather[0] is reused: records are only written there by the all-gather later)
+    if (!c->shard[i].empty())
+      FB_CUDA(c, cudaMemcpy(c->d_Fidx[i], c->shard[i].data(), sizeof(int32_t) * c->shard[i].size(),
+                            cudaMemcpyHostToDevice));
+  }
+  std::vector<int> src(std::max(n, 1));
+  for (int p = 0; p < n; ++p) src[p] = c->dev_of_point[p] * c->block + c->local_of_point[p];
+  FB_CUDA(c, cudaMalloc(&c->d_src, sizeof(int) * src.size()));
+  FB_CUDA(c, cudaMemcpy(c->d_src, src.data(), sizeof(int) * src.size(), cudaMemcpyHostToDevice));
+  return FIBRA_OK;
+}
+
+// all states of the shards in global PackedStates layout (host)
+struct HostStates {
+  std::vector<double> a[7], t;
+  std::vector<int64_t> iters;
+  std::vector<uint8_t> conv;
+};
+
+int multi_download(fibra_ctx* c, double* const* dst7, double* t, int64_t* iters, uint8_t* conv) {
+  return for_each_sub(c, [&](int i, fibra_ctx* sc) {
+    const auto& sh = c->shard[i];
+    const size_t tot = sc->offsets.empty() ? 0 : static_cast<size_t>(sc->offsets.back());
+    HostStates h;
+    for (auto& v : h.a) v.resize(std::max<size_t>(tot, 1));
+    h.t.resize(sh.size() + 1);
+    h.iters.resize(sh.size() + 1);
+    h.conv.resize(sh.size() + 1);
+    const int r = fibra_cuda_download_states(sc, dst7[0] ? h.a[0].data() : nullptr,
+                                             dst7[1] ? h.a[1].data() : nullptr,
+                                             dst7[2] ? h.a[2].data() : nullptr,
+                                             dst7[3] ? h.a[3].data() : nullptr,
+                                             dst7[4] ? h.a[4].data() : nullptr,
+                                             dst7[5] ? h.a[5].data() : nullptr,
+                                             dst7[6] ? h.a[6].data() : nullptr, h.t.data(),
+                                             h.iters.data(), h.conv.data());
+    if (r) return r;
+    for (size_t k = 0; k < sh.size(); ++k) {
+      const int p = sh[k];
+      const long long go = c->offsets[p], lo = sc->offsets[k], len = c->offsets[p + 1] - go;
+      for (int a = 0; a < 7; ++a)
+        if (dst7[a]) std::memcpy(dst7[a] + go, h.a[a].data() + lo, sizeof(double) * len);
+      if (t) t[p] = h.t[k];
+      if (iters) iters[p] = h.iters[k];
+      if (conv) conv[p] = h.conv[k];
+    }
+    return FIBRA_OK;
+  });
+}
+
+int multi_upload(fibra_ctx* c, const double* u, const double* t, const int64_t* iters,
+                 const uint8_t* conv) {
+  return for_each_sub(c, [&](int i, fibra_ctx* sc) {
+    const auto& sh = c->shard[i];
+    const size_t tot = sc->offsets.empty() ? 0 : static_cast<size_t>(sc->offsets.back());
+    std::vector<double> hu(std::max<size_t>(tot, 1)), ht(sh.size() + 1);
+    std::vector<int64_t> hi(sh.size() + 1);
+    std::vector<uint8_t> hc(sh.size() + 1);
+    for (size_t k = 0; k < sh.size(); ++k) {
+      const int p = sh[k];
+      const long long go = c->offsets[p], lo = sc->offsets[k], len = c->offsets[p + 1] - go;
+      if (u) std::memcpy(hu.data() + lo, u + go, sizeof(double) * len);
+      if (t) ht[k] = t[p];
+      if (iters) hi[k] = iters[p];
+      if (conv) hc[k] = conv[p];
+    }
+    return fibra_cuda_upload_states(sc, u ? hu.data() : nullptr, t ? ht.data() : nullptr,
+                                    iters ? hi.data() : nullptr, conv ? hc.data() : nullptr);
+  });
+}
+
+// Shards are planned lazily: at the first solve the cost model sees F (the strain term of
+// the input-only model, as prep_kernel's schedule key), before that only the topology.
+std::vector<double> strain_costs(const fibra_ctx* c, const double* F) {
+  const int n = c->n_points;
+  std::vector<double> cost(std::max(n, 1), 1.0);
+  for (int p = 0; p < n; ++p) {
+    const double* f = F + 9 * p;
+    double e2 = 0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const double cij = f[i] * f[j] + f[3 + i] * f[3 + j] + f[6 + i] * f[6 + j] - (i == j);
+        e2 += cij * cij;
+      }
+    const int e = c->entry_of_point[p];
+    const double lk = e2 > 0 ? c->entry_log_its[e] - 0.185 * std::log(e2) : 30.0;
+    cost[p] = std::exp(std::min(lk, 30.0)) * std::max(c->entry_fibers[e], 1);
+  }
+  return cost;
+}
+
+int ensure_plan(fibra_ctx* c, const double* cost) {
+  if (!c->plan_pending) return FIBRA_OK;
+  const int n = c->n_points;
+  std::vector<double> topo;
+  if (!cost) {
+    topo.assign(std::max(n, 1), 1.0);
+    for (int p = 0; p < n; ++p) topo[p] = c->entry_cost[c->entry_of_point[p]];
+    cost = topo.data();
+  }
+  c->dev_of_point.assign(std::max(n, 1), 0);
+  fibra_plan_shards(cost, n, static_cast<int32_t>(c->subs.size()), c->dev_of_point.data());
+  c->dev_of_point.resize(n);
+  int rc = multi_bind_shards(c);
+  if (rc) return rc;
+  c->plan_pending = false;
+  if (c->staged) {
+    c->staged = false;
+    rc = multi_upload(c, c->stage_u.data(), c->stage_t.data(), c->stage_iters.data(),
+                      c->stage_conv.data());
+    c->stage_u = {};
+    c->stage_t = {};
+    c->stage_iters = {};
+    c->stage_conv = {};
+  }
+  return rc;
+}
+
+int multi_solve_device(fibra_ctx* c, const double* F_dev, const fibra_law* law,
+                       const fibra_relax_cfg* relax, const fibra_stiff_cfg* stiff,
+                       int32_t want_tangent, fibra_point_result* out_dev) {
+  const int nd = static_cast<int>(c->subs.size());
+  const int n = c->n_points;
+  if (c->offsets.empty()) return set_err(c, FIBRA_E_ARG, "bind_points must precede solve");
+  fibra_ctx* s0 = c->subs[0];
+  if (c->plan_pending) {  // the shard plan sees this call's F
+    std::vector<double> Fh(9 * static_cast<size_t>(std::max(n, 1)));
+    FB_CUDA(c, cudaSetDevice(s0->device));
+    if (n) FB_CUDA(c, cudaMemcpy(Fh.data(), F_dev, 9 * sizeof(double) * n, cudaMemcpyDeviceToHost));
+    const std::vector<double> cost = strain_costs(c, Fh.data());
+    const int rc = ensure_plan(c, cost.data());
+    if (rc) return rc;
+  }
+  FB_CUDA(c, cudaSetDevice(s0->device));
+  FB_CUDA(c, cudaEventRecord(c->ev[0], s0->stream));
+  // F of every shard: gathered on device 0, copied to its device over NVLink
+  for (int i = 0; i < nd; ++i) {
+    const int m = static_cast<int>(c->shard[i].size());
+    if (!m) continue;
+    double* stage = (i == 0) ? c->d_Fsh[0]
+                             : reinterpret_cast<double*>(c->d_gather[0] + static_cast<size_t>(i) * c->block);
+    gather_F_kernel<<<(9 * m + 255) / 256, 256, 0, s0->stream>>>(m, c->d_Fidx[i], F_dev, stage);
+    FB_CUDA(c, cudaGetLastError());
+    if (i)
+      FB_CUDA(c, cudaMemcpyPeerAsync(c->d_Fsh[i], c->subs[i]->device, stage, s0->device,
+                                     9 * sizeof(double) * m, s0->stream));
+  }
+  FB_CUDA(c, cudaEventRecord(c->ev_fork, s0->stream));
+  for (int i = 0; i < nd; ++i) {
+    fibra_ctx* sc = c->subs[i];
+    FB_CUDA(c, cudaSetDevice(sc->device));
+    FB_CUDA(c, cudaStreamWaitEvent(sc->stream, c->ev_fork, 0));
+    const int r = launch_solve(sc, c->d_Fsh[i], law, relax, stiff, want_tangent, c->d_block[i]);
+    if (r) return set_err(c, r, "device " + std::to_string(sc->device) + ": " + sc->err);
+  }
+  // one all-gather of the padded record blocks, every device receives all of them
+  const NcclApi& api = nccl_api();
+  const size_t bytes = sizeof(fibra_point_result) * static_cast<size_t>(c->block);
+  FB_NCCL(c, api.group_start());
+  for (int i = 0; i < nd; ++i)
+    FB_NCCL(c, api.all_gather(c->d_block[i], c->d_gather[i], bytes, ncclUint8, c->comms[i],
+                              c->subs[i]->stream));
+  FB_NCCL(c, api.group_end());
+  FB_CUDA(c, cudaSetDevice(s0->device));
+  FB_CUDA(c, cudaEventRecord(c->ev[1], s0->stream));
+  if (n) {
+    constexpr int W = sizeof(fibra_point_result) / 8;
+    const long long words = static_cast<long long>(W) * n;
+    permute_records_kernel<<<static_cast<unsigned>((words + 255) / 256), 256, 0, s0->stream>>>(
+        n, c->d_src, c->d_gather[0], out_dev);
+    FB_CUDA(c, cudaGetLastError());
+  }
+  FB_CUDA(c, cudaEventRecord(c->ev[3], s0->stream));
+  c->last_solves = 0;
+  return FIBRA_OK;
+}
+
+int multi_solve(fibra_ctx* c, const double* F, const fibra_law* law, const fibra_relax_cfg* relax,
+                const fibra_stiff_cfg* stiff, int32_t want_tangent, fibra_point_result* out) {
+  const int n = c->n_points;
+  fibra_ctx* s0 = c->subs[0];
+  if (c->offsets.empty()) return set_err(c, FIBRA_E_ARG, "bind_points must precede solve");
+  if (c->plan_pending) {
+    const std::vector<double> cost = strain_costs(c, F);
+    const int rp = ensure_plan(c, cost.data());
+    if (rp) return rp;
+  }
+  FB_CUDA(c, cudaSetDevice(s0->device));
+  if (c->cap0 < std::max(n, 1)) {
+    cudaFree(c->d_F0);
+    cudaFree(c->d_out0);
+    c->cap0 = std::max(n, 1);
+    FB_CUDA(c, cudaMalloc(&c->d_F0, 9 * sizeof(double) * c->cap0));
+    FB_CUDA(c, cudaMalloc(&c->d_out0, sizeof(fibra_point_result) * c->cap0));
+  }
+  if (n) FB_CUDA(c, cudaMemcpyAsync(c->d_F0, F, 9 * sizeof(double) * n, cudaMemcpyHostToDevice, s0->stream));
+  int rc = multi_solve_device(c, c->d_F0, law, relax, stiff, want_tangent, c->d_out0);
+  if (rc) return rc;
+  FB_CUDA(c, cudaSetDevice(s0->device));
+  if (n)
+    FB_CUDA(c, cudaMemcpyAsync(out, c->d_out0, sizeof(fibra_point_result) * n, cudaMemcpyDeviceToHost,
+                               s0->stream));
+  FB_CUDA(c, cudaStreamSynchronize(s0->stream));
+  return FIBRA_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int fibra_cuda_device_count(int* n) {
@@ -1385,8 +1771,89 @@ int fibra_cuda_open(int device, fibra_ctx** out) {
   return FIBRA_OK;
 }
 
+int fibra_plan_shards(const double* cost, int32_t n, int32_t n_dev, int32_t* dev_of_point) {
+  if (n < 0 || n_dev < 1 || (n && (!cost || !dev_of_point))) return FIBRA_E_ARG;
+  std::vector<int> order(n);
+  for (int p = 0; p < n; ++p) order[p] = p;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(n_dev, 0.0);
+  for (int p : order) {
+    int best = 0;
+    for (int d = 1; d < n_dev; ++d)
+      if (load[d] < load[best]) best = d;
+    dev_of_point[p] = best;
+    load[best] += std::max(cost[p], 0.0);
+  }
+  return FIBRA_OK;
+}
+
+int fibra_network_cost(const fibra_net_desc* d, double* cost) {
+  if (!d || !cost || d->n_nodes <= 0 || d->n_fibers < 0) return FIBRA_E_ARG;
+  const PackedNet P = pack(*d);
+  *cost = std::exp(static_cast<double>(topology_log_its(P))) * std::max(P.M, 1);
+  return FIBRA_OK;
+}
+
+int fibra_cuda_open_devices(const int32_t* devices, int32_t n_dev, fibra_ctx** out) {
+  if (!out || n_dev < 1 || !devices) return FIBRA_E_ARG;
+  *out = nullptr;
+  if (n_dev == 1) return fibra_cuda_open(devices[0], out);
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return FIBRA_E_CUDA;
+  auto* c = new fibra_ctx;
+  c->device = devices[0];
+  c->own_stream = false;
+  auto bail = [&](int code) {
+    for (fibra_ctx* sc : c->subs) fibra_cuda_close(sc);
+    delete c;
+    return code;
+  };
+  for (int i = 0; i < n_dev; ++i) {
+    fibra_ctx* sc = nullptr;
+    const int rc = fibra_cuda_open(devices[i], &sc);
+    if (rc) return bail(rc);
+    c->subs.push_back(sc);
+  }
+  for (int i = 0; i < n_dev; ++i)  // NVLink peer access (the F copies; NCCL finds its own)
+    for (int j = 0; j < n_dev; ++j) {
+      int can = 0;
+      if (i != j && cudaDeviceCanAccessPeer(&can, devices[i], devices[j]) == cudaSuccess && can) {
+        cudaSetDevice(devices[i]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return bail(FIBRA_E_CUDA);
+        cudaGetLastError();
+      }
+    }
+  c->comms.resize(n_dev);
+  std::vector<int> devs(devices, devices + n_dev);
+  if (api.comm_init_all(c->comms.data(), n_dev, devs.data()) != ncclSuccess) {
+    c->comms.clear();
+    return bail(FIBRA_E_CUDA);
+  }
+  cudaSetDevice(devices[0]);
+  c->n_sm = c->subs[0]->n_sm;
+  c->stream = c->subs[0]->stream;
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(FIBRA_E_CUDA);
+  if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+    return bail(FIBRA_E_CUDA);
+  *out = c;
+  return FIBRA_OK;
+}
+
 int fibra_cuda_close(fibra_ctx* c) {
   if (!c) return FIBRA_OK;
+  if (!c->subs.empty()) {
+    for (fibra_ctx* sc : c->subs) cudaSetDevice(sc->device), cudaStreamSynchronize(sc->stream);
+    free_multi_points(c);
+    for (ncclComm_t m : c->comms) nccl_api().comm_destroy(m);
+    cudaSetDevice(c->subs[0]->device);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    cudaEventDestroy(c->ev_fork);
+    for (fibra_ctx* sc : c->subs) fibra_cuda_close(sc);
+    delete c;
+    return FIBRA_OK;
+  }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   free_points(c);
@@ -1405,6 +1872,8 @@ int fibra_cuda_close(fibra_ctx* c) {
 const char* fibra_cuda_last_error(const fibra_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int fibra_cuda_set_stream(fibra_ctx* c, void* stream) {
+  if (!c->subs.empty())
+    return set_err(c, FIBRA_E_ARG, "set_stream: a multi-device context uses its devices' streams");
   cudaSetDevice(c->device);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   if (stream) {
@@ -1419,6 +1888,28 @@ int fibra_cuda_set_stream(fibra_ctx* c, void* stream) {
 
 int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32_t n) {
   if (!c || !entries || n < 1) return set_err(c, FIBRA_E_CONFIG, "RVE library is empty");
+  if (!c->subs.empty()) {  // replicated on every device
+    c->entry_cost.assign(n, 1.0);
+    c->entry_log_its.assign(n, 0.0f);
+    c->entry_fibers.assign(n, 0);
+    c->entry_ndof.assign(n, 0);
+    for (int i = 0; i < n; ++i) {
+      if (entries[i].n_nodes <= 0 || entries[i].n_fibers < 0)
+        return set_err(c, FIBRA_E_ARG, "malformed library entry " + std::to_string(i));
+      const PackedNet P = pack(entries[i]);
+      c->entry_log_its[i] = topology_log_its(P);
+      c->entry_fibers[i] = P.M;
+      c->entry_ndof[i] = 3 * P.N;
+      c->entry_cost[i] = std::exp(static_cast<double>(c->entry_log_its[i])) * std::max(P.M, 1);
+    }
+    c->entry_of_point.clear();
+    c->offsets.clear();
+    const int rc = for_each_sub(c, [&](int, fibra_ctx* sc) {
+      return fibra_cuda_upload_library(sc, entries, n);
+    });
+    if (!rc) c->entries.assign(n, DeviceEntry());  // marks the library as uploaded
+    return rc;
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   free_library(c);
@@ -1465,17 +1956,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     de.config_err = P.err;
     de.n_nodes = P.N;
     const int mp = max_pairs_of(P);
-    {  // schedule cost model: floppy networks (many nodes of degree <= 2, few fibres per
-       // node) relax slowest; fitted on config-3 knn networks (Spearman 0.83 on held-out
-       // points vs 0.08 for strain alone, tools/trace_solve.py); only orders the work
-      std::vector<int> deg(P.N, 0);
-      for (int f = 0; f < P.M; ++f) ++deg[P.a[f]], ++deg[P.b[f]];
-      int low = 0;
-      for (int d : deg) low += d <= 2;
-      const double fd2 = P.N ? static_cast<double>(low) / P.N : 0.0;
-      const double r = P.N ? static_cast<double>(P.M) / P.N : 0.0;
-      de.log_its = static_cast<float>(7.2 * fd2 - 3.3 * r + 1.75 * std::log(std::max(P.M, 1)));
-    }
+    de.log_its = topology_log_its(P);
     // diagnostics: FIBRA_NODE_SHAPE=i restricts the node kernel to kNodeVariants[i]
     const char* nshape_env = getenv("FIBRA_NODE_SHAPE");
     const int force_nshape = nshape_env ? atoi(nshape_env) : -1;
@@ -1640,6 +2121,21 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
 int fibra_cuda_bind_points(fibra_ctx* c, const int32_t* entry_of_point, int32_t n) {
   if (!c || n < 0) return FIBRA_E_ARG;
   if (c->entries.empty()) return set_err(c, FIBRA_E_ARG, "upload_library first");
+  if (!c->subs.empty()) {  // shards: longest-processing-time, planned at the first use
+    c->offsets.assign(n + 1, 0);
+    for (int p = 0; p < n; ++p) {
+      const int e = entry_of_point[p];
+      if (e < 0 || e >= static_cast<int>(c->entry_cost.size()))
+        return set_err(c, FIBRA_E_CONFIG, "assignment entry out of range");
+      c->offsets[p + 1] = c->offsets[p] + c->entry_ndof[e];  // global PackedStates layout
+    }
+    c->entry_of_point.assign(entry_of_point, entry_of_point + n);
+    c->n_points = n;
+    c->plan_pending = true;
+    c->staged = false;
+    free_multi_points(c);
+    return FIBRA_OK;
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   free_points(c);
@@ -1692,6 +2188,17 @@ int fibra_cuda_orientation(fibra_ctx* c, const int32_t* points, int32_t n, const
   for (int i = 0; i < n; ++i)
     if (points[i] < 0 || points[i] >= c->n_points)
       return set_err(c, FIBRA_E_ARG, "orientation: point out of range");
+  if (!c->subs.empty()) {  // each point on the device that holds its state
+    const int rp = ensure_plan(c, nullptr);
+    if (rp) return rp;
+    for (int i = 0; i < n; ++i) {
+      const int32_t loc = c->local_of_point[points[i]];
+      fibra_ctx* sc = c->subs[c->dev_of_point[points[i]]];
+      const int rc = fibra_cuda_orientation(sc, &loc, 1, ref_dir, out + i);
+      if (rc) return set_err(c, rc, sc->err);
+    }
+    return FIBRA_OK;
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   int* d_pts = nullptr;
   double* d_out = nullptr;
@@ -1710,6 +2217,7 @@ int fibra_cuda_orientation(fibra_ctx* c, const int32_t* points, int32_t n, const
 }
 
 int fibra_cuda_entry_kernel(const fibra_ctx* c, int32_t entry, int32_t* out) {
+  if (c && !c->subs.empty()) return fibra_cuda_entry_kernel(c->subs[0], entry, out);
   if (!c || !out || entry < 0 || entry >= static_cast<int>(c->entries.size())) return FIBRA_E_ARG;
   const KClass& K = c->classes[c->entries[entry].cls];
   if (K.node) {  // fibres per thread: 0 marks the node-centric kernel
@@ -1729,6 +2237,39 @@ int fibra_cuda_set_schedule(fibra_ctx* c, int32_t mode, const double* cost_hint)
   if (!c) return FIBRA_E_ARG;
   if (mode != FIBRA_SCHED_BATCH && mode != FIBRA_SCHED_STRAIN && mode != FIBRA_SCHED_HINT)
     return set_err(c, FIBRA_E_ARG, "unknown schedule mode");
+  if (!c->subs.empty()) {
+    if (mode == FIBRA_SCHED_HINT) {
+      if (!cost_hint) return set_err(c, FIBRA_E_ARG, "FIBRA_SCHED_HINT needs cost_hint");
+      if (c->offsets.empty()) return set_err(c, FIBRA_E_ARG, "bind_points first");
+      // re-plan the shards on the caller's costs; the warm states of the points that
+      // change device move with them (host round trip)
+      const int n = c->n_points;
+      if (c->plan_pending) {
+        const int rp = ensure_plan(c, cost_hint);
+        if (rp) return rp;
+      }
+      std::vector<int32_t> dev(std::max(n, 1));
+      fibra_plan_shards(cost_hint, n, static_cast<int32_t>(c->subs.size()), dev.data());
+      if (!std::equal(dev.begin(), dev.begin() + n, c->dev_of_point.begin())) {
+        const size_t tot = static_cast<size_t>(c->offsets.back());
+        std::vector<double> u(std::max<size_t>(tot, 1)), t(std::max(n, 1));
+        std::vector<int64_t> it(std::max(n, 1));
+        std::vector<uint8_t> cv(std::max(n, 1));
+        double* dst7[7] = {u.data(), nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        int rc = multi_download(c, dst7, t.data(), it.data(), cv.data());
+        if (rc) return rc;
+        c->dev_of_point.assign(dev.begin(), dev.begin() + n);
+        if ((rc = multi_bind_shards(c))) return rc;
+        if ((rc = multi_upload(c, u.data(), t.data(), it.data(), cv.data()))) return rc;
+      }
+      return for_each_sub(c, [&](int i, fibra_ctx* sc) {
+        std::vector<double> h(std::max<size_t>(c->shard[i].size(), 1));
+        for (size_t k = 0; k < c->shard[i].size(); ++k) h[k] = cost_hint[c->shard[i][k]];
+        return fibra_cuda_set_schedule(sc, mode, h.data());
+      });
+    }
+    return for_each_sub(c, [&](int, fibra_ctx* sc) { return fibra_cuda_set_schedule(sc, mode, nullptr); });
+  }
   if (mode == FIBRA_SCHED_HINT) {
     if (!cost_hint) return set_err(c, FIBRA_E_ARG, "FIBRA_SCHED_HINT needs cost_hint");
     if (c->offsets.empty()) return set_err(c, FIBRA_E_ARG, "bind_points first");
@@ -1747,6 +2288,13 @@ int fibra_cuda_set_schedule(fibra_ctx* c, int32_t mode, const double* cost_hint)
 }
 
 int fibra_cuda_reset_states(fibra_ctx* c) {
+  if (!c->subs.empty()) {
+    if (c->plan_pending) {
+      c->staged = false;
+      return FIBRA_OK;
+    }
+    return for_each_sub(c, [&](int, fibra_ctx* sc) { return fibra_cuda_reset_states(sc); });
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   const size_t tot = c->offsets.empty() ? 0 : static_cast<size_t>(c->offsets.back());
   for (int k = 0; k < 7; ++k)
@@ -1761,6 +2309,23 @@ int fibra_cuda_reset_states(fibra_ctx* c) {
 
 int fibra_cuda_upload_states(fibra_ctx* c, const double* u, const double* t, const int64_t* iters,
                              const uint8_t* converged) {
+  if (!c->subs.empty()) {
+    if (c->plan_pending) {  // staged until the first solve plans the shards
+      const size_t tot = static_cast<size_t>(c->offsets.back());
+      const size_t n = c->n_points;
+      c->stage_u.assign(std::max<size_t>(tot, 1), 0.0);
+      c->stage_t.assign(std::max<size_t>(n, 1), 0.0);
+      c->stage_iters.assign(std::max<size_t>(n, 1), 0);
+      c->stage_conv.assign(std::max<size_t>(n, 1), 0);
+      if (u && tot) std::memcpy(c->stage_u.data(), u, sizeof(double) * tot);
+      if (t && n) std::memcpy(c->stage_t.data(), t, sizeof(double) * n);
+      if (iters && n) std::memcpy(c->stage_iters.data(), iters, sizeof(int64_t) * n);
+      if (converged && n) std::memcpy(c->stage_conv.data(), converged, n);
+      c->staged = true;
+      return FIBRA_OK;
+    }
+    return multi_upload(c, u, t, iters, converged);
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   const size_t tot = static_cast<size_t>(c->offsets.back());
   const size_t n = c->n_points;
@@ -1775,6 +2340,12 @@ int fibra_cuda_upload_states(fibra_ctx* c, const double* u, const double* t, con
 int fibra_cuda_download_states(fibra_ctx* c, double* u, double* v, double* a, double* f_int,
                                double* f_damp, double* mass, double* inv_mass, double* t,
                                int64_t* iters, uint8_t* converged) {
+  if (!c->subs.empty()) {
+    const int rp = ensure_plan(c, nullptr);
+    if (rp) return rp;
+    double* dst7[7] = {u, v, a, f_int, f_damp, mass, inv_mass};
+    return multi_download(c, dst7, t, iters, converged);
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   const size_t tot = static_cast<size_t>(c->offsets.back());
   const size_t n = c->n_points;
@@ -1793,6 +2364,7 @@ int fibra_cuda_solve(fibra_ctx* c, const double* F, const fibra_law* law,
                      const fibra_relax_cfg* relax, const fibra_stiff_cfg* stiff,
                      int32_t want_tangent, fibra_point_result* out) {
   if (!c || !law || !relax) return FIBRA_E_ARG;
+  if (!c->subs.empty()) return multi_solve(c, F, law, relax, stiff, want_tangent, out);
   FB_CUDA(c, cudaSetDevice(c->device));
   const int n = c->n_points;
   int rc;
@@ -1815,11 +2387,13 @@ int fibra_cuda_solve_device(fibra_ctx* c, const double* F_dev, const fibra_law* 
                             const fibra_relax_cfg* relax, const fibra_stiff_cfg* stiff,
                             int32_t want_tangent, fibra_point_result* out_dev) {
   if (!c || !law || !relax) return FIBRA_E_ARG;
+  if (!c->subs.empty()) return multi_solve_device(c, F_dev, law, relax, stiff, want_tangent, out_dev);
   FB_CUDA(c, cudaSetDevice(c->device));
   return launch_solve(c, F_dev, law, relax, stiff, want_tangent, out_dev);
 }
 
 int fibra_cuda_selftest_fastmath(fibra_ctx* c, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  if (!c->subs.empty()) return fibra_cuda_selftest_fastmath(c->subs[0], n, seed, mismatches);
   FB_CUDA(c, cudaSetDevice(c->device));
   unsigned long long* d = nullptr;
   FB_CUDA(c, cudaMalloc(&d, sizeof(unsigned long long)));
@@ -1834,7 +2408,8 @@ int fibra_cuda_selftest_fastmath(fibra_ctx* c, uint64_t n, uint64_t seed, uint64
   return FIBRA_OK;
 }
 
-int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {
+int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {  // per device
+  if (!c->subs.empty()) return fibra_cuda_fp64_peak(c->subs[0], out);
   FB_CUDA(c, cudaSetDevice(c->device));
   double* sink = nullptr;
   FB_CUDA(c, cudaMalloc(&sink, 1024 * sizeof(double)));
@@ -1858,6 +2433,7 @@ int fibra_cuda_fp64_peak(fibra_ctx* c, double* out) {
 
 int fibra_cuda_trace(fibra_ctx* c, unsigned long long* out, size_t cap, size_t* n) {
   if (!c || !n) return FIBRA_E_ARG;
+  if (!c->subs.empty()) return fibra_cuda_trace(c->subs[0], out, cap, n);
   *n = c->trace_n;
   if (!out || !c->d_trace || !c->trace_n) return FIBRA_OK;
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -1866,6 +2442,7 @@ int fibra_cuda_trace(fibra_ctx* c, unsigned long long* out, size_t cap, size_t* 
 }
 
 int fibra_cuda_phase_profile(fibra_ctx* c, unsigned long long* out, size_t cap, size_t* n) {
+  if (!c->subs.empty()) return fibra_cuda_phase_profile(c->subs[0], out, cap, n);
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   *n = c->phase_prof_n;
   if (c->phase_prof && out && cap >= c->phase_prof_n)
@@ -1874,12 +2451,35 @@ int fibra_cuda_phase_profile(fibra_ctx* c, unsigned long long* out, size_t cap, 
 }
 
 int fibra_cuda_synchronize(fibra_ctx* c) {
+  if (!c->subs.empty())
+    return for_each_sub(c, [&](int, fibra_ctx* sc) { return fibra_cuda_synchronize(sc); });
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   FB_CUDA(c, cudaGetLastError());
   return FIBRA_OK;
 }
 
 int fibra_cuda_last_stats(fibra_ctx* c, fibra_solve_stats* s) {
+  if (!c->subs.empty()) {  // sums over devices; DR time = the slowest device's
+    std::memset(s, 0, sizeof *s);
+    for (fibra_ctx* sc : c->subs) {
+      fibra_solve_stats d;
+      const int rc = fibra_cuda_last_stats(sc, &d);
+      if (rc) return set_err(c, rc, sc->err);
+      s->solves += d.solves;
+      s->iterations += d.iterations;
+      s->fiber_iterations += d.fiber_iterations;
+      s->pipe_ops += d.pipe_ops;
+      s->alg_flops += d.alg_flops;
+      s->kernel_launches += d.kernel_launches;
+      s->dr_kernel_ms = std::max(s->dr_kernel_ms, d.dr_kernel_ms);
+    }
+    s->kernel_launches += 1 + static_cast<int32_t>(c->subs.size());  // F gathers + permute
+    FB_CUDA(c, cudaSetDevice(c->subs[0]->device));
+    FB_CUDA(c, cudaStreamSynchronize(c->subs[0]->stream));
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[3]) == cudaSuccess) s->total_ms = ms;
+    return FIBRA_OK;
+  }
   FB_CUDA(c, cudaSetDevice(c->device));
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   unsigned long long cnt[5] = {0, 0, 0, 0, 0};

@@ -1,9 +1,14 @@
-"""Multi-GPU sharding of a batch of RVE points (one process per GPU).
+"""Multi-GPU sharding of a batch of RVE points.
 
-RVEs are independent (reference batch.cpp:169-182), so a batch is cut into contiguous
-per-rank ranges balanced by a cost weight (fibers per point by default), each
-rank solves its range on its own B200, and one all-gather over NCCL (NVLink) returns the
-fixed-size result records to every rank.  No collective runs inside a solve.
+RVEs are independent (reference batch.cpp:169-182).  Two ways to spread a batch:
+  * one process over several GPUs: DeviceBatch(devices=[...]) / fibra_cuda_open_devices,
+    where the library shards the points itself and returns the records with one
+    ncclAllGather (the product path of the C++ drop-in and NetworkBatchProvider);
+  * one process per GPU (torchrun): every rank computes the same plan with
+    ``plan_shards`` (longest-processing-time on a per-point cost, the library's own
+    fibra_plan_shards), solves its points and ``allgather_records`` returns the records in
+    point order to every rank (one all-gather over NCCL/NVLink; gloo on CPU).
+No collective runs inside a solve.
 """
 from __future__ import annotations
 
@@ -23,6 +28,42 @@ def shard_ranges(weights, world: int):
         cuts.append(int(np.clip(np.searchsorted(cum, target, side="left"), cuts[-1], n)))
     cuts.append(n)
     return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def plan_shards(costs, world: int):
+    """Points of each rank: longest-processing-time on `costs` (descending cost, each point
+    to the least-loaded rank, ties to the lower rank), the same plan on every rank; each
+    rank's points ascending."""
+    import ctypes as C
+    from . import _capi
+    c = np.ascontiguousarray(costs, dtype=np.float64)
+    dev = np.zeros(max(len(c), 1), np.int32)
+    rc = _capi.load().fibra_plan_shards(c.ctypes.data_as(_capi._dp), len(c), int(world),
+                                        dev.ctypes.data_as(_capi._ip))
+    if rc:
+        raise ValueError("fibra_plan_shards failed")
+    dev = dev[:len(c)]
+    del C
+    return [np.nonzero(dev == r)[0].astype(np.int32) for r in range(world)]
+
+
+def network_cost(net) -> float:
+    """The library's schedule cost model of one network (fibra_network_cost)."""
+    import ctypes as C
+    from . import _capi
+    v = C.c_double()
+    if _capi.load().fibra_network_cost(net.desc(), C.byref(v)):
+        raise ValueError("fibra_network_cost failed")
+    return v.value
+
+
+def allgather_records_planned(local: np.ndarray, shards, device=None):
+    """All-gather of per-rank records whose points are the index lists `shards` (from
+    plan_shards): one all-gather, then the records in point order."""
+    full = allgather_records(local, [len(s) for s in shards], device)
+    out = np.zeros(sum(len(s) for s in shards), dtype=local.dtype)
+    out[np.concatenate(shards)] = full
+    return out
 
 
 def allgather_records(local: np.ndarray, counts, device=None):

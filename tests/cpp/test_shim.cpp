@@ -191,6 +191,29 @@ int main() {
                 static_cast<long long>(ps.iters[0]));
     bad += pb;
   }
+  // 5. several GPUs of this process (fibra_cuda_open_devices) == one GPU, bit for bit
+  int ndev = 0;
+  fibra_cuda_device_count(&ndev);
+  if (ndev >= 2) {
+    BatchAssignment assign;
+    for (int p = 0; p < 10; ++p) assign.entry_of_point.push_back(p % 3);
+    const std::vector<Def3> fs = batch_defs(10);
+    PackedStates s1 = fresh_states(lib, assign), s2 = fresh_states(lib, assign);
+    WorkerPool pool(1);
+    const BatchResult b1 = fibra_b200::batch_response(lib, assign, s1, FiberLaw{}, fs,
+                                                      RelaxConfig{}, StiffnessConfig{}, pool, 0);
+    const BatchResult b2 = fibra_b200::batch_response(lib, assign, s2, FiberLaw{}, fs,
+                                                      RelaxConfig{}, StiffnessConfig{}, pool,
+                                                      std::vector<int32_t>{0, 1});
+    int mb = b1.failed != b2.failed;
+    for (int p = 0; p < 10; ++p) {
+      mb += std::memcmp(&b1.responses[p], &b2.responses[p], sizeof(PointResponse)) != 0;
+      mb += b1.stats[p].relax_iterations != b2.stats[p].relax_iterations;
+    }
+    mb += s1.u != s2.u || s1.f_int != s2.f_int || s1.iters != s2.iters;
+    std::printf("two GPUs in one process vs one GPU: %d mismatches\n", mb);
+    bad += mb;
+  }
   std::printf("%s: %d mismatches (sigma, C, stats, PackedStates, provider)\n", bad ? "FAIL" : "OK", bad);
   return bad ? 1 : 0;
 }

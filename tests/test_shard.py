@@ -21,6 +21,21 @@ def test_shard_ranges_balance_and_cover():
         assert max(loads) - min(loads) <= 2 * w.max()
 
 
+def test_plan_shards_lpt():
+    """plan_shards (fibra_plan_shards): every point once, longest-processing-time balance
+    (max load <= mean + largest cost), deterministic."""
+    from paper_2306_09427_b200.shard import plan_shards
+    rng = np.random.default_rng(1)
+    c = rng.lognormal(0, 1.5, size=2000)
+    for world in (1, 2, 4, 8):
+        sh = plan_shards(c, world)
+        allp = np.sort(np.concatenate(sh))
+        assert np.array_equal(allp, np.arange(len(c)))
+        loads = [c[s].sum() for s in sh]
+        assert max(loads) <= c.sum() / world + c.max() + 1e-9
+        assert all(np.array_equal(a, b) for a, b in zip(sh, plan_shards(c, world)))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -43,6 +58,13 @@ def _worker(rank, world, port, q):
     rec["status"] = np.arange(lo, hi)
     rec["sigma"][:, 0] = np.arange(lo, hi) * 0.5
     full = allgather_records(rec, [b - a for a, b in rr])
+    # planned (non-contiguous) shards: records come back in point order
+    from paper_2306_09427_b200.shard import allgather_records_planned, plan_shards
+    sh = plan_shards(np.arange(n, dtype=float) % 7 + 1, world)
+    mine = np.zeros(len(sh[rank]), P.RESULT_DTYPE)
+    mine["status"] = sh[rank]
+    planned = allgather_records_planned(mine, sh)
+    assert planned["status"].tolist() == list(range(n))
     q.put((rank, full["status"].tolist(), full["sigma"][:, 0].tolist()))
     dist.destroy_process_group()
 
