@@ -26,6 +26,7 @@ SOURCES = [
     os.path.join(HERE, "csrc", "kernels_resident.cu"),
     os.path.join(HERE, "csrc", "kernels_cluster.cu"),
     os.path.join(HERE, "csrc", "kernels_node.cu"),
+    os.path.join(HERE, "csrc", "kernels_stream.cu"),
     os.path.join(HERE, "csrc", "assembly.cu"),
     os.path.join(HERE, "csrc", "host", "network.cpp"),
     os.path.join(HERE, "csrc", "host", "netgen.cpp"),
@@ -37,6 +38,7 @@ DEPS = SOURCES + [
     os.path.join(HERE, "csrc", "dr_kernel.cuh"),
     os.path.join(HERE, "csrc", "dr_cluster.cuh"),
     os.path.join(HERE, "csrc", "dr_node.cuh"),
+    os.path.join(HERE, "csrc", "dr_stream.cuh"),
     os.path.join(HERE, "csrc", "host", "node_schedule.hpp"),
     os.path.join(HERE, "csrc", "variants.hpp"),
     os.path.join(HERE, "csrc", "host", "cluster_schedule.hpp"),

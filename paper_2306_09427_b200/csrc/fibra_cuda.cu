@@ -286,6 +286,12 @@ __global__ void fastmath_selftest_kernel(unsigned long long n, unsigned long lon
   if (local) atomicAdd(bad, local);
 }
 
+// (l0, 0) -> (l0, rcp_refined(l0)) for the streaming kernel's incidence rows
+__global__ void init_rcp_kernel(double2* p, long long n) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n) p[i].y = rcp_refined(p[i].x);
+}
+
 // FP64 pipe peak probe: 8 independent DADD chains per thread, 1024 threads per SM
 __global__ void fp64_peak_kernel(double* sink, int iters, double c) {
   double x[8];
@@ -307,6 +313,7 @@ constexpr int kMaxClasses = 16;  // 4 bits of the schedule key
 struct DeviceEntry {
   EntryDev dev;           // resident-kernel entry
   NodeEntryDev ndev;      // node-centric kernel entry
+  StreamEntryDev sdev;    // HBM-streaming kernel entry
   ClusterEntryDev cdev;   // cluster-kernel entry
   OrientDev orient;       // reference-order fibres + packed reference (orientation_p2)
   Schedule sched;
@@ -325,6 +332,8 @@ struct DeviceEntry {
 struct KClass {
   bool cluster = false;
   bool node = false;      // node-centric resident kernel (dr_node.cuh)
+  bool streaming = false; // HBM-streaming cluster kernel (dr_stream.cuh)
+  int s_cap = 0, n_cap = 0, m_cap = 0;  // stream: slots, nodes, fibres (scratch layout)
   int vi = 0, C = 1;
   int x_bytes = 0, g_bytes = 0, ts = 0, csr_cap = 0, push_cap = 0, ck_stride = 0;
   int max_halo = 0;  // cluster: halo slots per bank (two banks, dr_cluster.cuh)
@@ -332,6 +341,7 @@ struct KClass {
   bool uniform_ea = true;
   EntryDev* d_entries = nullptr;          // [n_entries] (resident)
   NodeEntryDev* d_nentries = nullptr;     // [n_entries] (node)
+  StreamEntryDev* d_sentries = nullptr;   // [n_entries] (stream)
   ClusterEntryDev* d_centries = nullptr;  // [n_entries] (cluster)
   int n_points = 0, point_off = 0;        // bound points of the class, offset in the order
   cudaStream_t stream = nullptr;   // head launch (several classes) or the class's only launch
@@ -348,7 +358,11 @@ struct KClass {
     return 2ull * x_bytes + ((4ull * csr_cap + 15) & ~15ull) + 16ull * csr_cap +
            (uniform_ea ? 0ull : 8ull * csr_cap) + (nonlinear ? 8ull * csr_cap : 0ull);
   }
+  long long stream_scratch() const {  // doubles per cluster (dr_stream.cuh layout)
+    return 6ll * s_cap + 9ll * n_cap + m_cap + 8 + 2 * 16 * 16;
+  }
   size_t smem() const {
+    if (streaming) return 0;
     if (node) return node_smem(true);
     if (cluster)
       return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 8ull * csr_cap + 4ull * push_cap;
@@ -435,6 +449,7 @@ struct fibra_ctx {
   double* d_F0 = nullptr;                       // device 0: F of the host path
   int cap0 = 0;
   float last_gather_ms = 0;
+  int host_threads = 0;  // host build threads of upload_library (0: all cores)
 };
 
 namespace {
@@ -516,6 +531,7 @@ void free_library(fibra_ctx* c) {
   for (auto& k : c->classes) {
     cudaFree(k.d_entries);
     cudaFree(k.d_nentries);
+    cudaFree(k.d_sentries);
     cudaFree(k.d_centries);
     cudaFree(k.d_ckpt);
     cudaFree(k.d_scratch);
@@ -672,7 +688,10 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   for (int p = 0; p < n; ++p) {
     const DeviceEntry& de = c->entries[c->entry_of_point[p]];
     const KClass& Kc = c->classes[de.cls];
-    const int m = Kc.cluster ? de.cdev.n_fibers : (Kc.node ? de.ndev.n_fibers : de.dev.n_fibers);
+    const int m = Kc.cluster  ? de.cdev.n_fibers
+                  : Kc.node   ? de.ndev.n_fibers
+                  : Kc.streaming ? de.sdev.n_fibers
+                              : de.dev.n_fibers;
     class_work[de.cls] += m;
     class_cost[de.cls] += std::exp(static_cast<double>(de.log_its)) * m;
   }
@@ -701,7 +720,26 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     const int n_solves = want_tangent ? 7 * K.n_points : K.n_points;
     const size_t smem = K.smem();
     int cap = 0;  // co-resident CTAs (resident) or clusters (cluster) on the device
-    if (K.node) {
+    if (K.streaming) {
+      const StreamVariant& v = kStreamVariants[K.vi];
+      StreamFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      if (K.C > 8)
+        FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = K.C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(K.C);
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = 0;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      FB_CUDA(c, cudaOccupancyMaxActiveClusters(&cap, fn, &cfg));
+      if (cap < 1)
+        return set_err(c, FIBRA_E_ARG, "streaming DR kernel cannot be co-scheduled on this device");
+    } else if (K.node) {
       const NodeVariant& v = kNodeVariants[K.vi];
       KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       const size_t nsm = K.node_smem(law->kind != 0);
@@ -768,7 +806,36 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
     P.csr_cap = K.csr_cap;
     P.ck_stride = K.ck_stride;
     const size_t smem = K.smem();
-    if (K.node) {
+    if (K.streaming) {
+      const StreamVariant& v = kStreamVariants[K.vi];
+      StreamFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = K.C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(units * K.C);
+      cfg.blockDim = dim3(v.T);
+      cfg.dynamicSmemBytes = 0;
+      cfg.stream = sm;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      StreamParams SPm;
+      SPm.d = P;
+      SPm.d.entries = nullptr;
+      SPm.d.nentries = nullptr;
+      SPm.d.ckpt = K.d_ckpt + static_cast<size_t>(slot0) * K.C * 12 * K.ck_stride;
+      SPm.d.phase_prof = nullptr;
+      SPm.sentries = K.d_sentries;
+      SPm.scratch = K.d_scratch + static_cast<size_t>(slot0) * K.scratch_stride;
+      SPm.scratch_stride = K.scratch_stride;
+      SPm.s_cap = K.s_cap;
+      SPm.n_cap = K.n_cap;
+      SPm.m_cap = K.m_cap;
+      SPm.pad = 0;
+      FB_CUDA(c, cudaLaunchKernelEx(&cfg, fn, SPm));
+    } else if (K.node) {
       const NodeVariant& v = kNodeVariants[K.vi];
       KernelFn fn = v.fn[law->kind + 2 * (law->buckling_off ? 1 : 0)][K.uniform_ea ? 1 : 0];
       const size_t nsm = K.node_smem(law->kind != 0);
@@ -840,9 +907,12 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
   for (int ci : launch_order) {  // checkpoint / scratch slots for the class's full grid
     KClass& K = c->classes[ci];
     const size_t units = static_cast<size_t>(plan[ci].full);
-    if ((r = grow(c, &K.d_ckpt, K.ckpt_cap, units * (K.cluster ? K.C : 1) * 12 * K.ck_stride)))
+    if ((r = grow(c, &K.d_ckpt, K.ckpt_cap,
+                  units * ((K.cluster || K.streaming) ? K.C : 1) * 12 * K.ck_stride)))
       return r;
-    if (K.cluster && (r = grow(c, &K.d_scratch, K.scratch_cap, units * K.scratch_stride))) return r;
+    if ((K.cluster || K.streaming) &&
+        (r = grow(c, &K.d_scratch, K.scratch_cap, units * K.scratch_stride)))
+      return r;
     FB_CUDA(c, cudaStreamWaitEvent(K.stream, c->ev_fork, 0));
     FB_CUDA(c, cudaStreamWaitEvent(K.stream2, c->ev_fork, 0));
   }
@@ -1010,6 +1080,7 @@ struct Arena {
 // kernel-class capacities one entry needs (merged into its KClass after the parallel build)
 struct Caps {
   int ts = 0, x_bytes = 0, g_bytes = 0, csr_cap = 0, push_cap = 0, max_halo = 0;
+  int s_cap = 0, n_cap = 0, m_cap = 0;  // streaming kernel
   long long scratch_stride = 0;
 };
 
@@ -1022,6 +1093,10 @@ void merge_caps(KClass& K, const Caps& e) {
   K.push_cap = std::max(K.push_cap, e.push_cap);
   K.max_halo = std::max(K.max_halo, e.max_halo);
   K.scratch_stride = std::max(K.scratch_stride, e.scratch_stride);
+  K.s_cap = std::max(K.s_cap, e.s_cap);
+  K.n_cap = std::max(K.n_cap, e.n_cap);
+  K.m_cap = std::max(K.m_cap, e.m_cap);
+  if (K.streaming) K.scratch_stride = K.stream_scratch();
 }
 
 // node-centric kernel: shared-memory components of an entry for shape v (Caps fields:
@@ -1112,6 +1187,71 @@ void build_node_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc&
   const size_t region = 2ull * 0 + ((4ull * K.csr_cap + 15) & ~15ull) + 16ull * K.csr_cap;
   const size_t exit_need = 8ull * (3 * P.N + 3 * P.NFN + P.M);
   if (region < exit_need) K.csr_cap = static_cast<int>((exit_need + 19) / 20 + 32);
+}
+
+// streaming-kernel entry (dr_stream.cuh): node placement over the cluster's C*T*NPT slots
+// (no bank search: the rows and x live in global memory), step-major incidence rows
+void build_stream_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc& d,
+                        const StreamVariant& v, int C, Arena& A, Caps& K) {
+  const NodeSchedule& S = de.nsched;
+  const int TS = C * v.T * v.NPT;
+  const int G = TS / 32;
+  std::vector<int> slot_pn(TS, -1), slot_deg(TS, 0);
+  std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
+  for (int sl = 0; sl < TS; ++sl) {
+    const int pn = S.pn_of_slot[sl];
+    slot_pn[sl] = pn;
+    slot_deg[sl] = S.deg[sl];
+    if (pn < 0) continue;
+    for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
+    slot_lump[sl] = P.lump[pn];
+  }
+  const size_t ninc = 32ull * std::max(S.n_rows, 1);
+  std::vector<int> inc_x(ninc, 0);
+  std::vector<double> inc_l0(2 * ninc, 1.0), inc_ea(ninc, 1.0), inc_lump(ninc, 1.0);
+  for (int g = 0; g < G; ++g)
+    for (int l = 0; l < 32; ++l) {
+      const int sl = 32 * g + l;
+      for (int st = 0; st < S.deg[sl]; ++st) {
+        const size_t ix = 32ull * (S.group_row0[g] + st) + l;
+        const int f = S.inc_fiber[sl][st], o = S.inc_other[sl][st];
+        inc_x[ix] = 3 * S.slot_of_pn[o];
+        inc_l0[2 * ix] = P.l0[f];
+        inc_l0[2 * ix + 1] = 0.0;  // rcp_refined(l0), filled on the device (init_rcp_kernel)
+        inc_ea[ix] = P.ea[f];
+        inc_lump[ix] = P.lump[o];
+      }
+    }
+  StreamEntryDev& E = de.sdev;
+  E = StreamEntryDev{};
+  E.n_nodes = P.N;
+  E.n_fibers = P.M;
+  E.n_free_nodes = P.NFN;
+  E.n_fix_nodes = P.N - P.NFN;
+  E.f0 = S.f0;
+  E.node_slots = TS;
+  E.n_rows = S.n_rows;
+  E.max_lump = P.max_lump;
+  E.max_ea = d.max_ea;
+  E.box_volume = 8.0 * d.box_half * d.box_half * d.box_half;
+  E.ea0 = P.M > 0 ? P.ea[0] : 1.0;
+  A.add(&E.slot_pn, slot_pn);
+  A.add(&E.slot_ref, slot_ref);
+  A.add(&E.slot_lump, slot_lump);
+  A.add(&E.slot_deg, slot_deg);
+  A.add(&E.group_row0, S.group_row0);
+  A.add(&E.inc_x, inc_x);
+  A.add(reinterpret_cast<const double**>(&E.inc_l0), inc_l0);
+  A.add(&E.inc_ea, inc_ea);
+  A.add(&E.inc_lump, inc_lump);
+  A.add(&E.fib_a, P.a);
+  A.add(&E.fib_b, P.b);
+  A.add(&E.fib_l0, P.l0);
+  A.add(&E.fib_ea, P.ea);
+  K.ts = v.T * v.NPT;  // checkpoint slots per CTA
+  K.s_cap = TS;
+  K.n_cap = P.N;
+  K.m_cap = P.M;
 }
 
 // resident-kernel entry: slot arrays, g*d record colouring, step-major CSR pairs
@@ -1812,6 +1952,8 @@ int fibra_cuda_open_devices(const int32_t* devices, int32_t n_dev, fibra_ctx** o
     fibra_ctx* sc = nullptr;
     const int rc = fibra_cuda_open(devices[i], &sc);
     if (rc) return bail(rc);
+    // the devices build their copies of the library concurrently: share the host cores
+    sc->host_threads = std::max(1, static_cast<int>(std::thread::hardware_concurrency()) / n_dev);
     c->subs.push_back(sc);
   }
   for (int i = 0; i < n_dev; ++i)  // NVLink peer access (the F copies; NCCL finds its own)
@@ -1919,7 +2061,8 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       return set_err(c, FIBRA_E_ARG, "malformed library entry " + std::to_string(i));
   }
   // host work per entry (packing, shape selection, schedules) runs on all host cores
-  const int workers = std::max(1, std::min<int>(n, static_cast<int>(std::thread::hardware_concurrency())));
+  const int hw = static_cast<int>(std::thread::hardware_concurrency());
+  const int workers = std::max(1, std::min<int>(n, c->host_threads > 0 ? c->host_threads : hw));
   auto parallel_for = [&](int lo, int hi, const std::function<void(int)>& fn) {
     std::atomic<int> next(lo);
     std::vector<std::thread> pool;
@@ -1934,13 +2077,19 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   c->entries.resize(n);
   std::vector<PackedNet> nets(n);
   std::vector<ClusterPlan> plans(n);
-  std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1), kind_node(n, 0);
+  std::vector<int> kind_cl(n, 0), kind_vi(n, -1), kind_C(n, 1), kind_node(n, 0), kind_stream(n, 0);
   // FIBRA_KERNEL=node: the node-centric kernel (dr_node.cuh) for the entries it holds.
   // Opt-in: it removes the fiber -> node barrier but evaluates every fibre twice, and on
   // config 2 it issues 13.0k instructions per RVE-iteration against the fiber/node kernel's
   // 6.2k, with warps waiting on the highest-degree warp (profiles/r02_node_*).
   const char* kern_env = getenv("FIBRA_KERNEL");
   const bool allow_node = kern_env && kern_env[0] == 'n';
+  // FIBRA_KERNEL=stream: every entry on the HBM-streaming kernel (A/B timing); it is
+  // otherwise taken by entries that fit no resident shape and no 16-CTA cluster.
+  // FIBRA_STREAM_C=C restricts it to C-CTA clusters.
+  const bool force_stream = kern_env && kern_env[0] == 's';
+  const char* stream_c_env = getenv("FIBRA_STREAM_C");
+  const int stream_c = stream_c_env ? atoi(stream_c_env) : 0;
   std::vector<Caps> est(n);  // the entry's shared-memory components (exact, = the build's)
   // diagnostics: FIBRA_FORCE_CLUSTER=C places every entry on a C-CTA cluster (kernel timing)
   const char* force_env = getenv("FIBRA_FORCE_CLUSTER");
@@ -1960,7 +2109,8 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     // diagnostics: FIBRA_NODE_SHAPE=i restricts the node kernel to kNodeVariants[i]
     const char* nshape_env = getenv("FIBRA_NODE_SHAPE");
     const int force_nshape = nshape_env ? atoi(nshape_env) : -1;
-    for (int v = 0; v < kNumNodeVariants && kind_vi[i] < 0 && !force_c && allow_node; ++v)
+    for (int v = 0; v < kNumNodeVariants && kind_vi[i] < 0 && !force_c && allow_node &&
+                    !force_stream; ++v)
       if ((force_nshape < 0 || v == force_nshape) &&
           node_fits(c, P, kNodeVariants[v], false, de.nsched)) {
         kind_vi[i] = v;
@@ -1975,7 +2125,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
         if (region < exit_need) capn = static_cast<int>((exit_need + 19) / 20 + 32);
         est[i].csr_cap = capn;
       }
-    for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c; ++v)
+    for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c && !force_stream; ++v)
       if (resident_fits(c, P, kVariants[v], mp, de.sched)) {
         kind_vi[i] = v;
         const int TS = kVariants[v].NPT * kVariants[v].T;
@@ -1987,7 +2137,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       }
     // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
     // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
-    for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0; cc *= 2)
+    for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0 && !force_stream; cc *= 2)
         for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v) {
           if (force_shape >= 0 && v != force_shape) continue;
           if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
@@ -2007,15 +2157,33 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             est[i].push_cap = plans[i].max_push * TS;
           }
         }
+    // beyond on-chip capacity: the streaming kernel, the lightest shape (fewest nodes per
+    // thread) on the fewest CTAs whose slots hold the nodes
+    for (int v = 0; v < kNumStreamVariants && kind_vi[i] < 0; ++v)
+      for (int cc = 2; cc <= 16 && kind_vi[i] < 0; cc *= 2) {
+        if (stream_c && cc != stream_c) continue;
+        const StreamVariant& sv = kStreamVariants[v];
+        if (!build_node_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), cc * sv.T, sv.NPT, 0,
+                                 de.nsched))
+          continue;
+        kind_vi[i] = v;
+        kind_C[i] = cc;
+        kind_stream[i] = 1;
+        est[i].ts = sv.T * sv.NPT;
+        est[i].s_cap = cc * sv.T * sv.NPT;
+        est[i].n_cap = P.N;
+        est[i].m_cap = P.M;
+      }
   });
   for (int i = 0; i < n; ++i) {
     if (kind_vi[i] < 0)
       return set_err(c, FIBRA_E_ARG, "RVE library entry " + std::to_string(i) + " (" +
                                          std::to_string(nets[i].M) + " fibers, " +
                                          std::to_string(nets[i].N) +
-                                         " nodes) exceeds a 16-CTA cluster");
+                                         " nodes) exceeds every kernel shape");
     const bool cl = kind_cl[i] != 0;
     const bool nd = kind_node[i] != 0;
+    const bool sm = kind_stream[i] != 0;
     // a class's footprint is the per-component maximum over its entries: join the first
     // class of this kernel shape that still fits the device with this entry, else open one
     auto fits_with = [&](const KClass& K) {
@@ -2027,7 +2195,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
     int k = 0;
     const int nk = static_cast<int>(c->classes.size());
     while (k < nk && !(c->classes[k].cluster == cl && c->classes[k].node == nd &&
-                       c->classes[k].vi == kind_vi[i] &&
+                       c->classes[k].streaming == sm && c->classes[k].vi == kind_vi[i] &&
                        c->classes[k].C == kind_C[i] && fits_with(c->classes[k])))
       ++k;
     if (k == nk) {
@@ -2035,6 +2203,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       KClass K;
       K.cluster = cl;
       K.node = nd;
+      K.streaming = sm;
       K.vi = kind_vi[i];
       K.C = kind_C[i];
       c->classes.push_back(K);
@@ -2067,6 +2236,9 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
       else if (K.node)
         build_node_entry(de, nets[i], entries[i], kNodeVariants[K.vi], arenas[i - lo],
                          caps[i - lo]);
+      else if (K.streaming)
+        build_stream_entry(de, nets[i], entries[i], kStreamVariants[K.vi], K.C, arenas[i - lo],
+                           caps[i - lo]);
       else
         build_resident_entry(de, nets[i], entries[i], kVariants[K.vi], arenas[i - lo],
                              caps[i - lo]);
@@ -2088,7 +2260,22 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
   for (KClass& K : c->classes) {
     if (K.smem() > static_cast<size_t>(c->max_smem - (K.cluster ? kClusterCtlExtra : 0)))
       return set_err(c, FIBRA_E_ARG, "library shared-memory footprint exceeds the device limit");
-    if (K.node) {
+    if (K.streaming) {
+      std::vector<StreamEntryDev> host(n, StreamEntryDev{});
+      for (int i = 0; i < n; ++i)
+        if (&c->classes[c->entries[i].cls] == &K) {
+          host[i] = c->entries[i].sdev;
+          // (l0, rcp_refined(l0)) pairs: the reciprocal with the device's own sequence
+          const long long ninc = 32ll * std::max(host[i].n_rows, 1);
+          init_rcp_kernel<<<static_cast<unsigned>((ninc + 255) / 256), 256, 0, c->stream>>>(
+              const_cast<double2*>(host[i].inc_l0), ninc);
+          FB_CUDA(c, cudaGetLastError());
+        }
+      FB_CUDA(c, cudaStreamSynchronize(c->stream));
+      FB_CUDA(c, cudaMalloc(&K.d_sentries, sizeof(StreamEntryDev) * n));
+      FB_CUDA(c, cudaMemcpy(K.d_sentries, host.data(), sizeof(StreamEntryDev) * n,
+                            cudaMemcpyHostToDevice));
+    } else if (K.node) {
       std::vector<NodeEntryDev> host(n, NodeEntryDev{});
       for (int i = 0; i < n; ++i)
         if (&c->classes[c->entries[i].cls] == &K) host[i] = c->entries[i].ndev;
@@ -2220,7 +2407,10 @@ int fibra_cuda_entry_kernel(const fibra_ctx* c, int32_t entry, int32_t* out) {
   if (c && !c->subs.empty()) return fibra_cuda_entry_kernel(c->subs[0], entry, out);
   if (!c || !out || entry < 0 || entry >= static_cast<int>(c->entries.size())) return FIBRA_E_ARG;
   const KClass& K = c->classes[c->entries[entry].cls];
-  if (K.node) {  // fibres per thread: 0 marks the node-centric kernel
+  if (K.streaming) {  // fibres per thread: -1 marks the streaming kernel
+    const StreamVariant& v = kStreamVariants[K.vi];
+    out[0] = K.C, out[1] = v.T, out[2] = -1, out[3] = v.NPT;
+  } else if (K.node) {  // fibres per thread: 0 marks the node-centric kernel
     const NodeVariant& v = kNodeVariants[K.vi];
     out[0] = 1, out[1] = v.T, out[2] = 0, out[3] = v.NPT;
   } else if (K.cluster) {

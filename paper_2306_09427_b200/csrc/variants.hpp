@@ -5,11 +5,13 @@
 #include "dr_cluster.cuh"
 #include "dr_kernel.cuh"
 #include "dr_node.cuh"
+#include "dr_stream.cuh"
 
 namespace fibra_b200 {
 
 using KernelFn = void (*)(DrParams);
 using ClusterFn = void (*)(ClusterParams);
+using StreamFn = void (*)(StreamParams);
 
 struct Variant {     // resident kernel: one CTA per RVE
   int T, FPT, NPT, MINB;
@@ -26,7 +28,14 @@ struct NodeVariant {  // node-centric kernel: one CTA per RVE, NPT node slots pe
   KernelFn fn[4][2];
 };
 
+struct StreamVariant {  // HBM-streaming kernel: one cluster per RVE, per-CTA shape
+  int T, NPT;
+  StreamFn fn[4][2];
+};
+
 extern const Variant kVariants[];
+extern const StreamVariant kStreamVariants[];
+extern const int kNumStreamVariants;
 extern const NodeVariant kNodeVariants[];
 extern const int kNumNodeVariants;
 extern const int kNumVariants;
