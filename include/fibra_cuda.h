@@ -258,6 +258,9 @@ int fibra_cuda_synchronize(fibra_ctx* ctx);
 /* counters of the last solve (synchronizes) */
 int fibra_cuda_last_stats(fibra_ctx* ctx, fibra_solve_stats* out);
 int fibra_cuda_device_count(int* n);
+/* Diagnostics: the exponential law's expm1 (which = 1) / exp (which = 0) on the device
+ * (csrc/libm_glibc.cuh, the host libm's operation sequences) for n host operands. */
+int fibra_cuda_eval_libm(fibra_ctx* ctx, int32_t which, const double* x, int64_t n, double* out);
 /* FP64-pipe roofline denominator measured on this device: independent DADD chains on every
  * SM; returns lane-operations per second (one DADD/DMUL/DFMA lane = 1 op). */
 int fibra_cuda_fp64_peak(fibra_ctx* ctx, double* lane_ops_per_s);

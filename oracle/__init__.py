@@ -119,6 +119,7 @@ def lib():
                                         C.c_int, C.c_int, C.c_int, C.POINTER(CResponse), _ip]
         L.or_polar_decompose.argtypes = [_dp, _dp, _dp]
         L.or_eigen_sym3.argtypes = [_dp, _dp, _dp]
+        L.or_libm.argtypes = [C.c_int, _dp, C.c_int64, _dp]
         L.or_pull_back_stress.argtypes = [_dp, _dp, _dp]
         L.or_push_forward_stiffness.argtypes = [_dp, _dp, _dp]
         L.or_material_stiffness_from_probes.argtypes = [_dp, _dp, _dp, C.c_double, _dp]
@@ -300,6 +301,14 @@ def eigen_sym3(A):
     if rc:
         raise OracleError(7, "eigen_sym3 NoConvergence")
     return lam, Q.reshape(3, 3)
+
+
+def libm(which, x):
+    """The host libm's exp (which 0) / expm1 (which 1), elementwise."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    lib().or_libm(int(which), _ptr(x, _dp), x.size, _ptr(out, _dp))
+    return out
 
 
 def norm2_sq(x):

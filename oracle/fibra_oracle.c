@@ -1249,3 +1249,9 @@ int or_assemble(const int32_t* tets, int32_t n_tets, const double* coords,
     if (!isfinite(residual[i])) return OR_ASM_RESIDUAL; /* :186-187 */
   return OR_OK;
 }
+
+/* The host libm's exp / expm1 (what the reference's FiberLaw calls, network.cpp:16-53) over
+ * an array: the checker of the device restatement (csrc/libm_glibc.cuh). */
+void or_libm(int which, const double* x, int64_t n, double* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = which ? expm1(x[i]) : exp(x[i]);
+}

@@ -135,6 +135,8 @@ void or_sym_from_full(const double a[9], double s[6]);
 int or_polar_decompose(const double F[9], double R[9], double U[6]);
 /* Eigen 3.4.0 SelfAdjointEigenSolver<Matrix3d> restatement: 0 Success, 1 NoConvergence */
 int or_eigen_sym3(const double a[9], double lam[3], double Q[9]);
+/* host libm exp (which 0) / expm1 (which 1) over an array */
+void or_libm(int which, const double* x, int64_t n, double* out);
 int or_pull_back_stress(const double sigma[6], const double F[9], double pk2[6]);
 void or_mandel(const double s[6], double v[6]);
 void or_mandel_M_of_U(const double U[6], double M[36]);

@@ -37,7 +37,7 @@ EXPORTS = [
     "fibra_cuda_upload_states", "fibra_cuda_download_states", "fibra_cuda_solve",
     "fibra_cuda_solve_device", "fibra_cuda_synchronize", "fibra_cuda_last_stats",
     "fibra_cuda_device_count", "fibra_cuda_fp64_peak", "fibra_cuda_phase_profile", "fibra_cuda_trace",
-    "fibra_cuda_selftest_fastmath",
+    "fibra_cuda_selftest_fastmath", "fibra_cuda_eval_libm",
     "fibra_cuda_assembly_create", "fibra_cuda_assembly_set_stream", "fibra_cuda_assembly_pattern",
     "fibra_cuda_assemble", "fibra_cuda_assemble_device", "fibra_cuda_assembly_status",
     "fibra_cuda_assembly_times", "fibra_cuda_assembly_info", "fibra_cuda_assembly_last_error",
@@ -144,6 +144,7 @@ def load(build_if_missing: bool = True):
         "fibra_schedule_slots": (C.c_int, [C.POINTER(NetDesc), C.c_int, C.c_int, C.c_int, _ip,
                                            C.c_int32]),
         "fibra_cuda_open": (C.c_int, [C.c_int, pp]),
+        "fibra_cuda_eval_libm": (C.c_int, [vp, C.c_int32, _dp, C.c_int64, _dp]),
         "fibra_cuda_open_devices": (C.c_int, [_ip, C.c_int32, pp]),
         "fibra_plan_shards": (C.c_int, [_dp, C.c_int32, C.c_int32, _ip]),
         "fibra_network_cost": (C.c_int, [C.POINTER(NetDesc), _dp]),

@@ -40,6 +40,7 @@
 
 #include "fastmath.cuh"
 #include "fibra_cuda.h"
+#include "libm_glibc.cuh"
 #include "tensor.cuh"
 
 namespace fibra_b200 {
@@ -198,13 +199,15 @@ __device__ __forceinline__ Tp* sm_at(unsigned char* base, int byte_off) {
   return reinterpret_cast<Tp*>(base + byte_off);
 }
 
-// axial force N(lambda) and tangent (network.cpp:16-38); s = ea_scale*ea
+// axial force N(lambda) and tangent (network.cpp:16-38); s = ea_scale*ea.  expm1 / exp are
+// the host libm's own operation sequences (libm_glibc.cuh), so the exponential law is
+// bitwise too.
 template <int LAW>
 __device__ __forceinline__ double law_force(double s, double stretch, int buckling_off,
                                             double B) {
   if (LAW == 0) return (buckling_off && stretch < 1.0) ? 0.0 : s * (stretch - 1.0);
   if (buckling_off && stretch < 1.0) return 0.0;
-  return s / B * expm1(B * (stretch - 1.0));
+  return s / B * glibc::expm1(B * (stretch - 1.0));
 }
 
 template <int LAW>
@@ -212,7 +215,7 @@ __device__ __forceinline__ double law_tangent(double s, double stretch, int buck
                                               double B) {
   if (buckling_off && stretch < 1.0) return 0.0;
   if (LAW == 0) return s;
-  return s * exp(B * (stretch - 1.0));
+  return s * glibc::exp(B * (stretch - 1.0));
 }
 
 template <int LAW>
@@ -221,7 +224,7 @@ __device__ __forceinline__ double law_energy(double s, double stretch, double rl
   if (buckling_off && stretch < 1.0) return 0.0;
   const double e = stretch - 1.0;
   if (LAW == 0) return 0.5 * s * rl * e * e;
-  return rl * s / B * (expm1(B * e) / B - e);
+  return rl * s / B * (glibc::expm1(B * e) / B - e);
 }
 
 // g*d record offsets in fib_g are 16-bit byte offsets >> kGShift: 8-byte units for the large

@@ -55,8 +55,33 @@ struct StreamParams {
   double* scratch;
   long long scratch_stride;  // doubles per cluster
   int s_cap, n_cap;          // slots / nodes capacity of the class (scratch layout)
-  int m_cap, pad;            // fibres capacity
+  int m_cap;                 // fibres capacity
+  int stage;                 // 1: this CTA's incidence rows are TMA-staged into shared
+                             //    memory once per solve (they fit), 0: streamed every pass
 };
+
+// bulk copy global -> this CTA's shared memory, completing on an mbarrier (TMA engine)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(sh_addr(dst)), "l"(src), "r"(bytes), "r"(sh_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sh_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sh_addr(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(sh_addr(bar)), "r"(phase) : "memory");
+}
 
 struct __align__(16) StreamCtl {
   int solve, point, q, entry;
@@ -86,6 +111,8 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
   constexpr int LAW = LAWBO & 1;
   constexpr int bo = LAWBO >> 1;
   __shared__ StreamCtl ctl;
+  __shared__ __align__(8) unsigned long long stage_bar;
+  extern __shared__ __align__(16) unsigned char smem[];
   const DrParams& P = SP.d;
   constexpr int NW = T / 32;
   const int tid = threadIdx.x;
@@ -107,6 +134,8 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
   const double B = P.nonlinearity;
   const long long XS = 3ll * SP.s_cap;  // doubles per x buffer
 
+  if (tid == 0) mbar_init(&stage_bar, 1);
+  unsigned stage_phase = 0;
   cl_sync();
   for (;;) {
     // ---- ticket (rank 0), broadcast into every CTA's control block ----
@@ -166,6 +195,60 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
       nsteps[j] = E.group_row0[(slot[j] >> 5) + 1] - row0[j];
     }
 #define NREF(j, c) __ldg(E.slot_ref + 3 * slot[j] + (c))
+    // this CTA's incidence rows: block j holds the rows of its warp groups for slot block j
+    // (contiguous in HBM); staged = one TMA bulk copy per array and block into shared
+    // memory, once per solve
+    const int* rIX[NPT];
+    const double2* rIL[NPT];
+    const double* rIE[NPT];
+    const double* rIM[NPT];
+    int rbase[NPT];
+    {
+      unsigned char* sp = smem;
+      unsigned total = 0;
+      size_t e0s[NPT], nes[NPT];
+#pragma unroll
+      for (int j = 0; j < NPT; ++j) {
+        const int g0 = (j * CT + static_cast<int>(rank) * T) >> 5;
+        rbase[j] = E.group_row0[g0];
+        const int rows = E.group_row0[g0 + NW] - rbase[j];
+        const size_t e0 = 32ull * rbase[j], ne = 32ull * rows;
+        e0s[j] = e0;
+        nes[j] = ne;
+        if (SP.stage) {
+          int* sx = reinterpret_cast<int*>(sp);
+          double2* sl = reinterpret_cast<double2*>(sx + ne);
+          double* se = reinterpret_cast<double*>(sl + ne);
+          double* sm = se + (UEA ? 0 : ne);
+          total += static_cast<unsigned>(ne * (4 + 16 + (UEA ? 0 : 8) + (LAW != 0 ? 8 : 0)));
+          rIX[j] = sx;
+          rIL[j] = sl;
+          rIE[j] = se;
+          rIM[j] = sm;
+          sp = reinterpret_cast<unsigned char*>(sm + (LAW != 0 ? ne : 0));
+        } else {
+          rIX[j] = E.inc_x + e0;
+          rIL[j] = E.inc_l0 + e0;
+          rIE[j] = E.inc_ea + e0;
+          rIM[j] = E.inc_lump + e0;
+        }
+      }
+      if (SP.stage && tid == 0) {
+        // the previous solve's generic-proxy reads of these bytes are ordered before the
+        // bulk (async-proxy) writes; then arm the barrier and issue the copies
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&stage_bar, total);  // the single arrival of this phase
+#pragma unroll
+        for (int j = 0; j < NPT; ++j) {
+          if (!nes[j]) continue;
+          const unsigned ne = static_cast<unsigned>(nes[j]);
+          bulk_g2s(const_cast<int*>(rIX[j]), E.inc_x + e0s[j], 4u * ne, &stage_bar);
+          bulk_g2s(const_cast<double2*>(rIL[j]), E.inc_l0 + e0s[j], 16u * ne, &stage_bar);
+          if (!UEA) bulk_g2s(const_cast<double*>(rIE[j]), E.inc_ea + e0s[j], 8u * ne, &stage_bar);
+          if (LAW != 0) bulk_g2s(const_cast<double*>(rIM[j]), E.inc_lump + e0s[j], 8u * ne, &stage_bar);
+        }
+      }
+    }
 
     // ---- per-solve setup (relax.cpp:95-145) ----
     double Fm[9];
@@ -243,6 +326,10 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
       if (lane == 0) WMIN[rank * NW + warp] = lmin;
     }
     const bool det_ok = det3(Fm) > 0;
+    if (SP.stage) {  // the rows of this solve have landed
+      mbar_wait(&stage_bar, stage_phase);
+      stage_phase ^= 1;
+    }
     cl_sync();
     double dt_const = 0;
     if (LAW == 0) {
@@ -326,14 +413,14 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
         };
         auto eval = [&](int st) {
           Inc r;
-          const int ix = 32 * (row0[j] + st) + lane;
-          const int xo = __ldg(E.inc_x + ix);
-          const double2 lr = __ldg(E.inc_l0 + ix);  // 128-bit coalesced
+          const int ix = 32 * (row0[j] - rbase[j] + st) + lane;  // within this CTA's block
+          const int xo = SP.stage ? rIX[j][ix] : __ldg(rIX[j] + ix);
+          const double2 lr = SP.stage ? rIL[j][ix] : __ldg(rIL[j] + ix);  // 128-bit coalesced
           r.dx = __ldcg(Xc + xo) - x0;  // d' = x_other - x_own
           r.dy = __ldcg(Xc + xo + 1) - x1;
           r.dz = __ldcg(Xc + xo + 2) - x2;
           r.l0 = lr.x;
-          const double sj = UEA ? s_uni : P.ea_scale * __ldg(E.inc_ea + ix);
+          const double sj = UEA ? s_uni : P.ea_scale * (SP.stage ? rIE[j][ix] : __ldg(rIE[j] + ix));
           bool o1, o2, o3 = true;
           r.len = sqrt_fast(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz, o1);
           const double stretch = div_fast_rcp(r.len, lr.x, lr.y, o2);
@@ -342,7 +429,7 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
           } else {
             r.g = law_force<LAW>(sj, stretch, bo, B) / r.len;
             if (st < n_j) {
-              const double mb = __ldg(E.inc_lump + ix) * scale;
+              const double mb = (SP.stage ? rIM[j][ix] : __ldg(rIM[j] + ix)) * scale;
               const double mred = mj[j] * mb / (mj[j] + mb) * lr.x;  // relax.cpp:50-53
               const double kt = smax(fabs(law_tangent<LAW>(sj, stretch, bo, B)), sj);
               kmin = smin(kmin, mred / kt);
@@ -353,8 +440,8 @@ __global__ void __launch_bounds__(T, 1) dr_stream_kernel(StreamParams SP) {
         };
         auto slow = [&](Inc& r, int st) {
           if (!r.ok) {
-            const int ix = 32 * (row0[j] + st) + lane;
-            const double sj = UEA ? s_uni : P.ea_scale * __ldg(E.inc_ea + ix);
+            const int ix = 32 * (row0[j] - rbase[j] + st) + lane;
+            const double sj = UEA ? s_uni : P.ea_scale * (SP.stage ? rIE[j][ix] : __ldg(rIE[j] + ix));
             r.len = sqrt(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
             r.g = law_force<LAW>(sj, r.len / r.l0, bo, B) / r.len;
           }

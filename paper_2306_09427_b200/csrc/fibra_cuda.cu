@@ -286,6 +286,13 @@ __global__ void fastmath_selftest_kernel(unsigned long long n, unsigned long lon
   if (local) atomicAdd(bad, local);
 }
 
+// expm1 / exp of the exponential fibre law (libm_glibc.cuh) on the device, for the parity
+// test against the host libm (tests/test_gpu_fastmath.py)
+__global__ void eval_libm_kernel(int which, const double* x, long long n, double* out) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = which ? glibc::expm1(x[i]) : glibc::exp(x[i]);
+}
+
 // (l0, 0) -> (l0, rcp_refined(l0)) for the streaming kernel's incidence rows
 __global__ void init_rcp_kernel(double2* p, long long n) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -334,6 +341,7 @@ struct KClass {
   bool node = false;      // node-centric resident kernel (dr_node.cuh)
   bool streaming = false; // HBM-streaming cluster kernel (dr_stream.cuh)
   int s_cap = 0, n_cap = 0, m_cap = 0;  // stream: slots, nodes, fibres (scratch layout)
+  long long stage_bytes = 0;            // stream: largest per-CTA incidence-row block (entries)
   int vi = 0, C = 1;
   int x_bytes = 0, g_bytes = 0, ts = 0, csr_cap = 0, push_cap = 0, ck_stride = 0;
   int max_halo = 0;  // cluster: halo slots per bank (two banks, dr_cluster.cuh)
@@ -730,10 +738,17 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       attr[0].val.clusterDim.x = K.C;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      const char* st_env = getenv("FIBRA_STREAM_STAGE");
+      const long long sbytes =
+          K.stage_bytes * (20 + (K.uniform_ea ? 0 : 8) + (law->kind != 0 ? 8 : 0));
+      const bool stage = sbytes <= c->max_smem && !(st_env && st_env[0] == '0');
+      const size_t dyn = stage ? static_cast<size_t>(sbytes) : 0;
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(dyn)));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(K.C);
       cfg.blockDim = dim3(v.T);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = dyn;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       FB_CUDA(c, cudaOccupancyMaxActiveClusters(&cap, fn, &cfg));
@@ -814,14 +829,24 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       attr[0].val.clusterDim.x = K.C;
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
+      // incidence rows TMA-staged in shared memory when a CTA's block fits
+      // (diagnostics: FIBRA_STREAM_STAGE=0 streams them every pass)
+      const char* st_env = getenv("FIBRA_STREAM_STAGE");
+      const long long sbytes =
+          K.stage_bytes * (20 + (K.uniform_ea ? 0 : 8) + (law->kind != 0 ? 8 : 0));
+      const bool stage = sbytes <= c->max_smem && !(st_env && st_env[0] == '0');
+      const size_t dyn = stage ? static_cast<size_t>(sbytes) : 0;
+      FB_CUDA(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(dyn)));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(units * K.C);
       cfg.blockDim = dim3(v.T);
-      cfg.dynamicSmemBytes = 0;
+      cfg.dynamicSmemBytes = dyn;
       cfg.stream = sm;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
       StreamParams SPm;
+      SPm.stage = stage ? 1 : 0;
       SPm.d = P;
       SPm.d.entries = nullptr;
       SPm.d.nentries = nullptr;
@@ -833,7 +858,6 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       SPm.s_cap = K.s_cap;
       SPm.n_cap = K.n_cap;
       SPm.m_cap = K.m_cap;
-      SPm.pad = 0;
       FB_CUDA(c, cudaLaunchKernelEx(&cfg, fn, SPm));
     } else if (K.node) {
       const NodeVariant& v = kNodeVariants[K.vi];
@@ -1081,6 +1105,7 @@ struct Arena {
 struct Caps {
   int ts = 0, x_bytes = 0, g_bytes = 0, csr_cap = 0, push_cap = 0, max_halo = 0;
   int s_cap = 0, n_cap = 0, m_cap = 0;  // streaming kernel
+  long long stage_bytes = 0;
   long long scratch_stride = 0;
 };
 
@@ -1096,6 +1121,7 @@ void merge_caps(KClass& K, const Caps& e) {
   K.s_cap = std::max(K.s_cap, e.s_cap);
   K.n_cap = std::max(K.n_cap, e.n_cap);
   K.m_cap = std::max(K.m_cap, e.m_cap);
+  K.stage_bytes = std::max(K.stage_bytes, e.stage_bytes);
   if (K.streaming) K.scratch_stride = K.stream_scratch();
 }
 
@@ -1249,6 +1275,19 @@ void build_stream_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_des
   A.add(&E.fib_l0, P.l0);
   A.add(&E.fib_ea, P.ea);
   K.ts = v.T * v.NPT;  // checkpoint slots per CTA
+  // incidence entries of one CTA's rows (staged in shared memory at 20 bytes an entry --
+  // x offset, l0 pair -- plus EA / lumping weight when the launch needs them), the largest
+  // over the cluster's CTAs
+  long long stage = 0;
+  for (int r = 0; r < C; ++r) {
+    long long b = 0;
+    for (int j = 0; j < v.NPT; ++j) {
+      const int g0 = (j * C * v.T + r * v.T) / 32;
+      b += 32ll * (S.group_row0[g0 + v.T / 32] - S.group_row0[g0]);
+    }
+    stage = std::max(stage, b);
+  }
+  K.stage_bytes = stage;
   K.s_cap = TS;
   K.n_cap = P.N;
   K.m_cap = P.M;
@@ -2595,6 +2634,22 @@ int fibra_cuda_selftest_fastmath(fibra_ctx* c, uint64_t n, uint64_t seed, uint64
   FB_CUDA(c, cudaStreamSynchronize(c->stream));
   cudaFree(d);
   *mismatches = h;
+  return FIBRA_OK;
+}
+
+int fibra_cuda_eval_libm(fibra_ctx* c, int32_t which, const double* x, int64_t n, double* out) {
+  if (!c || n < 0 || (n && (!x || !out))) return FIBRA_E_ARG;
+  if (!c->subs.empty()) return fibra_cuda_eval_libm(c->subs[0], which, x, n, out);
+  if (n == 0) return FIBRA_OK;
+  FB_CUDA(c, cudaSetDevice(c->device));
+  double* d = nullptr;
+  FB_CUDA(c, cudaMalloc(&d, 2 * sizeof(double) * n));
+  FB_CUDA(c, cudaMemcpyAsync(d, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  eval_libm_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, c->stream>>>(which, d, n, d + n);
+  FB_CUDA(c, cudaGetLastError());
+  FB_CUDA(c, cudaMemcpyAsync(out, d + n, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+  FB_CUDA(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d);
   return FIBRA_OK;
 }
 

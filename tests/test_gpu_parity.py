@@ -124,9 +124,9 @@ def test_schedule_modes_bitwise(small_lib):
             assert same_bits(getattr(st, k), getattr(s0, k)), k
 
 
-def test_exponential_law_tolerance(oracle_lib):
-    """Exponential law on the resident kernel: libm vs CUDA expm1/exp differ by ulps, so
-    sigma to 1e-12 and the tangent to 1e-8 (test_gpu_cluster.check_exponential)."""
+def test_exponential_law_bitwise(oracle_lib):
+    """Exponential law on the resident kernel, bitwise: expm1 / exp on the device replay the
+    host libm's sequences (csrc/libm_glibc.cuh; test_gpu_cluster.check_exponential)."""
     from test_gpu_cluster import check_exponential
     pn, on = knn(375, 1000, 1)
     F = batch_F(4)
