@@ -283,8 +283,8 @@ def run_reference(args, rank, world):
 
 def measured_traffic(args, n_steps):
     """DRAM bytes per DR launch from the committed ncu --set full capture of this exact
-    workload (profiles/r01_dr_traffic.json), else None."""
-    path = os.path.join(ROOT, "profiles", "r01_dr_traffic.json")
+    workload (profiles/r02_dr_traffic.json), else None."""
+    path = os.path.join(ROOT, "profiles", "r02_dr_traffic.json")
     if args.config != 2 or args.tangent or args.points != DEFAULT_POINTS[2] or not os.path.exists(path):
         return None
     with open(path) as f:
@@ -479,7 +479,7 @@ def main():
             "roofline": {"bound": "fp64_pipe", "achieved": achieved / 1e9, "peak": peak / 1e9,
                          "unit": "Gop/s (FP64-pipe lane ops)", "frac": achieved / peak,
                          "traffic": measured_traffic(args, args.steps),
-                         "traffic_unit": "DRAM bytes per DR launch (ncu --set full, profiles/r01_dr_traffic.json)",
+                         "traffic_unit": "DRAM bytes per DR launch (ncu --set full, profiles/r02_dr_traffic.json)",
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},

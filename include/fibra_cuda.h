@@ -94,8 +94,8 @@ const char* fibra_host_last_error(void);
 int fibra_assign_random(uint64_t seed, int32_t n_points, int32_t n_entries, int32_t* out);
 /* Diagnostics: quality of the bank-aware slot schedule (csrc/host/schedule.cpp) of one
  * network for a kernel shape (T threads, FPT fibers and NPT nodes per thread).
- * out[6] = {fits, conflicting fiber groups, gather excess wavefronts, gather steps,
- *           g*d records, node slots}. */
+ * out[7] = {fits, conflicting fiber groups, gather excess wavefronts, gather steps,
+ *           g*d records, node slots, store excess wavefronts}. */
 int fibra_schedule_report(const fibra_net_desc* net, int T, int FPT, int NPT, int64_t* out);
 /* Diagnostics: that schedule's node slot placement, pn_of_slot[cap] (-1 = empty slot). */
 int fibra_schedule_slots(const fibra_net_desc* net, int T, int FPT, int NPT, int32_t* pn_of_slot,

@@ -21,6 +21,11 @@ ROOT = os.path.dirname(HERE)
 LIB_DIR = os.path.join(HERE, "lib")
 PROF = bool(os.environ.get("FIBRA_PHASE_PROF"))
 LIB = os.path.join(LIB_DIR, "libfibra_b200_prof.so" if PROF else "libfibra_b200.so")
+# diagnostics: FIBRA_LIB=<path> loads a prebuilt layout-experiment library (tools/variants.py)
+# as is, without the staleness rebuild
+LIB_OVERRIDE = os.environ.get("FIBRA_LIB")
+if LIB_OVERRIDE:
+    LIB = LIB_OVERRIDE
 SOURCES = [
     os.path.join(HERE, "csrc", "fibra_cuda.cu"),
     os.path.join(HERE, "csrc", "kernels_resident.cu"),
@@ -61,6 +66,8 @@ def _stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile every translation unit to an object (in parallel), then link the library."""
+    if LIB_OVERRIDE:
+        return LIB
     if not force and not _stale():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)

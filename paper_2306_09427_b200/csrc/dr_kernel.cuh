@@ -25,9 +25,12 @@
 // free; empty fiber/node slots hold harmless dummies so the hot loop has no per-slot
 // branches.  CSR lists are padded to even length with a record of +0.0 (f + 0.0 == f for
 // every f the accumulation can produce, since it starts at +0.0 and never reaches -0.0).
-// The convergence reduction is off the critical path: node threads store one |f|^2
-// partial per node; during the next fiber phase the last warp reduces them (tree order)
-// and the following node phase reads the verdict, one iteration late.  The CTA keeps two
+// The convergence test is off the critical path: node threads store one |f|^2 per slot;
+// during the next fiber phase the last warp -- whose last fiber row is the one left empty
+// when the fibers do not fill every row (its fiber phase is shorter by one fiber) --
+// reduces them with a short branch-free tree and the following node phase reads the
+// verdict, one iteration late.  (Every warp owns fibers; a warp whose last fiber row is
+// empty skips it.)  The CTA keeps two
 // checkpoints of (u, v_half, t, dt) in global memory; when a verdict says "stop at k"
 // (converged, iteration cap, non-finite, or a near tie |R - eps| <= 1e-10 eps where the
 // tree sum could disagree with the reference's 4-lane sum) it restores the newest
@@ -57,7 +60,7 @@ struct EntryDev {          // one RveLibrary entry in HBM, already in slot order
   const int2* csr_pairs;   // [max_pairs][thread_slots] step-major: lanes read consecutive
                            // pairs; entry = 24*gslot | (node is the stored tail) << 31
   const int* fib_ab;       // [fiber_slots] 24*tail_slot | 24*head_slot << 16
-  const int* fib_g;        // [fiber_slots] 24*gslot
+  const int* fib_g;        // [fiber_slots] 24*gslot: the fiber's +g*d record
   const int* fib_id;       // [fiber_slots] reference fiber id, -1 dummy
   const double* fib_l0;    // [fiber_slots]
   const double* fib_ea;    // [fiber_slots] area*modulus
@@ -140,6 +143,14 @@ enum : int { kDecConv = 1, kDecExact = 2, kDecNonfinite = 4 };
 // at most 2C passes.
 constexpr int kCkInterval = 8;
 
+// Diagnostics switches for layout experiments (defaults are the product configuration):
+// FIBRA_TOPO_REG 1 keeps each fiber's x-record offsets, record offset and rest length in
+// registers for the whole solve, 0 re-reads them from L1 every fiber phase.
+#ifndef FIBRA_TOPO_REG
+#define FIBRA_TOPO_REG 1
+#endif
+constexpr int kLag = 1;  // the node phase of pass k reads the verdict of pass k - kLag
+
 // Per-warp phase cycle counters, compiled only into the diagnostics build
 // (FIBRA_PHASE_PROF=1 python -m paper_2306_09427_b200.build -> lib/libfibra_b200_prof.so).
 #ifdef FIBRA_PHASE_PROF
@@ -150,7 +161,8 @@ constexpr int kCkInterval = 8;
 
 struct __align__(16) DrCtl {
   int solve, point, q, entry;
-  int flag, collapse, dec, skip;  // skip: last pass whose exact verdict said "continue"
+  int flag, collapse, skip;  // skip: last pass whose exact verdict said "continue"
+  int dec;                   // speculative verdict of the last pass (the decider warp's)
   double ck_t[2], ck_dt[2];  // checkpoint buffers: t after, dt of, the resume pass
   double warp_min[32];
   double ex[12];
@@ -186,6 +198,12 @@ __device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = smin(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// +1.0 or -1.0 by the CSR entry's bit 31: fma(sign_one(e), r, f) == f + r or f - r, one
+// rounding (the product is exact) -- the gather's signed add in one LOP3 + one DFMA
+__device__ __forceinline__ double sign_one(int entry) {
+  return __hiloint2double((entry & static_cast<int>(0x80000000u)) | 0x3ff00000, 0);
 }
 
 // x or -x, exact: xor of the CSR entry's bit 31 into the sign bit (one LOP3)
@@ -227,12 +245,6 @@ __device__ __forceinline__ double law_energy(double s, double stretch, double rl
   return rl * s / B * (glibc::expm1(B * e) / B - e);
 }
 
-// g*d record offsets in fib_g are 16-bit byte offsets >> kGShift: 8-byte units for the large
-// shapes (FPT >= 4: up to 512 KB of records, ~10k fibres), bytes otherwise (no shift in the
-// hot loop of the config-1/2 shape)
-template <int FPT>
-constexpr int kGShift = FPT >= 4 ? 3 : 0;
-
 // UEA: every fiber of the library has the same area*modulus (true for generated
 // networks), so the axial stiffness s = ea_scale*EA is one scalar instead of FPT registers.
 template <int T, int FPT, int NPT, int LAWBO, int MINB, bool UEA>
@@ -247,19 +259,26 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   const int lane = tid & 31, warp = tid >> 5;
 
   // shared layout: [X: x records (24 B/slot) | exact scratch][G: g*d records | exit scratch]
-  //                [SPART: |f|^2 per node slot][CSR off][CSR entries]
+  //                [SPART: |f|^2 per node slot][CSR entries]
   unsigned char* X = smem;
   unsigned char* G = smem + P.x_bytes;
   double* spart = reinterpret_cast<double*>(G + P.g_bytes);
-  int2* cent = reinterpret_cast<int2*>(spart + P.part_slots);  // step-major CSR pairs
+  int2* cent = reinterpret_cast<int2*>(spart + NPT * T);  // step-major CSR pairs
   double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
 
   const double B = P.nonlinearity;
 
   // register-resident topology of the loaded entry
-  int fab[FPT], fgo[FPT];
-  double fl0[FPT], frl0[FPT], fs[FPT], fmred[FPT];  // frl0: rcp_refined(l0), loop invariant
+  // (x-record offsets, record offset and rest length are re-read from L1 each fiber phase:
+  //  kept in registers they would be live through the node phase's gather, whose loads
+  //  then cannot be issued ahead of their uses under the 2-CTA/SM register budget)
+  double frl0[FPT], fs[FPT], fmred[FPT];  // frl0: rcp_refined(l0), loop invariant
+#if FIBRA_TOPO_REG
+  int fab_r[FPT], fgo_r[FPT];
+  double fl0_r[FPT];
+#endif
   int npair[NPT];
+  int frows = FPT;  // fiber rows holding a real fiber in some lane of this warp
   double ninv[NPT], ncm[NPT];  // (reference coordinates: NREF, read through L1 when used)
   int cur_entry = -1;
   bool first_ticket = true;
@@ -335,20 +354,30 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     if (e != cur_entry) {
       cur_entry = e;
       s_uni = P.ea_scale * E.fib_ea[0];
-      for (int i = tid; i < E.max_pairs * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
-      for (int i = tid; i < E.thread_slots; i += T) spart[i] = 0.0;
+      for (int i = tid; i < (E.max_pairs + 1) * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
       // dummy x records for empty fiber slots, and the zero g*d record (last record)
       if (tid < 6) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid == 3) ? 1.0 : 0.0;
       if (tid < 3) sm_at<double>(G, 24 * (E.gd_slots - 1))[tid] = 0.0;
 #pragma unroll
       for (int j = 0; j < FPT; ++j) {
         const int f = j * T + tid;
-        fab[j] = E.fib_ab[f];
-        fgo[j] = E.fib_g[f];
-        fl0[j] = E.fib_l0[f];
-        frl0[j] = rcp_refined(fl0[j]);
+        {  // (NaN outside [2^-1000, 2^1000]: the fast-path range test then sends the fiber
+           //  to the built-in operators, fastmath.cuh fiber_fast_ok)
+          const double l0 = E.fib_l0[f];
+          frl0[j] = (l0 >= 0x1p-1000 && l0 <= 0x1p1000) ? rcp_refined(l0) : __longlong_as_double(0x7ff8000000000000ll);
+        }
+#if FIBRA_TOPO_REG
+        fab_r[j] = E.fib_ab[f];
+        fgo_r[j] = E.fib_g[f];
+        fl0_r[j] = E.fib_l0[f];
+#endif
         if (!UEA) fs[j] = P.ea_scale * E.fib_ea[f];
       }
+      int rows = 0;
+#pragma unroll
+      for (int j = 0; j < FPT; ++j)
+        if (E.fib_id[j * T + tid] >= 0) rows = j + 1;
+      frows = __reduce_max_sync(0xffffffffu, rows);
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
@@ -364,11 +393,12 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     double lmin = INFINITY;
 #pragma unroll
     for (int j = 0; j < FPT; ++j) {  // reduced_mass_l0 relax.cpp:46-55
-      const int ta = (fab[j] & 0xffff) / 24, hb = (static_cast<unsigned>(fab[j]) >> 16) / 24;
+      const int fab = E.fib_ab[j * T + tid];
+      const int ta = (fab & 0xffff) / 24, hb = (static_cast<unsigned>(fab) >> 16) / 24;
       if (ta < E.thread_slots) {
         const double ma = E.slot_lump[ta] * scale;
         const double mb = E.slot_lump[hb] * scale;
-        fmred[j] = ma * mb / (ma + mb) * fl0[j];
+        fmred[j] = ma * mb / (ma + mb) * E.fib_l0[j * T + tid];
       } else {
         fmred[j] = INFINITY;  // dummy fiber
       }
@@ -452,24 +482,46 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
       FB_PROF(tq = clock64());
-      if (target < 0 && k >= 1 && warp == NW - 1) {  // verdict for pass k-1, tree order
-        // a pass already decided exactly ("continue" at a near tie) is not re-decided
-        double sf = 0, sfix = 0;
-        for (int i = lane; i < F0; i += 32) sf += spart[i];
-        for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
-        sf = warp_sum(sf);
-        sfix = warp_sum(sfix);
+      if (target < 0 && k >= 1 && warp == NW - 1) {  // speculative verdict of pass k-1
+        // Lane l sums slots l, l+32, ...: row r = slot/32 is free iff r < F0/32.  Loads
+        // first, then a tree: the chain is short, so this warp's fiber phase stays below
+        // the full-row warps' (any summation order will do).
+        constexpr int R = NPT * T / 32;
+        const int R0 = F0 >> 5;
+        double vf[R], vx[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double v = spart[32 * r + lane];
+          vf[r] = r < R0 ? v : 0.0;
+          vx[r] = r < R0 ? 0.0 : v;
+        }
+#pragma unroll
+        for (int w = 1; w < R; w *= 2)
+#pragma unroll
+          for (int r = 0; r + w < R; r += 2 * w) {
+            vf[r] += vf[r + w];
+            vx[r] += vx[r + w];
+          }
+        double sf = vf[0], sfix = vx[0];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sf += __shfl_xor_sync(0xffffffffu, sf, o);
+          sfix += __shfl_xor_sync(0xffffffffu, sfix, o);
+        }
+        // squared form of res <= tol * max(sqrt(sfix), floor); a near tie (|res - eps| <=
+        // 1e-10 eps, within ~2e-10 in squares) or a tiny threshold is decided exactly with
+        // the reference's sums; a pass already decided exactly ("continue" at a near tie)
+        // is not re-decided
         if (lane == 0) {
-          const double res = sqrt(sf);
-          const double eps = P.tolerance * smax(sqrt(sfix), ctl.force_floor);
-          int d = (res <= eps) ? kDecConv : 0;
-          if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
-          else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
+          const double fl = ctl.force_floor;
+          const double e2 = (P.tolerance * P.tolerance) * smax(sfix, fl * fl);
+          int d = (sf <= e2) ? kDecConv : 0;
+          if (!isfinite(sf) || !isfinite(e2)) d |= kDecExact | kDecNonfinite;
+          else if (fabs(sf - e2) <= 4e-10 * e2 || e2 < 0x1p-900) d |= kDecExact;
           ctl.dec = (k - 1 > ctl.skip) ? d : 0;
         }
       }
-      if (LAW != 0 && warp == NW - 1 && lane == 0) ctl.warp_min[warp] = INFINITY;
-      if (warp != NW - 1) {  // the reducer warp owns no fibers (host/schedule.cpp)
+      {
         double kmin = INFINITY;
         bool collapsed = false;
         // fibres in blocks of <= 4 so only one block's temporaries are live (the FPT >= 6
@@ -477,22 +529,35 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         auto fiber_block = [&](auto j0c, auto j1c) {
           constexpr int J0 = decltype(j0c)::value, J1 = decltype(j1c)::value;
           bool fast = true;
-          double dx[J1 - J0], dy[J1 - J0], dz[J1 - J0], g[J1 - J0];
+          double dx[J1 - J0], dy[J1 - J0], dz[J1 - J0], g[J1 - J0], fl0[J1 - J0];
+          int fgo[J1 - J0];
 #pragma unroll
           for (int jj = 0; jj < J1 - J0; ++jj) {
             const int j = J0 + jj;
-            const double* xa_ = sm_at<double>(X, fab[j] & 0xffff);
-            const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab[j]) >> 16);
+#if FIBRA_TOPO_REG
+            const int fab = fab_r[j];
+            fgo[jj] = fgo_r[j];
+            fl0[jj] = fl0_r[j];
+#else
+            const int fab = E.fib_ab[j * T + tid];
+            fgo[jj] = E.fib_g[j * T + tid];
+            fl0[jj] = E.fib_l0[j * T + tid];
+#endif
+            const double* xa_ = sm_at<double>(X, fab & 0xffff);
+            const double* xb_ = sm_at<double>(X, static_cast<unsigned>(fab) >> 16);
             dx[jj] = xb_[0] - xa_[0];
             dy[jj] = xb_[1] - xa_[1];
             dz[jj] = xb_[2] - xa_[2];
-            bool o1, o2, o3 = true;
+            bool o1, o2 = true, o3 = true;
             const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
-            collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
-            const double stretch = div_fast_rcp(len, fl0[j], frl0[j], o2);
-            if (LAW == 0) {
-              g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+            collapsed |= (len <= 1e-8 * fl0[jj]);  // network.cpp:291
+            if (LAW == 0) {  // one range test for both divisions (fastmath.cuh)
+              const double stretch = div_rcp_raw(len, fl0[jj], frl0[j]);
+              const double n = law_force<0>(SJ(j), stretch, bo, B);
+              g[jj] = div_rcp_raw(n, len, rcp_refined(len));
+              o2 = fiber_fast_ok(len, stretch, n);
             } else {
+              const double stretch = div_fast_rcp(len, fl0[jj], frl0[j], o2);
               g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
               const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
               kmin = smin(kmin, fmred[j] / kt);
@@ -504,29 +569,33 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
             for (int jj = 0; jj < J1 - J0; ++jj) {
               const int j = J0 + jj;
               const double len = sqrt(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj]);
-              collapsed |= (len <= 1e-8 * fl0[j]);  // exact length (e.g. 0): network.cpp:291
-              const double stretch = len / fl0[j];
+              collapsed |= (len <= 1e-8 * fl0[jj]);  // exact length (e.g. 0): network.cpp:291
+              const double stretch = len / fl0[jj];
               g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
             }
           }
 #pragma unroll
-          for (int jj = 0; jj < J1 - J0; ++jj) {  // head record +g*d, tail (-g)*d == -(g*d)
+          for (int jj = 0; jj < J1 - J0; ++jj) {  // one record +g*d (the tail gathers -1 *)
             const int j = J0 + jj;
-            double* gh = sm_at<double>(G, (static_cast<unsigned>(fgo[j]) >> 16) << kGShift<FPT>);
-            double* gt = sm_at<double>(G, (fgo[j] & 0xffff) << kGShift<FPT>);
-            const double ng = -g[jj];
-            gh[0] = g[jj] * dx[jj];
-            gh[1] = g[jj] * dy[jj];
-            gh[2] = g[jj] * dz[jj];
-            gt[0] = ng * dx[jj];
-            gt[1] = ng * dy[jj];
-            gt[2] = ng * dz[jj];
+            double* gr = sm_at<double>(G, fgo[jj]);
+            gr[0] = g[jj] * dx[jj];
+            gr[1] = g[jj] * dy[jj];
+            gr[2] = g[jj] * dz[jj];
           }
         };
         constexpr int B1 = FPT < 4 ? FPT : (FPT + 1) / 2;
-        fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, B1>());
-        if constexpr (B1 < FPT)
-          fiber_block(std::integral_constant<int, B1>(), std::integral_constant<int, FPT>());
+        if constexpr (B1 < FPT) {
+          fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, B1>());
+          if (frows > B1)
+            fiber_block(std::integral_constant<int, B1>(), std::integral_constant<int, FPT>());
+        } else if constexpr (FPT >= 2) {
+          if (frows == FPT)
+            fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, FPT>());
+          else  // the warp's last fiber row is empty
+            fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, FPT - 1>());
+        } else {
+          fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, FPT>());
+        }
         if (collapsed) ctl.collapse = 1;
         if (LAW != 0) {
           kmin = warp_min(kmin);
@@ -538,13 +607,14 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       FB_PROF({ const long long t1 = clock64(); pc1 += t1 - tq; tq = t1; })
 
       // ================= node phase (pass k) =================
-      if (target < 0 && k >= 1) {
-        const int d = ctl.dec;
-        if ((d & (kDecConv | kDecExact)) || k - 1 == P.max_iterations) {
-          // stop at k-1: replay from the newest checkpoint that resumes at or before it
-          target = k - 1;
+      if (target < 0 && k >= kLag) {
+        const int dec = ctl.dec;
+        if ((dec & (kDecConv | kDecExact)) || k - kLag == P.max_iterations) {
+          // stop at k-kLag: replay from the newest checkpoint that resumes at or before it
+          target = k - kLag;
           // resume points are the multiples of kCkInterval, alternating between buffers;
-          // the newest one <= target is still held (the save at target+1 used the other)
+          // the newest one <= target is still held (the saves at target+1 .. target+kLag --
+          // at most one of them, kCkInterval > kLag -- used the other)
           k = target / kCkInterval * kCkInterval;
           const int b = (k / kCkInterval) & 1;
           dt_k = ctl.ck_dt[b];
@@ -590,24 +660,30 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
         double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
-#pragma unroll 2
+        // the next step's pair is loaded one step ahead (row max_pairs is padding), so a
+        // step's six record loads depend only on registers and issue back to back
+        int2 ep = cent[sl];
         for (int kp = 0; kp < npair[j]; ++kp) {  // two incidences per step
-          const int2 ep = cent[kp * (NPT * T) + sl];
-          const double* g0 = sm_at<double>(G, ep.x);  // this node's own signed record
-          const double* g1 = sm_at<double>(G, ep.y);
+          const int2 en = cent[(kp + 1) * (NPT * T) + sl];
+          const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);  // the fiber's +g*d
+          const double* g1 = sm_at<double>(G, ep.y & 0x7fffffff);
           const double a0 = g0[0], a1 = g0[1], a2 = g0[2];
           const double b0 = g1[0], b1 = g1[1], b2 = g1[2];
-          f0 = f0 + a0;  // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
-          f1 = f1 + a1;
-          f2 = f2 + a2;
-          f0 = f0 + b0;
-          f1 = f1 + b1;
-          f2 = f2 + b2;
+          const double sa = sign_one(ep.x), sb = sign_one(ep.y);  // -1 for the tail
+          // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
+          f0 = __fma_rn(sa, a0, f0);
+          f1 = __fma_rn(sa, a1, f1);
+          f2 = __fma_rn(sa, a2, f2);
+          f0 = __fma_rn(sb, b0, f0);
+          f1 = __fma_rn(sb, b1, f1);
+          f2 = __fma_rn(sb, b2, f2);
+          ep = en;
         }
         fk[j][0] = f0;
         fk[j][1] = f1;
         fk[j][2] = f2;
-        spart[sl] = f0 * f0 + f1 * f1 + f2 * f2;
+        const double q = f0 * f0 + f1 * f1 + f2 * f2;
+        spart[sl] = q;
       }
       if (k == target) {
         // ---- exact verdict at the target pass (reference-order norms) ----
@@ -760,13 +836,15 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       for (int j = 0; j < FPT; ++j) {
         const int f = E.fib_id[j * T + tid];
         if (f >= 0) {  // strain_energy relax.cpp:57-72 (reference fiber id order)
-          const int ta = E.slot_pn[(fab[j] & 0xffff) / 24];
-          const int hb = E.slot_pn[(static_cast<unsigned>(fab[j]) >> 16) / 24];
+          const int fab = E.fib_ab[j * T + tid];
+          const int ta = E.slot_pn[(fab & 0xffff) / 24];
+          const int hb = E.slot_pn[(static_cast<unsigned>(fab) >> 16) / 24];
           const double dx = SX[3 * hb] - SX[3 * ta];
           const double dy = SX[3 * hb + 1] - SX[3 * ta + 1];
           const double dz = SX[3 * hb + 2] - SX[3 * ta + 2];
           const double len = sqrt(dx * dx + dy * dy + dz * dz);
-          SE[f] = law_energy<LAW>(SJ(j), len / fl0[j], fl0[j], bo, B);
+          const double l0 = E.fib_l0[j * T + tid];
+          SE[f] = law_energy<LAW>(SJ(j), len / l0, l0, bo, B);
         }
       }
     }

@@ -374,7 +374,7 @@ struct KClass {
     if (node) return node_smem(true);
     if (cluster)
       return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 8ull * csr_cap + 4ull * push_cap;
-    return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 4ull * (ts + 1) + 4ull * csr_cap;
+    return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 4ull * csr_cap;  // dr_kernel.cuh
   }
 };
 
@@ -1038,12 +1038,11 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
   if (!build_schedule(P.N, P.NFN, P.M, P.a.data(), P.b.data(), v.T, v.FPT, v.NPT, S))
     return false;
   const int TS = v.NPT * v.T;
-  const int gd_total = S.gd_slots + 33;
-  const int gshift = v.FPT >= 4 ? 3 : 0;  // kGShift (dr_kernel.cuh)
-  if (S.node_slots * 24 >= 65536 || ((24 * gd_total) >> gshift) >= 65536) return false;  // 16 bit
+  const int gd_total = S.gd_slots + 17;  // + per-lane dummy records + the zero record
+  if (S.node_slots * 24 >= 65536) return false;  // 16-bit x-record offsets
   const size_t smem = align16(24 * static_cast<size_t>(TS + 2)) +
                       align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
-                      8ull * TS + 4ull * (TS + 1) + 8ull * max_pairs * TS;
+                      8ull * TS + 8ull * (max_pairs + 1) * TS;
   return smem <= static_cast<size_t>(c->max_smem);
 }
 
@@ -1298,7 +1297,6 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
                           const Variant& v, Arena& A, Caps& K) {
   const Schedule& S = de.sched;
   const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS, TS+1
-  const int gshift = v.FPT >= 4 ? 3 : 0;  // record offsets in 8-byte units (kGShift)
   const int FS = S.fiber_slots;
   std::vector<int> slot_pn(TS, -1);
   std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
@@ -1309,20 +1307,17 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
     slot_lump[sl] = P.lump[pn];
   }
-  // g*d records: [real: tail (-g*d) and head (+g*d) per fiber, schedule colouring]
-  //               [two per dummy fiber slot, bank = lane] [zero record]
-  // (all dummies of one lane share a record pair: their values are never read, and within
-  //  one store instruction the 16 lanes still hit 16 different banks)
-  std::vector<int> dummy_tail(FS, -1), dummy_head(FS, -1);
+  // g*d records: [real: +g*d per fiber, schedule colouring] [one per dummy fiber slot,
+  // bank = lane] [zero record]  (all dummies of one lane share a record: their values are
+  // never read, and within one store instruction the 16 lanes still hit 16 banks)
+  std::vector<int> dummy_rec(FS, -1);
   for (int fs = 0; fs < FS; ++fs)
-    if (S.fiber_of_fslot[fs] < 0) {
-      dummy_tail[fs] = S.gd_slots + fs % 16;
-      dummy_head[fs] = S.gd_slots + 16 + fs % 16;
-    }
-  const int zero_rec = S.gd_slots + 32;
+    if (S.fiber_of_fslot[fs] < 0) dummy_rec[fs] = S.gd_slots + fs % 16;
+  const int zero_rec = S.gd_slots + 16;
   const int gd_total = zero_rec + 1;
   // CSR by slot, ascending fiber id, padded to even length with the zero record;
-  // entry = byte offset of the node's own record of that fiber
+  // entry = byte offset of the fiber's record | 1u << 31 when the node is the fiber's tail
+  // (the gather adds -1 * record: f - g*d, network.cpp:298-303)
   std::vector<std::vector<int>> lists(TS);
   for (int f = 0; f < P.M; ++f) {
     lists[S.slot_of_pn[S.tail_pn[f]]].push_back(f);
@@ -1333,16 +1328,17 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     std::sort(lists[sl].begin(), lists[sl].end());  // reference order (network.cpp:298-303)
     max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
   }
-  // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step)
-  std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs) * TS, 24 * zero_rec);
+  // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step), plus
+  // one padding row of zero-record pairs (the gather loads the next step's pair ahead)
+  std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs + 1) * TS, 24 * zero_rec);
   for (int sl = 0; sl < TS; ++sl) {
     const auto& L = lists[sl];
     const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
     npairs[sl] = static_cast<int>((L.size() + 1) / 2);
     for (size_t i = 0; i < L.size(); ++i) {
       const int f = L[i];
-      ent[2 * ((i / 2) * TS + sl) + (i % 2)] =
-          24 * (pn == S.tail_pn[f] ? S.rec_tail[f] : S.rec_head[f]);
+      const unsigned neg = pn == S.tail_pn[f] ? 0x80000000u : 0u;
+      ent[2 * ((i / 2) * TS + sl) + (i % 2)] = static_cast<int>((24u * S.rec[f]) | neg);
     }
   }
   std::vector<int> fab(FS), fg(FS), fid(FS, -1);
@@ -1351,11 +1347,11 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     const int f = S.fiber_of_fslot[fs];
     if (f < 0) {  // dummy: unit segment between the two dummy x records
       fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
-      fg[fs] = ((24 * dummy_tail[fs]) >> gshift) | (((24 * dummy_head[fs]) >> gshift) << 16);
+      fg[fs] = 24 * dummy_rec[fs];
       continue;
     }
     fab[fs] = (24 * S.slot_of_pn[S.tail_pn[f]]) | ((24 * S.slot_of_pn[S.head_pn[f]]) << 16);
-    fg[fs] = ((24 * S.rec_tail[f]) >> gshift) | (((24 * S.rec_head[f]) >> gshift) << 16);
+    fg[fs] = 24 * S.rec[f];
     fid[fs] = f;
     fl0[fs] = P.l0[f];
     fea[fs] = P.ea[f];
@@ -2171,8 +2167,8 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
         est[i].ts = TS;
         est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2)));
         est[i].g_bytes = static_cast<int>(align16(std::max<size_t>(
-            24ull * (de.sched.gd_slots + 33), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
-        est[i].csr_cap = 2 * mp * TS;
+            24ull * (de.sched.gd_slots + 17), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
+        est[i].csr_cap = 2 * (mp + 1) * TS;  // + the padding row
       }
     // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
     // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
@@ -2869,7 +2865,7 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
     std::memcpy(f.first, &addr, sizeof addr);
   }
   const EntryDev& E = de.dev;
-  const int TS = E.thread_slots, FS = E.fiber_slots, gshift = v.FPT >= 4 ? 3 : 0;
+  const int TS = E.thread_slots, FS = E.fiber_slots;
   std::vector<double> X(3 * static_cast<size_t>(TS + 2), 0.0), G(3 * static_cast<size_t>(E.gd_slots), 0.0);
   X[3 * TS + 3] = 1.0;
   auto x_of = [&](int pn, int c) { return P.ref[3 * pn + c] + u[3 * pn + c]; };
@@ -2886,15 +2882,9 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
     }
     const double L = std::sqrt(dd), l0 = E.fib_l0[fs];
     const double g = E.fib_ea[fs] * (L - l0) / (l0 * L);
-    const int gt = ((E.fib_g[fs] & 0xffff) << gshift) / 8;
-    const int gh = ((static_cast<unsigned>(E.fib_g[fs]) >> 16) << gshift) / 8;
-    if (E.fib_id[fs] >= 0) {
-      if (written[gt / 3]++ || written[gh / 3]++) return 200;  // two fibers on one record
-    }
-    for (int c = 0; c < 3; ++c) {
-      G[gt + c] = -(g * dx[c]);
-      G[gh + c] = g * dx[c];
-    }
+    const int gr = E.fib_g[fs] / 8;
+    if (E.fib_id[fs] >= 0 && written[gr / 3]++) return 200;  // two fibers on one record
+    for (int c = 0; c < 3; ++c) G[gr + c] = g * dx[c];
   }
   for (int c = 0; c < 3; ++c) G[3 * (E.gd_slots - 1) + c] = 0.0;
   for (int i = 0; i < 3 * P.N; ++i) f_emul[i] = f_direct[i] = 0.0;
@@ -2903,7 +2893,9 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
     if (pn < 0) continue;
     for (int i = 0; i < 2 * E.csr_npairs[sl]; ++i) {
       const int e = reinterpret_cast<const int*>(E.csr_pairs)[2 * ((i / 2) * TS + sl) + (i % 2)];
-      for (int c = 0; c < 3; ++c) f_emul[3 * pn + c] += G[e / 8 + c];
+      const int r = (e & 0x7fffffff) / 8;
+      for (int c = 0; c < 3; ++c)  // f + (-1) * (g*d) == f - g*d
+        f_emul[3 * pn + c] = e < 0 ? f_emul[3 * pn + c] - G[r + c] : f_emul[3 * pn + c] + G[r + c];
     }
   }
   for (int f = 0; f < P.M; ++f) {

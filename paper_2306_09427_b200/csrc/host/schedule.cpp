@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <array>
 #include <cstdint>
 #include <numeric>
@@ -63,11 +65,10 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
   s.f0 = (NFN + 31) / 32 * 32;
   s.node_slots = s.f0 + (s.n_fix_nodes + 31) / 32 * 32;
   s.fiber_slots = FPT * T;
-  // the last warp reduces the convergence partials during the fiber phase and owns no
-  // fibers (dr_kernel.cuh); its fiber groups stay empty
-  const int reserved_warp = T / 32 - 1;
-  auto usable = [&](int g) { return (g % (T / kBanks)) / 2 != reserved_warp; };
-  if (s.node_slots > NPT * T || M > FPT * (T - 32)) return false;
+  // every warp owns fibers; groups fill row by row (fiber slot j*T + tid), so the empty
+  // slots gather in the last row of the last warps, which skip it (dr_kernel.cuh)
+  auto usable = [&](int) { return true; };
+  if (s.node_slots > NPT * T || M > FPT * T) return false;
 
   std::vector<int> deg(N, 0);
   for (int f = 0; f < M; ++f) {
@@ -175,12 +176,13 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
     s.groups_conflicting += conflict;
   }
 
-  // ---- g*d records: each fiber writes a tail record (-g*d) and a head record (+g*d), each
-  // read by exactly one gather step.  A record is an edge between its store group (the
-  // half-warp STS instruction that writes it: fiber group x {tail, head}) and its gather
-  // group (half-warp of the reading node x step in that node's list).  Both sides have
-  // degree <= 16, so the bipartite multigraph is 16-edge-colourable (Koenig); colour c
-  // becomes bank 3c mod 16 of the record and every store and gather is conflict-free.
+  // ---- g*d records: one per fiber (+g*d), written by its fiber group's store and read by
+  // two gather steps -- the tail's (negated) and the head's.  A record's colour c (bank
+  // 3c mod 16) should be unique at each of those three "vertices": the store group, and
+  // the (node half-warp, list position) of each reader.  Three vertices per record make
+  // this a hypergraph colouring, so it is found by min-conflict search; a leftover
+  // conflict costs one extra shared-memory wavefront, never a wrong result.  Gather
+  // conflicts (the node phase is the critical path) weigh twice a store conflict.
   std::vector<int> group_of(M, 0);
   for (int g = 0; g < n_groups; ++g)
     for (int f : best_groups[g]) group_of[f] = g;
@@ -190,83 +192,146 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
     inc_fibers[b_pn[f]].push_back(f);
   }
   int max_deg = 0;
-  for (int pn = 0; pn < N; ++pn) max_deg = std::max<int>(max_deg, inc_fibers[pn].size());
-  const int n_hw = s.node_slots / kBanks;
-  // edges: 2f = tail record, 2f+1 = head record
-  std::vector<int> eL(2 * M), eR(2 * M);
-  for (int f = 0; f < M; ++f) {
-    eL[2 * f] = 2 * group_of[f];
-    eL[2 * f + 1] = 2 * group_of[f] + 1;
+  for (int pn = 0; pn < N; ++pn) {
+    std::sort(inc_fibers[pn].begin(), inc_fibers[pn].end());  // the gather's list order
+    max_deg = std::max<int>(max_deg, inc_fibers[pn].size());
   }
+  const int n_hw = s.node_slots / kBanks;
+  // vertices: [0, n_groups) store groups, then n_hw * max_deg gather vertices
+  std::vector<std::array<int, 3>> vert(M);
+  for (int f = 0; f < M; ++f) vert[f] = {group_of[f], -1, -1};
   for (int pn = 0; pn < N; ++pn) {
     const int hw = s.slot_of_pn[pn] / kBanks;
     for (int k = 0; k < static_cast<int>(inc_fibers[pn].size()); ++k) {
       const int f = inc_fibers[pn][k];
-      eR[2 * f + (pn == s.tail_pn[f] ? 0 : 1)] = hw * max_deg + k;
+      const int v = n_groups + hw * max_deg + k;
+      if (vert[f][1] < 0) vert[f][1] = v;
+      else if (vert[f][1] != v) vert[f][2] = v;  // same vertex: one broadcast read
     }
   }
-  const int nL = 2 * n_groups, nR = n_hw * max_deg;
-  std::vector<std::array<int, kBanks>> atL(nL), atR(nR);  // edge holding colour c, or -1
-  for (auto& x : atL) x.fill(-1);
-  for (auto& x : atR) x.fill(-1);
-  std::vector<int> colour(2 * M, -1);
-  bool perfect = true;
-  for (int e = 0; e < 2 * M; ++e) {
-    const int u = eL[e], v = eR[e];
-    int a = -1, b = -1;
-    for (int c = 0; c < kBanks && a < 0; ++c)
-      if (atL[u][c] < 0) a = c;
-    for (int c = 0; c < kBanks && b < 0; ++c)
-      if (atR[v][c] < 0) b = c;
-    if (a < 0 || b < 0) {  // degree > 16 (cannot happen for <= 16-lane groups)
-      perfect = false;
-      colour[e] = 0;
-      continue;
-    }
-    if (atR[v][a] >= 0) {
-      // a is free at u, taken at v; b free at v.  Swap a<->b along the alternating path
-      // that starts at v with colour a; it cannot reach u, after which a is free at v.
-      std::vector<int> path;
-      int node = v, side = 1, c = a;
-      for (;;) {
-        const int pe = side ? atR[node][c] : atL[node][c];
-        if (pe < 0) break;
-        path.push_back(pe);
-        node = side ? eL[pe] : eR[pe];
-        side ^= 1;
-        c = (c == a) ? b : a;
-      }
-      for (int pe : path) {
-        atL[eL[pe]][colour[pe]] = -1;
-        atR[eR[pe]][colour[pe]] = -1;
-      }
-      for (int pe : path) {
-        colour[pe] = (colour[pe] == a) ? b : a;
-        atL[eL[pe]][colour[pe]] = pe;
-        atR[eR[pe]][colour[pe]] = pe;
+  const int nV = n_groups + n_hw * max_deg;
+  std::vector<std::array<int, kBanks>> cnt(nV);
+  for (auto& x : cnt) x.fill(0);
+  std::array<int, kBanks> used{};
+  std::vector<int> colour(M, -1);
+  auto weight = [&](int i) { return i == 0 ? 1 : 2; };
+  auto cost = [&](int f, int c) {  // conflicts f would add with colour c
+    int w = 0;
+    for (int i = 0; i < 3; ++i)
+      if (vert[f][i] >= 0) w += weight(i) * cnt[vert[f][i]][c];
+    return w;
+  };
+  auto place = [&](int f, int c, int d) {
+    for (int i = 0; i < 3; ++i)
+      if (vert[f][i] >= 0) cnt[vert[f][i]][c] += d;
+    used[c] += d;
+  };
+  // greedy in order of descending gather degree of the readers (hardest first)
+  std::vector<int> order_f(M);
+  std::iota(order_f.begin(), order_f.end(), 0);
+  std::stable_sort(order_f.begin(), order_f.end(), [&](int x, int y) {
+    return deg[a_pn[x]] + deg[b_pn[x]] > deg[a_pn[y]] + deg[b_pn[y]];
+  });
+  for (int f : order_f) {
+    int best = 0, bc = -1;
+    for (int c = 0; c < kBanks; ++c) {
+      const int w = cost(f, c);
+      if (bc < 0 || w < bc || (w == bc && used[c] < used[best])) {
+        bc = w;
+        best = c;
       }
     }
-    colour[e] = a;
-    atL[u][a] = e;
-    atR[v][a] = e;
+    colour[f] = best;
+    place(f, best, 1);
+  }
+  // tabu search (TabuCol) on the weighted conflict count: the best non-tabu recolouring of
+  // a conflicting record per step; a record may not return to a colour it just left
+  std::vector<std::vector<int>> at(nV);  // vertex -> records
+  for (int f = 0; f < M; ++f)
+    for (int i = 0; i < 3; ++i)
+      if (vert[f][i] >= 0) at[vert[f][i]].push_back(f);
+  std::vector<std::array<int, kBanks>> gam(M);  // weighted conflicts of f in colour c
+  for (int f = 0; f < M; ++f) {
+    place(f, colour[f], -1);
+    for (int c = 0; c < kBanks; ++c) gam[f][c] = cost(f, c);
+    place(f, colour[f], 1);
+  }
+  long conflicts = 0;
+  for (int f = 0; f < M; ++f) conflicts += gam[f][colour[f]];
+  conflicts /= 2;  // each conflicting pair is seen from both records
+  if (getenv("FIBRA_SCHED_DEBUG")) fprintf(stderr, "colouring: greedy conflicts %ld\n", conflicts);
+  std::vector<int> best_colour = colour;
+  long best_conflicts = conflicts;
+  std::vector<std::array<long, kBanks>> tabu(M);
+  for (auto& x : tabu) x.fill(0);
+  std::mt19937 crng(777);
+  const long max_iter = 40000;
+  long dbg_it = 0;
+  for (long it = 1; it <= max_iter && conflicts > 0; ++it) {
+    dbg_it = it;
+    int bf = -1, bcol = -1, bdelta = 0, ties = 0;
+    for (int f = 0; f < M; ++f) {
+      const int cur = gam[f][colour[f]];
+      if (cur == 0) continue;
+      for (int c = 0; c < kBanks; ++c) {
+        if (c == colour[f]) continue;
+        const int delta = gam[f][c] - cur;
+        const bool allowed = tabu[f][c] < it || conflicts + delta < best_conflicts;
+        if (!allowed) continue;
+        if (bf < 0 || delta < bdelta) {
+          bf = f; bcol = c; bdelta = delta; ties = 1;
+        } else if (delta == bdelta && std::uniform_int_distribution<int>(0, ties++)(crng) == 0) {
+          bf = f; bcol = c;
+        }
+      }
+    }
+    if (bf < 0) break;
+    const int old = colour[bf];
+    for (int i = 0; i < 3; ++i) {
+      const int v = vert[bf][i];
+      if (v < 0) continue;
+      const int w = weight(i);  // the vertex's kind: store group or gather step
+      for (int f2 : at[v]) {
+        if (f2 == bf) continue;
+        gam[f2][old] -= w;
+        gam[f2][bcol] += w;
+      }
+    }
+    place(bf, old, -1);
+    colour[bf] = bcol;
+    place(bf, bcol, 1);
+    conflicts += bdelta;
+    tabu[bf][old] = it + 10 + static_cast<long>(crng() % 10);
+    if (conflicts < best_conflicts) {
+      best_conflicts = conflicts;
+      best_colour = colour;
+    }
+  }
+  if (getenv("FIBRA_SCHED_DEBUG"))
+    fprintf(stderr, "colouring: conflicts %ld best %ld iters %ld\n", conflicts, best_conflicts, dbg_it);
+  if (best_conflicts < conflicts) {
+    for (int f = 0; f < M; ++f) place(f, colour[f], -1);
+    colour = best_colour;
+    for (int f = 0; f < M; ++f) place(f, colour[f], 1);
   }
   s.gather_steps = 0;
-  for (int v = 0; v < nR; ++v) {
-    bool any = false;
-    for (int c = 0; c < kBanks; ++c) any |= atR[v][c] >= 0;
-    s.gather_steps += any;
+  for (int v = n_groups; v < nV; ++v) {
+    int any = 0;
+    for (int c = 0; c < kBanks; ++c) any |= cnt[v][c];
+    s.gather_steps += any != 0;
   }
-  s.gather_excess = perfect ? 0 : -1;
-  std::array<int, kBanks> used{};
-  s.rec_tail.assign(M, -1);
-  s.rec_head.assign(M, -1);
-  for (int f = 0; f < M; ++f) {  // record index = colour + 16 * (running count of colour)
-    const int ct = colour[2 * f], ch = colour[2 * f + 1];
-    s.rec_tail[f] = ct + kBanks * used[ct]++;
-    s.rec_head[f] = ch + kBanks * used[ch]++;
+  s.gather_excess = 0;   // extra wavefronts: gather vertices
+  s.store_excess = 0;    // and store groups
+  for (int v = 0; v < nV; ++v) {
+    int mx = 0;
+    for (int c = 0; c < kBanks; ++c) mx = std::max(mx, cnt[v][c]);
+    if (mx > 1) (v < n_groups ? s.store_excess : s.gather_excess) += mx - 1;
   }
+  s.rec.assign(M, -1);
+  std::array<int, kBanks> run{};
+  for (int f = 0; f < M; ++f) s.rec[f] = colour[f] + kBanks * run[colour[f]]++;
   int mx = 0;
-  for (int v : used) mx = std::max(mx, v);
+  for (int v : run) mx = std::max(mx, v);
   s.gd_slots = kBanks * std::max(mx, 1);
   return true;
 }
@@ -304,6 +369,7 @@ extern "C" int fibra_schedule_report(const fibra_net_desc* d, int T, int FPT, in
   out[0] = ok;
   out[1] = s.groups_conflicting;
   out[2] = s.gather_excess;
+  out[6] = s.store_excess;
   out[3] = s.gather_steps;
   out[4] = s.gd_slots;
   out[5] = s.node_slots;

@@ -13,8 +13,9 @@
 //     paths/cycles, so after choosing each fiber's orientation the 16 "tail" loads and the
 //     16 "head" loads are bank-distinct.  Swapping a fiber's endpoints is bitwise neutral:
 //     x_a - x_b == -(x_b - x_a) and g*(-d) == -(g*d) in IEEE arithmetic;
-//   * g*d record slots: bank-distinct inside every fiber group (conflict-free stores) and,
-//     by min-conflict search, inside every gather step of every node half-warp.
+//   * g*d record slots, one per fiber: bank-distinct inside every fiber group (stores) and
+//     inside every gather step of every node half-warp (the tail's and the head's read),
+//     by min-conflict search.
 // Nothing here changes an arithmetic operation or its order: the reference accumulation
 // order (ascending fiber id per node, network.cpp:298-303) is kept in each node's CSR list.
 #pragma once
@@ -33,10 +34,11 @@ struct Schedule {
   std::vector<int> slot_of_pn, pn_of_slot;      // node placement (-1 empty)
   std::vector<int> fiber_of_fslot;              // fiber placement (-1 empty)
   std::vector<int> tail_pn, head_pn;            // stored orientation per fiber
-  std::vector<int> rec_tail, rec_head;          // g*d records per fiber (-g*d, +g*d)
+  std::vector<int> rec;                         // g*d record per fiber (+g*d)
   // quality report
   int groups_conflicting = 0;       // fiber groups with a bank conflict on x loads
-  long gather_excess = 0;           // 0 when the record colouring is perfect, -1 otherwise
+  long gather_excess = 0;           // extra wavefronts of the record colouring: gathers
+  long store_excess = 0;            //   and g*d stores (0 and 0: perfect)
   long gather_steps = 0;
 };
 

@@ -242,6 +242,33 @@ def test_reference_arm_workload_matches_product():
         assert min(len(s) for s in sl) >= 32
 
 
+def test_resident_kernel_force_emulation_bitwise():
+    """Resident kernel tables (fibra_debug_resident_forces: host emulation of one force pass
+    from the uploaded slot arrays -- one +g*d record per fiber at its coloured slot, each
+    node's step-major CSR list with the tail's entries flagged to subtract): the same bits
+    as accumulating f[b] += g*d, f[a] -= g*d in fiber-id order (network.cpp:298-303), for
+    every resident shape that holds the network."""
+    from paper_2306_09427_b200 import _capi, synth
+    lib = _capi.load()
+    for spec, seed in ((synth.config1_spec(), 1),
+                       (P.NetGenSpec(style="knn", nodes=20, fibers=56, neighbors=10), 31)):
+        net = P.generate_network(spec, seed)
+        checked = 0
+        for sh in range(6):
+            u = np.random.default_rng(sh).normal(0, 0.01, net.n_dof)
+            fe, fd = np.zeros(net.n_dof), np.zeros(net.n_dof)
+            r = lib.fibra_debug_resident_forces(net.desc(), sh, u.ctypes.data_as(_capi._dp),
+                                                fe.ctypes.data_as(_capi._dp),
+                                                fd.ctypes.data_as(_capi._dp))
+            if r == 200:
+                raise AssertionError("two fibers share a g*d record")
+            if r:
+                continue
+            checked += 1
+            assert np.array_equal(fe.view(np.uint64), fd.view(np.uint64))
+        assert checked >= 3
+
+
 def test_node_kernel_force_emulation_bitwise():
     """Node-centric kernel tables (fibra_debug_node_forces, host emulation of one force pass
     from the uploaded incidence tables with d' = x_other - x_own, f -= g d' from +0.0): the
