@@ -149,7 +149,13 @@ constexpr int kCkInterval = 8;
 #ifndef FIBRA_TOPO_REG
 #define FIBRA_TOPO_REG 1
 #endif
-constexpr int kLag = 1;  // the node phase of pass k reads the verdict of pass k - kLag
+// FIBRA_DECIDER_NODE 1: the last warp decides pass k-1 at the end of node phase k (its
+// gather is the lightest) and node phase k+1 reads it; 0: it decides in fiber phase k and
+// node phase k reads it.
+#ifndef FIBRA_DECIDER_NODE
+#define FIBRA_DECIDER_NODE 1
+#endif
+constexpr int kLag = FIBRA_DECIDER_NODE ? 2 : 1;  // node phase k reads the verdict of k-kLag
 
 // Per-warp phase cycle counters, compiled only into the diagnostics build
 // (FIBRA_PHASE_PROF=1 python -m paper_2306_09427_b200.build -> lib/libfibra_b200_prof.so).
@@ -162,7 +168,7 @@ constexpr int kLag = 1;  // the node phase of pass k reads the verdict of pass k
 struct __align__(16) DrCtl {
   int solve, point, q, entry;
   int flag, collapse, skip;  // skip: last pass whose exact verdict said "continue"
-  int dec;                   // speculative verdict of the last pass (the decider warp's)
+  int dec[2];                // speculative verdict of pass r in dec[r & 1] (decider warp)
   double ck_t[2], ck_dt[2];  // checkpoint buffers: t after, dt of, the resume pass
   double warp_min[32];
   double ex[12];
@@ -262,8 +268,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
   //                [SPART: |f|^2 per node slot][CSR entries]
   unsigned char* X = smem;
   unsigned char* G = smem + P.x_bytes;
-  double* spart = reinterpret_cast<double*>(G + P.g_bytes);
-  int2* cent = reinterpret_cast<int2*>(spart + NPT * T);  // step-major CSR pairs
+  double* spart = reinterpret_cast<double*>(G + P.g_bytes);  // [kLag][NPT * T]
+  int2* cent = reinterpret_cast<int2*>(spart + kLag * NPT * T);  // step-major CSR pairs
   double* ckpt = P.ckpt + static_cast<size_t>(blockIdx.x) * 12 * P.ck_stride;
 
   const double B = P.nonlinearity;
@@ -482,25 +488,26 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
       FB_PROF(tq = clock64());
-      if (target < 0 && k >= 1 && warp == NW - 1) {  // speculative verdict of pass k-1
-        // Lane l sums slots l, l+32, ...: row r = slot/32 is free iff r < F0/32.  Loads
-        // first, then a tree: the chain is short, so this warp's fiber phase stays below
-        // the full-row warps' (any summation order will do).
+      // Speculative verdict of pass r by the last warp.  Lane l sums slots l, l+32, ...:
+      // row i = slot/32 is free iff i < F0/32.  Loads first, then a tree: a short chain
+      // (any summation order will do).
+      auto decide = [&](int r) {
         constexpr int R = NPT * T / 32;
         const int R0 = F0 >> 5;
+        const double* sp = spart + (r % kLag) * (NPT * T);
         double vf[R], vx[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double v = spart[32 * r + lane];
-          vf[r] = r < R0 ? v : 0.0;
-          vx[r] = r < R0 ? 0.0 : v;
+        for (int i = 0; i < R; ++i) {
+          const double v = sp[32 * i + lane];
+          vf[i] = i < R0 ? v : 0.0;
+          vx[i] = i < R0 ? 0.0 : v;
         }
 #pragma unroll
         for (int w = 1; w < R; w *= 2)
 #pragma unroll
-          for (int r = 0; r + w < R; r += 2 * w) {
-            vf[r] += vf[r + w];
-            vx[r] += vx[r + w];
+          for (int i = 0; i + w < R; i += 2 * w) {
+            vf[i] += vf[i + w];
+            vx[i] += vx[i + w];
           }
         double sf = vf[0], sfix = vx[0];
 #pragma unroll
@@ -518,9 +525,10 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           int d = (sf <= e2) ? kDecConv : 0;
           if (!isfinite(sf) || !isfinite(e2)) d |= kDecExact | kDecNonfinite;
           else if (fabs(sf - e2) <= 4e-10 * e2 || e2 < 0x1p-900) d |= kDecExact;
-          ctl.dec = (k - 1 > ctl.skip) ? d : 0;
+          ctl.dec[r & 1] = (r > ctl.skip) ? d : 0;
         }
-      }
+      };
+      if (!FIBRA_DECIDER_NODE && target < 0 && k >= 1 && warp == NW - 1) decide(k - 1);
       {
         double kmin = INFINITY;
         bool collapsed = false;
@@ -608,7 +616,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 
       // ================= node phase (pass k) =================
       if (target < 0 && k >= kLag) {
-        const int dec = ctl.dec;
+        const int dec = ctl.dec[(k - kLag) & 1];
         if ((dec & (kDecConv | kDecExact)) || k - kLag == P.max_iterations) {
           // stop at k-kLag: replay from the newest checkpoint that resumes at or before it
           target = k - kLag;
@@ -640,9 +648,13 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           }
           rewrite_fixed = false;
           __syncthreads();
+          // verdicts of passes before the replay are void (every read of them is done)
+          if (FIBRA_DECIDER_NODE && tid == 0) ctl.dec[0] = ctl.dec[1] = 0;
           continue;
         }
       }
+      // the last warp decides pass k-1 at the end of this phase (not at an exact pass)
+      const bool decide_here = FIBRA_DECIDER_NODE && target < 0 && k >= 1 && warp == NW - 1;
       if (k >= 1) {  // commit iteration k (relax.cpp:150-153)
         if (!isfinite(dt_k) || !(dt_k > 0)) {
           status = FIBRA_E_BAD_DT;
@@ -683,7 +695,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         fk[j][1] = f1;
         fk[j][2] = f2;
         const double q = f0 * f0 + f1 * f1 + f2 * f2;
-        spart[sl] = q;
+        spart[(k % kLag) * (NPT * T) + sl] = q;
       }
       if (k == target) {
         // ---- exact verdict at the target pass (reference-order norms) ----
@@ -802,6 +814,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         }
       }
       rewrite_fixed = false;
+      if (decide_here) decide(k - 1);
       FB_PROF({ const long long t1 = clock64(); pc2 += t1 - tq; tq = t1; })
       __syncthreads();
       FB_PROF({ const long long t1 = clock64(); pc3 += t1 - tq; tq = t1; })

@@ -374,7 +374,7 @@ struct KClass {
     if (node) return node_smem(true);
     if (cluster)
       return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 8ull * csr_cap + 4ull * push_cap;
-    return static_cast<size_t>(x_bytes) + g_bytes + 8ull * ts + 4ull * csr_cap;  // dr_kernel.cuh
+    return static_cast<size_t>(x_bytes) + g_bytes + 16ull * ts + 4ull * csr_cap;  // dr_kernel.cuh
   }
 };
 
@@ -1042,7 +1042,7 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
   if (S.node_slots * 24 >= 65536) return false;  // 16-bit x-record offsets
   const size_t smem = align16(24 * static_cast<size_t>(TS + 2)) +
                       align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
-                      8ull * TS + 8ull * (max_pairs + 1) * TS;
+                      16ull * TS + 8ull * (max_pairs + 1) * TS;
   return smem <= static_cast<size_t>(c->max_smem);
 }
 
