@@ -105,7 +105,7 @@ struct DrParams {
   double ea_scale, nonlinearity;
   double damping, tolerance, dt_safety, density_scale;
   long long max_iterations;
-  unsigned long long* phase_prof;  // optional [grid][NW][4] cycle accumulators
+  unsigned long long* phase_prof;  // optional [grid][NW][8] cycle accumulators
   unsigned long long* trace;       // optional [solve][4]: start ns, end ns,
                                    // sm << 32 | class << 24 | block, iterations (FIBRA_TRACE)
   int trace_class;
@@ -484,7 +484,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     int conv = 0;
     bool rewrite_fixed = false;
 
-    FB_PROF(long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, tq = 0;)
+    // fiber | bar1 | node: verdict/commit checks | gather | exact + update + decider | bar2
+    FB_PROF(long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0, pc4 = 0, pc5 = 0, tq = 0;)
     while (status == FIBRA_OK) {
       // ================= fiber phase (force pass k) =================
       FB_PROF(tq = clock64());
@@ -667,6 +668,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         break;
       }
       const double h_k = 0.5 * dt_k;
+      FB_PROF({ const long long t1 = clock64(); pc4 += t1 - tq; tq = t1; })
       double fk[NPT][3];
 #pragma unroll
       for (int j = 0; j < NPT; ++j) {
@@ -697,6 +699,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         const double q = f0 * f0 + f1 * f1 + f2 * f2;
         spart[(k % kLag) * (NPT * T) + sl] = q;
       }
+      FB_PROF({ const long long t1 = clock64(); pc5 += t1 - tq; tq = t1; })
       if (k == target) {
         // ---- exact verdict at the target pass (reference-order norms) ----
         double* SF = reinterpret_cast<double*>(X);
@@ -832,8 +835,8 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     // of it (the reference leaves a partially updated state behind on a throw).
     const int n_done = (status == FIBRA_OK) ? k : (k > 0 ? k - 1 : 0);
     FB_PROF(if (P.phase_prof && lane == 0) {
-      unsigned long long* pp = P.phase_prof + (static_cast<size_t>(blockIdx.x) * NW + warp) * 4;
-      pp[0] += pc0; pp[1] += pc1; pp[2] += pc2; pp[3] += pc3;
+      unsigned long long* pp = P.phase_prof + (static_cast<size_t>(blockIdx.x) * NW + warp) * 8;
+      pp[0] += pc0; pp[1] += pc1; pp[2] += pc4; pp[3] += pc5; pp[4] += pc2; pp[5] += pc3;
     })
     const bool zero_iter = (n_done == 0);
     const int N = E.n_nodes, M = E.n_fibers, NFN = E.n_free_nodes, NFIX = E.n_fix_nodes;

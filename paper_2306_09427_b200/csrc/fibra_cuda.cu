@@ -884,7 +884,7 @@ int launch_solve(fibra_ctx* c, const double* dF, const fibra_law* law,
       if (getenv("FIBRA_PHASE_PROF") && !prof_used) {  // diagnostics: per-warp phase cycles
         static unsigned long long* buf = nullptr;
         static size_t pcap = 0;
-        const size_t need = static_cast<size_t>(units) * (v.T / 32) * 4;
+        const size_t need = static_cast<size_t>(units) * (v.T / 32) * 8;
         if (need > pcap) { cudaFree(buf); cudaMalloc(&buf, need * 8); pcap = need; }
         cudaMemsetAsync(buf, 0, need * 8, sm);
         P.phase_prof = buf;

@@ -181,8 +181,7 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
   // 3c mod 16) should be unique at each of those three "vertices": the store group, and
   // the (node half-warp, list position) of each reader.  Three vertices per record make
   // this a hypergraph colouring, so it is found by min-conflict search; a leftover
-  // conflict costs one extra shared-memory wavefront, never a wrong result.  Gather
-  // conflicts (the node phase is the critical path) weigh twice a store conflict.
+  // conflict costs one extra shared-memory wavefront, never a wrong result.
   std::vector<int> group_of(M, 0);
   for (int g = 0; g < n_groups; ++g)
     for (int f : best_groups[g]) group_of[f] = g;
@@ -214,7 +213,7 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
   for (auto& x : cnt) x.fill(0);
   std::array<int, kBanks> used{};
   std::vector<int> colour(M, -1);
-  auto weight = [&](int i) { return i == 0 ? 1 : 2; };
+  auto weight = [&](int) { return 1; };  // a wavefront is a wavefront
   auto cost = [&](int f, int c) {  // conflicts f would add with colour c
     int w = 0;
     for (int i = 0; i < 3; ++i)
@@ -244,76 +243,150 @@ bool build_schedule(int N, int NFN, int M, const int* a_pn, const int* b_pn, int
     colour[f] = best;
     place(f, best, 1);
   }
-  // tabu search (TabuCol) on the weighted conflict count: the best non-tabu recolouring of
-  // a conflicting record per step; a record may not return to a colour it just left
-  std::vector<std::vector<int>> at(nV);  // vertex -> records
-  for (int f = 0; f < M; ++f)
-    for (int i = 0; i < 3; ++i)
-      if (vert[f][i] >= 0) at[vert[f][i]].push_back(f);
-  std::vector<std::array<int, kBanks>> gam(M);  // weighted conflicts of f in colour c
-  for (int f = 0; f < M; ++f) {
-    place(f, colour[f], -1);
-    for (int c = 0; c < kBanks; ++c) gam[f][c] = cost(f, c);
-    place(f, colour[f], 1);
-  }
-  long conflicts = 0;
-  for (int f = 0; f < M; ++f) conflicts += gam[f][colour[f]];
-  conflicts /= 2;  // each conflicting pair is seen from both records
-  if (getenv("FIBRA_SCHED_DEBUG")) fprintf(stderr, "colouring: greedy conflicts %ld\n", conflicts);
-  std::vector<int> best_colour = colour;
-  long best_conflicts = conflicts;
-  std::vector<std::array<long, kBanks>> tabu(M);
-  for (auto& x : tabu) x.fill(0);
+  // Alternate (a) tabu search (TabuCol) over the colours -- the best non-tabu recolouring
+  // of a conflicting record per step, a record may not return to a colour it just left --
+  // and (b) store-group swaps: two fibers whose tail and head x slots lie in the same banks
+  // may trade groups without disturbing the x loads; a swap is kept when it lowers the
+  // conflicts of the two store groups (the gather vertices do not change).
   std::mt19937 crng(777);
-  const long max_iter = 40000;
-  long dbg_it = 0;
-  for (long it = 1; it <= max_iter && conflicts > 0; ++it) {
-    dbg_it = it;
-    int bf = -1, bcol = -1, bdelta = 0, ties = 0;
+  std::vector<std::vector<int>> at(nV);  // vertex -> records
+  auto rebuild_at = [&]() {
+    for (auto& x : at) x.clear();
+    for (int f = 0; f < M; ++f)
+      for (int i = 0; i < 3; ++i)
+        if (vert[f][i] >= 0) at[vert[f][i]].push_back(f);
+  };
+  auto tabu = [&](long max_iter) {
+    rebuild_at();
+    std::vector<std::array<int, kBanks>> gam(M);  // weighted conflicts of f in colour c
     for (int f = 0; f < M; ++f) {
-      const int cur = gam[f][colour[f]];
-      if (cur == 0) continue;
-      for (int c = 0; c < kBanks; ++c) {
-        if (c == colour[f]) continue;
-        const int delta = gam[f][c] - cur;
-        const bool allowed = tabu[f][c] < it || conflicts + delta < best_conflicts;
-        if (!allowed) continue;
-        if (bf < 0 || delta < bdelta) {
-          bf = f; bcol = c; bdelta = delta; ties = 1;
-        } else if (delta == bdelta && std::uniform_int_distribution<int>(0, ties++)(crng) == 0) {
-          bf = f; bcol = c;
+      place(f, colour[f], -1);
+      for (int c = 0; c < kBanks; ++c) gam[f][c] = cost(f, c);
+      place(f, colour[f], 1);
+    }
+    long conflicts = 0;
+    for (int f = 0; f < M; ++f) conflicts += gam[f][colour[f]];
+    conflicts /= 2;  // each conflicting pair is seen from both records
+    std::vector<int> best_colour = colour;
+    long best_conflicts = conflicts;
+    std::vector<std::array<long, kBanks>> tabu_until(M);
+    for (auto& x : tabu_until) x.fill(0);
+    // the records in conflict, kept up to date as moves change their neighbours' counts
+    std::vector<int> hot, where(M, -1);
+    auto refresh = [&](int f) {
+      const bool h = gam[f][colour[f]] > 0;
+      if (h && where[f] < 0) {
+        where[f] = static_cast<int>(hot.size());
+        hot.push_back(f);
+      } else if (!h && where[f] >= 0) {
+        const int last = hot.back();
+        hot[where[f]] = last;
+        where[last] = where[f];
+        hot.pop_back();
+        where[f] = -1;
+      }
+    };
+    for (int f = 0; f < M; ++f) refresh(f);
+    long since_best = 0;
+    for (long it = 1; it <= max_iter && conflicts > 0 && since_best < 4000; ++it, ++since_best) {
+      int bf = -1, bcol = -1, bdelta = 0, ties = 0;
+      for (int f : hot) {
+        const int cur = gam[f][colour[f]];
+        for (int c = 0; c < kBanks; ++c) {
+          if (c == colour[f]) continue;
+          const int delta = gam[f][c] - cur;
+          if (!(tabu_until[f][c] < it || conflicts + delta < best_conflicts)) continue;
+          if (bf < 0 || delta < bdelta) {
+            bf = f; bcol = c; bdelta = delta; ties = 1;
+          } else if (delta == bdelta && std::uniform_int_distribution<int>(0, ties++)(crng) == 0) {
+            bf = f; bcol = c;
+          }
         }
       }
-    }
-    if (bf < 0) break;
-    const int old = colour[bf];
-    for (int i = 0; i < 3; ++i) {
-      const int v = vert[bf][i];
-      if (v < 0) continue;
-      const int w = weight(i);  // the vertex's kind: store group or gather step
-      for (int f2 : at[v]) {
-        if (f2 == bf) continue;
-        gam[f2][old] -= w;
-        gam[f2][bcol] += w;
+      if (bf < 0) break;
+      const int old = colour[bf];
+      for (int i = 0; i < 3; ++i) {
+        const int v = vert[bf][i];
+        if (v < 0) continue;
+        const int w = weight(i);  // the vertex's kind: store group or gather step
+        for (int f2 : at[v]) {
+          if (f2 == bf) continue;
+          gam[f2][old] -= w;
+          gam[f2][bcol] += w;
+        }
+      }
+      place(bf, old, -1);
+      colour[bf] = bcol;
+      place(bf, bcol, 1);
+      for (int i = 0; i < 3; ++i)
+        if (vert[bf][i] >= 0)
+          for (int f2 : at[vert[bf][i]]) refresh(f2);
+      conflicts += bdelta;
+      tabu_until[bf][old] = it + 10 + static_cast<long>(crng() % 10);
+      if (conflicts < best_conflicts) {
+        best_conflicts = conflicts;
+        best_colour = colour;
+        since_best = 0;
       }
     }
-    place(bf, old, -1);
-    colour[bf] = bcol;
-    place(bf, bcol, 1);
-    conflicts += bdelta;
-    tabu[bf][old] = it + 10 + static_cast<long>(crng() % 10);
-    if (conflicts < best_conflicts) {
-      best_conflicts = conflicts;
-      best_colour = colour;
+    if (best_conflicts < conflicts) {
+      for (int f = 0; f < M; ++f) place(f, colour[f], -1);
+      colour = best_colour;
+      for (int f = 0; f < M; ++f) place(f, colour[f], 1);
     }
+    return best_conflicts;
+  };
+  // swap partners: same (tail x bank, head x bank)
+  auto xkey = [&](int f) {
+    return (s.slot_of_pn[s.tail_pn[f]] % kBanks) * kBanks + s.slot_of_pn[s.head_pn[f]] % kBanks;
+  };
+  std::vector<std::vector<int>> by_key(kBanks * kBanks);
+  for (int f = 0; f < M; ++f) by_key[xkey(f)].push_back(f);
+  auto pairs = [&](int v) {
+    int t = 0;
+    for (int c = 0; c < kBanks; ++c) t += cnt[v][c] * (cnt[v][c] - 1) / 2;
+    return t;
+  };
+  auto swap_pass = [&]() {
+    bool any = false;
+    for (int f = 0; f < M; ++f) {
+      const int g1 = vert[f][0];
+      if (cnt[g1][colour[f]] < 2) continue;  // f's store is not in conflict
+      for (int f2 : by_key[xkey(f)]) {
+        const int g2 = vert[f2][0];
+        if (g2 == g1 || colour[f2] == colour[f]) continue;
+        const int before = pairs(g1) + pairs(g2);
+        --cnt[g1][colour[f]]; ++cnt[g2][colour[f]];
+        --cnt[g2][colour[f2]]; ++cnt[g1][colour[f2]];
+        if (pairs(g1) + pairs(g2) < before) {
+          vert[f][0] = g2;
+          vert[f2][0] = g1;
+          auto& m1 = best_groups[g1];
+          auto& m2 = best_groups[g2];
+          *std::find(m1.begin(), m1.end(), f) = f2;
+          *std::find(m2.begin(), m2.end(), f2) = f;
+          any = true;
+          break;
+        }
+        ++cnt[g1][colour[f]]; --cnt[g2][colour[f]];
+        ++cnt[g2][colour[f2]]; --cnt[g1][colour[f2]];
+      }
+    }
+    return any;
+  };
+  const char* rounds_env = getenv("FIBRA_SCHED_ROUNDS");  // diagnostics: search effort
+  const int rounds = rounds_env ? atoi(rounds_env) : 2;
+  const long iters = getenv("FIBRA_SCHED_ITERS") ? atol(getenv("FIBRA_SCHED_ITERS")) : 2000;
+  long conflicts = tabu(2 * iters);
+  for (int round = 0; round < rounds && conflicts > 0; ++round) {
+    for (int sweep = 0; sweep < 10 && swap_pass(); ++sweep) {
+    }
+    conflicts = tabu(iters);
   }
-  if (getenv("FIBRA_SCHED_DEBUG"))
-    fprintf(stderr, "colouring: conflicts %ld best %ld iters %ld\n", conflicts, best_conflicts, dbg_it);
-  if (best_conflicts < conflicts) {
-    for (int f = 0; f < M; ++f) place(f, colour[f], -1);
-    colour = best_colour;
-    for (int f = 0; f < M; ++f) place(f, colour[f], 1);
-  }
+  if (getenv("FIBRA_SCHED_DEBUG")) fprintf(stderr, "colouring: conflicts %ld\n", conflicts);
+  for (int g = 0; g < n_groups; ++g)  // the store groups as finally composed
+    for (int i = 0; i < static_cast<int>(best_groups[g].size()); ++i)
+      s.fiber_of_fslot[kBanks * g + i] = best_groups[g][i];
   s.gather_steps = 0;
   for (int v = n_groups; v < nV; ++v) {
     int any = 0;

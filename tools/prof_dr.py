@@ -25,9 +25,10 @@ if os.environ.get("FIBRA_PHASE_PROF"):
     L.fibra_cuda_phase_profile(db._ctx, None, 0, C.byref(nn))
     buf = (C.c_uint64 * nn.value)()
     L.fibra_cuda_phase_profile(db._ctx, buf, nn.value, C.byref(nn))
-    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 4).astype(float) / its
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 8).astype(float)[:, :6] / its
     nw = a.shape[0] // (len(F) if len(F) < 296 else 296)
-    print("per-iteration cycles per warp (mean over CTAs): fiber, bar1, node, bar2")
-    a = a.reshape(-1, nw, 4)
+    print("per-iteration cycles per warp (mean over CTAs): fiber, bar1, node checks, gather, "
+          "update+decider, bar2")
+    a = a.reshape(-1, nw, 6)
     for w in range(nw):
         print(w, np.round(a[:, w].mean(0), 1))
