@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
   const double B = P.nonlinearity;
 
   int fab[FPT], fgh[FPT];
-  double fl0[FPT], fs[FPT], fmred[FPT];
+  double fl0[FPT], frl0[FPT], fs[FPT], fmred[FPT];  // frl0: rcp_refined(l0), loop invariant
   int npair[NPT], npush[NPT];
   double nref[NPT][3], ninv[NPT], ncm[NPT];
   int cur_entry = -1;
@@ -270,6 +270,10 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         fab[j] = Q.fib_ab[f];
         fgh[j] = Q.fib_gh[f];
         fl0[j] = Q.fib_l0[f];
+        // (NaN outside [2^-1000, 2^1000]: the fast-path range test then takes the built-in
+        //  operators, fastmath.cuh fiber_fast_ok)
+        frl0[j] = (fl0[j] >= 0x1p-1000 && fl0[j] <= 0x1p1000)
+                      ? rcp_refined(fl0[j]) : __longlong_as_double(0x7ff8000000000000ll);
         if (!UEA) fs[j] = P.ea_scale * Q.fib_ea[f];
       }
 #pragma unroll
@@ -432,13 +436,16 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
             dx[jj] = xb_[0] - xa_[0];
             dy[jj] = xb_[1] - xa_[1];
             dz[jj] = xb_[2] - xa_[2];
-            bool o1, o2, o3 = true;
+            bool o1, o2 = true, o3 = true;
             const double len = sqrt_fast(dx[jj] * dx[jj] + dy[jj] * dy[jj] + dz[jj] * dz[jj], o1);
             collapsed |= (len <= 1e-8 * fl0[j]);  // network.cpp:291
-            const double stretch = div_fast(len, fl0[j], o2);
-            if (LAW == 0) {
-              g[jj] = div_fast(law_force<0>(SJ(j), stretch, bo, B), len, o3);
+            if (LAW == 0) {  // one range test for both divisions (fastmath.cuh)
+              const double stretch = div_rcp_raw(len, fl0[j], frl0[j]);
+              const double n = law_force<0>(SJ(j), stretch, bo, B);
+              g[jj] = div_rcp_raw(n, len, rcp_refined(len));
+              o2 = fiber_fast_ok(len, stretch, n);
             } else {
+              const double stretch = div_fast_rcp(len, fl0[j], frl0[j], o2);
               g[jj] = law_force<LAW>(SJ(j), stretch, bo, B) / len;
               const double kt = smax(fabs(law_tangent<LAW>(SJ(j), stretch, bo, B)), SJ(j));
               kmin = smin(kmin, fmred[j] / kt);
