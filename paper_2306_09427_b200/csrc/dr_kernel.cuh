@@ -51,7 +51,7 @@ namespace fibra_b200 {
 struct EntryDev {          // one RveLibrary entry in HBM, already in slot order
   int n_nodes, n_fibers, n_free_nodes, n_fix_nodes;
   int f0, node_slots, fiber_slots, gd_slots;  // gd_slots includes dummies + zero record
-  int thread_slots, max_pairs, pad1, pad2;    // NPT*T (two dummy x records follow)
+  int thread_slots, max_pairs, pad1, pad2;    // NPT*T (32 dummy x records follow)
   double max_lump, max_ea, box_volume, pad3;
   const int* slot_pn;      // [thread_slots] packed node id per slot, -1 empty
   const double* slot_ref;  // [3*thread_slots] reference coordinates by slot
@@ -361,16 +361,17 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
       cur_entry = e;
       s_uni = P.ea_scale * E.fib_ea[0];
       for (int i = tid; i < (E.max_pairs + 1) * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
-      // dummy x records for empty fiber slots, and the zero g*d record (last record)
-      if (tid < 6) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid == 3) ? 1.0 : 0.0;
+      // dummy x records for empty fiber slots (16 tails (0,0,0), 16 heads (1,0,0)), and the
+      // zero g*d record (last record)
+      if (tid < 96) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid >= 48 && tid % 3 == 0) ? 1.0 : 0.0;
       if (tid < 3) sm_at<double>(G, 24 * (E.gd_slots - 1))[tid] = 0.0;
 #pragma unroll
       for (int j = 0; j < FPT; ++j) {
         const int f = j * T + tid;
-        {  // (NaN outside [2^-1000, 2^1000]: the fast-path range test then sends the fiber
+        {  // (NaN outside [2^-900, 2^1000]: the fast-path range test then sends the fiber
            //  to the built-in operators, fastmath.cuh fiber_fast_ok)
           const double l0 = E.fib_l0[f];
-          frl0[j] = (l0 >= 0x1p-1000 && l0 <= 0x1p1000) ? rcp_refined(l0) : __longlong_as_double(0x7ff8000000000000ll);
+          frl0[j] = (l0 >= 0x1p-900 && l0 <= 0x1p1000) ? rcp_refined(l0) : __longlong_as_double(0x7ff8000000000000ll);
         }
 #if FIBRA_TOPO_REG
         fab_r[j] = E.fib_ab[f];

@@ -1040,7 +1040,7 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
   const int TS = v.NPT * v.T;
   const int gd_total = S.gd_slots + 17;  // + per-lane dummy records + the zero record
   if (S.node_slots * 24 >= 65536) return false;  // 16-bit x-record offsets
-  const size_t smem = align16(24 * static_cast<size_t>(TS + 2)) +
+  const size_t smem = align16(24 * static_cast<size_t>(TS + 32)) +
                       align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
                       16ull * TS + 8ull * (max_pairs + 1) * TS;
   return smem <= static_cast<size_t>(c->max_smem);
@@ -1296,7 +1296,7 @@ void build_stream_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_des
 void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_desc& d,
                           const Variant& v, Arena& A, Caps& K) {
   const Schedule& S = de.sched;
-  const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS, TS+1
+  const int TS = v.NPT * v.T;  // thread slots; dummy x records at TS .. TS+31
   const int FS = S.fiber_slots;
   std::vector<int> slot_pn(TS, -1);
   std::vector<double> slot_ref(3 * static_cast<size_t>(TS), 0.0), slot_lump(TS, 1.0);
@@ -1307,12 +1307,44 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     for (int k = 0; k < 3; ++k) slot_ref[3 * sl + k] = P.ref[3 * pn + k];
     slot_lump[sl] = P.lump[pn];
   }
-  // g*d records: [real: +g*d per fiber, schedule colouring] [one per dummy fiber slot,
-  // bank = lane] [zero record]  (all dummies of one lane share a record: their values are
-  // never read, and within one store instruction the 16 lanes still hit 16 banks)
-  std::vector<int> dummy_rec(FS, -1);
-  for (int fs = 0; fs < FS; ++fs)
-    if (S.fiber_of_fslot[fs] < 0) dummy_rec[fs] = S.gd_slots + fs % 16;
+  // g*d records: [real: +g*d per fiber, schedule colouring] [16 dummy records, one per
+  // bank] [zero record].  Dummy fibers (empty fiber slots) load x from dummy records too:
+  // 16 tail records at slots TS .. TS+15 (0,0,0) and 16 head records at TS+16 .. TS+31
+  // (1,0,0), a unit segment.  In each half-warp group a dummy takes x records and a g*d
+  // record in banks the group's real fibers leave free, so it adds no bank conflict to the
+  // group's loads and stores (values of dummies are never read).
+  std::vector<int> dummy_rec(FS, -1), dummy_xt(FS, -1), dummy_xh(FS, -1);
+  {
+    auto xbank = [](int slot) { return (3 * slot) % 16; };  // 24-byte records: bank pair 3r
+    int xt_of_bank[16], xh_of_bank[16], rec_of_bank[16];
+    for (int r = 0; r < 16; ++r) {
+      xt_of_bank[xbank(TS + r)] = TS + r;
+      xh_of_bank[xbank(TS + 16 + r)] = TS + 16 + r;
+      rec_of_bank[(3 * (S.gd_slots + r)) % 16] = S.gd_slots + r;
+    }
+    for (int g = 0; g < FS / 16; ++g) {
+      bool ut[16] = {}, uh[16] = {}, ur[16] = {};
+      for (int l = 0; l < 16; ++l) {
+        const int f = S.fiber_of_fslot[16 * g + l];
+        if (f < 0) continue;
+        ut[xbank(S.slot_of_pn[S.tail_pn[f]])] = true;
+        uh[xbank(S.slot_of_pn[S.head_pn[f]])] = true;
+        ur[(3 * S.rec[f]) % 16] = true;
+      }
+      int bt = 0, bh = 0, br = 0;
+      for (int l = 0; l < 16; ++l) {
+        const int fs = 16 * g + l;
+        if (S.fiber_of_fslot[fs] >= 0) continue;
+        while (ut[bt]) ++bt;
+        while (uh[bh]) ++bh;
+        while (ur[br]) ++br;
+        dummy_xt[fs] = xt_of_bank[bt];
+        dummy_xh[fs] = xh_of_bank[bh];
+        dummy_rec[fs] = rec_of_bank[br];
+        ut[bt] = uh[bh] = ur[br] = true;
+      }
+    }
+  }
   const int zero_rec = S.gd_slots + 16;
   const int gd_total = zero_rec + 1;
   // CSR by slot, ascending fiber id, padded to even length with the zero record;
@@ -1345,8 +1377,8 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
   std::vector<double> fl0(FS, 0.5), fea(FS, P.M > 0 ? P.ea[0] : 1.0);
   for (int fs = 0; fs < FS; ++fs) {
     const int f = S.fiber_of_fslot[fs];
-    if (f < 0) {  // dummy: unit segment between the two dummy x records
-      fab[fs] = (24 * TS) | ((24 * (TS + 1)) << 16);
+    if (f < 0) {  // dummy: unit segment between two dummy x records
+      fab[fs] = (24 * dummy_xt[fs]) | ((24 * dummy_xh[fs]) << 16);
       fg[fs] = 24 * dummy_rec[fs];
       continue;
     }
@@ -1382,7 +1414,7 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
   A.add(&E.fib_l0, fl0);
   A.add(&E.fib_ea, fea);
   K.ts = TS;
-  K.x_bytes = static_cast<int>(align16(24 * static_cast<size_t>(TS + 2)));
+  K.x_bytes = static_cast<int>(align16(24 * static_cast<size_t>(TS + 32)));
   const size_t gb = std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M));
   K.g_bytes = static_cast<int>(align16(gb));
   K.csr_cap = static_cast<int>(ent.size());
@@ -2165,7 +2197,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
         kind_vi[i] = v;
         const int TS = kVariants[v].NPT * kVariants[v].T;
         est[i].ts = TS;
-        est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 2)));
+        est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 32)));
         est[i].g_bytes = static_cast<int>(align16(std::max<size_t>(
             24ull * (de.sched.gd_slots + 17), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
         est[i].csr_cap = 2 * (mp + 1) * TS;  // + the padding row
@@ -2866,8 +2898,8 @@ int fibra_debug_resident_forces(const fibra_net_desc* d, int shape, const double
   }
   const EntryDev& E = de.dev;
   const int TS = E.thread_slots, FS = E.fiber_slots;
-  std::vector<double> X(3 * static_cast<size_t>(TS + 2), 0.0), G(3 * static_cast<size_t>(E.gd_slots), 0.0);
-  X[3 * TS + 3] = 1.0;
+  std::vector<double> X(3 * static_cast<size_t>(TS + 32), 0.0), G(3 * static_cast<size_t>(E.gd_slots), 0.0);
+  for (int r = 16; r < 32; ++r) X[3 * (TS + r)] = 1.0;  // dummy head records (1,0,0)
   auto x_of = [&](int pn, int c) { return P.ref[3 * pn + c] + u[3 * pn + c]; };
   for (int sl = 0; sl < TS; ++sl)
     if (E.slot_pn[sl] >= 0)
