@@ -545,20 +545,24 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       for (int j = 0; j < NPT; ++j) {
         const int sl = j * T + tid;
         double f0 = 0.0, f1 = 0.0, f2 = 0.0;  // CSR gather, ascending fiber id
+        // the next step's pair is loaded one step ahead (predicated: no padding row in the
+        // tight config-4 shapes), and the tail's negation is a signed DFMA (dr_kernel.cuh)
+        int2 ep = npair[j] > 0 ? cent[sl] : make_int2(0, 0);
         for (int kp = 0; kp < npair[j]; ++kp) {
-          const int2 ep = cent[kp * TS + sl];
+          const int2 en = kp + 1 < npair[j] ? cent[(kp + 1) * TS + sl] : ep;
           const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);
           const double* g1 = sm_at<double>(G, ep.y & 0x7fffffff);
-          const double a0 = signed_by(g0[0], ep.x), a1 = signed_by(g0[1], ep.x);
-          const double a2 = signed_by(g0[2], ep.x);
-          const double b0 = signed_by(g1[0], ep.y), b1 = signed_by(g1[1], ep.y);
-          const double b2 = signed_by(g1[2], ep.y);
-          f0 = f0 + a0;  // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
-          f1 = f1 + a1;
-          f2 = f2 + a2;
-          f0 = f0 + b0;
-          f1 = f1 + b1;
-          f2 = f2 + b2;
+          const double a0 = g0[0], a1 = g0[1], a2 = g0[2];
+          const double b0 = g1[0], b1 = g1[1], b2 = g1[2];
+          const double sa = sign_one(ep.x), sb = sign_one(ep.y);  // -1 for the tail
+          // f -= g*d for the tail, f += g*d for the head (network.cpp:298-303)
+          f0 = __fma_rn(sa, a0, f0);
+          f1 = __fma_rn(sa, a1, f1);
+          f2 = __fma_rn(sa, a2, f2);
+          f0 = __fma_rn(sb, b0, f0);
+          f1 = __fma_rn(sb, b1, f1);
+          f2 = __fma_rn(sb, b2, f2);
+          ep = en;
         }
         fk[j][0] = f0;
         fk[j][1] = f1;

@@ -212,11 +212,6 @@ __device__ __forceinline__ double sign_one(int entry) {
   return __hiloint2double((entry & static_cast<int>(0x80000000u)) | 0x3ff00000, 0);
 }
 
-// x or -x, exact: xor of the CSR entry's bit 31 into the sign bit (one LOP3)
-__device__ __forceinline__ double signed_by(double x, int entry) {
-  return __hiloint2double(__double2hiint(x) ^ (entry & static_cast<int>(0x80000000u)),
-                          __double2loint(x));
-}
 
 template <class Tp>
 __device__ __forceinline__ Tp* sm_at(unsigned char* base, int byte_off) {
