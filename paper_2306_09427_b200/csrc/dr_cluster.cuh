@@ -395,28 +395,46 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
       if (warp == NW - 1) {  // reducer warp: owns no fibers
         if (LAW != 0) push_wmin(INFINITY);
         if (target < 0 && k >= 1) {
-          double sf = 0, sfix = 0;  // partials of pass k-1 -> every CTA
-          for (int i = lane; i < F0; i += 32) sf += spart[i];
-          for (int i = F0 + lane; i < NSLOT; i += 32) sfix += spart[i];
-          sf = warp_sum(sf);
-          sfix = warp_sum(sfix);
+          // partials of pass k-1 -> every CTA.  Lane l sums slots l, l+32, ... (row i of 32
+          // slots is free iff i < F0/32) in four chains, then a butterfly: a short dependency
+          // chain (any summation order will do for the speculation)
+          constexpr int R = TS / 32;
+          const int R0 = F0 >> 5;
+          double vf[4] = {0.0, 0.0, 0.0, 0.0}, vx[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int i = 0; i < R; ++i) {  // four independent chains of R/4 adds
+            const double v = spart[32 * i + lane];
+            if (i < R0) vf[i & 3] += v;
+            else vx[i & 3] += v;
+          }
+          double sf = (vf[0] + vf[1]) + (vf[2] + vf[3]), sfix = (vx[0] + vx[1]) + (vx[2] + vx[3]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            sf += __shfl_xor_sync(0xffffffffu, sf, o);
+            sfix += __shfl_xor_sync(0xffffffffu, sfix, o);
+          }
           if (lane < static_cast<int>(C)) {
             const unsigned a = cl_map(ctl_sh + off_part + ((k - 1) & 1) * 256 + rank * 16, lane);
             cl_st_f64(a, sf);
             cl_st_f64(a + 8, sfix);
           }
-          if (k >= 2 && lane == 0) {  // verdict for pass k-2 (rank order, every CTA)
-            double tf = 0, tx = 0;
-            for (unsigned r = 0; r < C; ++r) {
-              tf += ctl.part[(k - 2) & 1][r][0];
-              tx += ctl.part[(k - 2) & 1][r][1];
+          if (k >= 2) {  // verdict for pass k-2 from every CTA's partials (every CTA alike)
+            double tf = lane < static_cast<int>(C) ? ctl.part[(k - 2) & 1][lane][0] : 0.0;
+            double tx = lane < static_cast<int>(C) ? ctl.part[(k - 2) & 1][lane][1] : 0.0;
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) {  // C <= 16
+              tf += __shfl_xor_sync(0xffffffffu, tf, o);
+              tx += __shfl_xor_sync(0xffffffffu, tx, o);
             }
-            const double res = sqrt(tf);
-            const double eps = P.tolerance * smax(sqrt(tx), ctl.force_floor);
-            int d = (res <= eps) ? kDecConv : 0;
-            if (!isfinite(res) || !isfinite(eps)) d |= kDecExact | kDecNonfinite;
-            else if (fabs(res - eps) <= 1e-10 * eps) d |= kDecExact;
-            ctl.dec = (k - 2 > ctl.skip) ? d : 0;  // decided passes are not re-decided
+            // squared form of res <= tol * max(sqrt(tx), floor); a near tie (within ~2e-10
+            // in squares) or a tiny threshold is decided exactly with the reference's sums
+            const double fl = ctl.force_floor;
+            const double e2 = (P.tolerance * P.tolerance) * smax(tx, fl * fl);
+            int d = (tf <= e2) ? kDecConv : 0;
+            if (!isfinite(tf) || !isfinite(e2)) d |= kDecExact | kDecNonfinite;
+            else if (fabs(tf - e2) <= 4e-10 * e2 || e2 < 0x1p-900) d |= kDecExact;
+            if (lane == 0)
+              ctl.dec = (k - 2 > ctl.skip) ? d : 0;  // decided passes are not re-decided
           }
         }
       } else {
