@@ -2192,8 +2192,11 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
         if (region < exit_need) capn = static_cast<int>((exit_need + 19) / 20 + 32);
         est[i].csr_cap = capn;
       }
+    // diagnostics: FIBRA_RESIDENT_SKIP=i leaves kVariants[i] out (shape experiments)
+    const char* skip_env = getenv("FIBRA_RESIDENT_SKIP");
+    const int skip_v = skip_env ? atoi(skip_env) : -1;
     for (int v = 0; v < kNumVariants && kind_vi[i] < 0 && !force_c && !force_stream; ++v)
-      if (resident_fits(c, P, kVariants[v], mp, de.sched)) {
+      if (v != skip_v && resident_fits(c, P, kVariants[v], mp, de.sched)) {
         kind_vi[i] = v;
         const int TS = kVariants[v].NPT * kVariants[v].T;
         est[i].ts = TS;

@@ -13,7 +13,7 @@ spec = P.NetGenSpec(style="knn", nodes=375, fibers=1000, neighbors=10)
 for seed in (1, 2, 4):
     net = P.generate_network(spec, seed)
     out = np.zeros(7, np.int64)
-    for T, FPT, NPT in ((384, 3, 1), (512, 2, 1), (512, 4, 1)):
+    for T, FPT, NPT in ((384, 3, 1), (512, 4, 1)):
         _capi.load().fibra_schedule_report(C.byref(net.desc()), T, FPT, NPT,
                                            out.ctypes.data_as(_capi._lp))
         print(f"seed {seed} T={T} FPT={FPT}: fits={out[0]} conflicting_groups={out[1]} "
