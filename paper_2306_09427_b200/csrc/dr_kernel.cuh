@@ -17,7 +17,7 @@
 //
 // Per DR iteration the CTA runs two phases separated by __syncthreads():
 //   fiber phase: each thread evaluates FPT register-resident fibers, reading x records
-//                (24-byte AoS) from shared memory and writing g*d records;
+//                (24-byte AoS) from shared memory and writing one g*d record each;
 //   node phase:  each thread owns NPT nodes (u and the half-step velocity in registers),
 //                gathers its CSR list, applies the damped central-difference update and
 //                writes the next x record.
@@ -25,12 +25,14 @@
 // free; empty fiber/node slots hold harmless dummies so the hot loop has no per-slot
 // branches.  CSR lists are padded to even length with a record of +0.0 (f + 0.0 == f for
 // every f the accumulation can produce, since it starts at +0.0 and never reaches -0.0).
-// The convergence test is off the critical path: node threads store one |f|^2 per slot;
-// during the next fiber phase the last warp -- whose last fiber row is the one left empty
-// when the fibers do not fill every row (its fiber phase is shorter by one fiber) --
-// reduces them with a short branch-free tree and the following node phase reads the
-// verdict, one iteration late.  (Every warp owns fibers; a warp whose last fiber row is
-// empty skips it.)  The CTA keeps two
+// Each fiber writes one +g*d record; its tail node reads it back as fma(-1, r, f), which
+// equals f - r (one rounding, the product is exact).
+// The convergence test is off the critical path: node threads store one |f|^2 per slot
+// (two buffers by pass parity); at the end of the next node phase the last warp -- the
+// lightest gather, fixed nodes -- reduces them with a short branch-free tree and compares
+// in squares, and the node phase after that reads the verdict, two iterations late
+// (FIBRA_DECIDER_NODE=0: in the last warp's fiber phase, one late).  Every warp owns
+// fibers; a warp whose last fiber row is empty skips it.  The CTA keeps two
 // checkpoints of (u, v_half, t, dt) in global memory; when a verdict says "stop at k"
 // (converged, iteration cap, non-finite, or a near tie |R - eps| <= 1e-10 eps where the
 // tree sum could disagree with the reference's 4-lane sum) it restores the newest
