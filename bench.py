@@ -281,14 +281,30 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def measured_traffic(args, n_steps):
-    """DRAM bytes per DR launch from the committed ncu --set full capture of this exact
-    workload (profiles/r02_dr_traffic.json), else None."""
+def measured_capture(args):
+    """The committed ncu --set full capture of this exact workload's DR launch
+    (profiles/r02_dr_traffic.json), else None."""
     path = os.path.join(ROOT, "profiles", "r02_dr_traffic.json")
     if args.config != 2 or args.tangent or args.points != DEFAULT_POINTS[2] or not os.path.exists(path):
         return None
     with open(path) as f:
-        return json.load(f)["dram_bytes_per_launch"]
+        return json.load(f)
+
+
+def measured_traffic(args, n_steps):
+    """DRAM bytes per DR launch from the committed capture, else None."""
+    cap = measured_capture(args)
+    return cap["dram_bytes_per_launch"] if cap else None
+
+
+def measured_smem(args):
+    """Shared-memory pipe figures of the DR kernel from the committed capture, else None."""
+    cap = measured_capture(args)
+    if not cap or "smem_wavefronts_per_launch" not in cap:
+        return None
+    return {"wavefronts_per_rve_iteration": cap["smem_wavefronts_per_launch"] / cap["rve_iterations_per_launch"],
+            "pipe_pct_of_peak": cap["smem_pipe_pct_of_peak_elapsed"],
+            "source": "ncu --set full of one config-2 DR launch (profiles/r02_dr_traffic.json)"}
 
 
 class ClockSampler:
@@ -480,6 +496,7 @@ def main():
                          "unit": "Gop/s (FP64-pipe lane ops)", "frac": achieved / peak,
                          "traffic": measured_traffic(args, args.steps),
                          "traffic_unit": "DRAM bytes per DR launch (ncu --set full, profiles/r02_dr_traffic.json)",
+                         "shared_memory": measured_smem(args),
                          "work_model": "W_pipe = 51 M + 12 n_free + 2 n_fix per RVE-iteration "
                                        "(SURVEY 8d); peak measured by a DADD stream on this "
                                        "device"},
