@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     const double scale = P.density_scale / E.max_lump;  // setup_mass relax.cpp:35-43
     // sizes are re-read from E where needed: keeping them live across the DR loop costs
     // registers the 2-CTA/SM budget does not have
-    const int F0 = E.f0, NSLOT = E.node_slots;
+    const int F0 = E.f0;
     if (e != cur_entry) {
       cur_entry = e;
       s_uni = P.ea_scale * E.fib_ea[0];
@@ -675,6 +675,15 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         // the next step's pair is loaded one step ahead (row max_pairs is padding), so a
         // step's six record loads depend only on registers and issue back to back
         int2 ep = cent[sl];
+        // not unrolled: with the CSR pair loaded a step ahead, ptxas's default 4-way unroll
+        // only adds register pressure (2.39 -> 2.33 us per CTA-iteration without it);
+        // FIBRA_GATHER_UNROLL=n (diagnostics) sets another factor
+#ifndef FIBRA_GATHER_UNROLL
+#define FIBRA_GATHER_UNROLL 1
+#endif
+#define FB_PRAGMA(x) _Pragma(#x)
+#define FB_UNROLL(n) FB_PRAGMA(unroll n)
+        FB_UNROLL(FIBRA_GATHER_UNROLL)
         for (int kp = 0; kp < npair[j]; ++kp) {  // two incidences per step
           const int2 en = cent[(kp + 1) * (NPT * T) + sl];
           const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);  // the fiber's +g*d
