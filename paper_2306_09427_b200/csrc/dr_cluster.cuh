@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(T, 1) dr_cluster_kernel(ClusterParams CP) {
         // the next step's pair is loaded one step ahead (predicated: no padding row in the
         // tight config-4 shapes), and the tail's negation is a signed DFMA (dr_kernel.cuh)
         int2 ep = npair[j] > 0 ? cent[sl] : make_int2(0, 0);
+#pragma unroll 1
         for (int kp = 0; kp < npair[j]; ++kp) {
           const int2 en = kp + 1 < npair[j] ? cent[(kp + 1) * TS + sl] : ep;
           const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);

@@ -590,7 +590,11 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
             gr[2] = g[jj] * dz[jj];
           }
         };
+#ifdef FIBRA_FIBER_B1  // diagnostics: fibers per block of the first block
+        constexpr int B1 = FIBRA_FIBER_B1 < FPT ? FIBRA_FIBER_B1 : FPT;
+#else
         constexpr int B1 = FPT < 4 ? FPT : (FPT + 1) / 2;
+#endif
         if constexpr (B1 < FPT) {
           fiber_block(std::integral_constant<int, 0>(), std::integral_constant<int, B1>());
           if (frows > B1)
