@@ -157,7 +157,10 @@ constexpr int kCkInterval = 8;
 #ifndef FIBRA_DECIDER_NODE
 #define FIBRA_DECIDER_NODE 1
 #endif
-constexpr int kLag = FIBRA_DECIDER_NODE ? 2 : 1;  // node phase k reads the verdict of k-kLag
+constexpr int kLag = FIBRA_DECIDER_NODE ? 2 : 1;
+#ifndef FIBRA_GATHER_AHEAD  // how many steps ahead the gather loads its CSR pair (1 or 2)
+#define FIBRA_GATHER_AHEAD 1
+#endif  // node phase k reads the verdict of k-kLag
 
 // Per-warp phase cycle counters, compiled only into the diagnostics build
 // (FIBRA_PHASE_PROF=1 python -m paper_2306_09427_b200.build -> lib/libfibra_b200_prof.so).
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
     if (e != cur_entry) {
       cur_entry = e;
       s_uni = P.ea_scale * E.fib_ea[0];
-      for (int i = tid; i < (E.max_pairs + 1) * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
+      for (int i = tid; i < (E.max_pairs + 2) * E.thread_slots; i += T) cent[i] = E.csr_pairs[i];
       // dummy x records for empty fiber slots (16 tails (0,0,0), 16 heads (1,0,0)), and the
       // zero g*d record (last record)
       if (tid < 96) sm_at<double>(X, 24 * E.thread_slots)[tid] = (tid >= 48 && tid % 3 == 0) ? 1.0 : 0.0;
@@ -679,6 +682,9 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
         // the next step's pair is loaded one step ahead (row max_pairs is padding), so a
         // step's six record loads depend only on registers and issue back to back
         int2 ep = cent[sl];
+#if FIBRA_GATHER_AHEAD == 2  // diagnostics: the pair two steps ahead (two padding rows)
+        int2 ep1 = cent[NPT * T + sl];
+#endif
         // not unrolled: with the CSR pair loaded a step ahead, ptxas's default 4-way unroll
         // only adds register pressure (2.39 -> 2.33 us per CTA-iteration without it);
         // FIBRA_GATHER_UNROLL=n (diagnostics) sets another factor
@@ -689,7 +695,7 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
 #define FB_UNROLL(n) FB_PRAGMA(unroll n)
         FB_UNROLL(FIBRA_GATHER_UNROLL)
         for (int kp = 0; kp < npair[j]; ++kp) {  // two incidences per step
-          const int2 en = cent[(kp + 1) * (NPT * T) + sl];
+          const int2 en = cent[(kp + FIBRA_GATHER_AHEAD) * (NPT * T) + sl];
           const double* g0 = sm_at<double>(G, ep.x & 0x7fffffff);  // the fiber's +g*d
           const double* g1 = sm_at<double>(G, ep.y & 0x7fffffff);
           const double a0 = g0[0], a1 = g0[1], a2 = g0[2];
@@ -702,7 +708,12 @@ __global__ void __launch_bounds__(T, MINB) dr_persistent_kernel(DrParams P) {
           f0 = __fma_rn(sb, b0, f0);
           f1 = __fma_rn(sb, b1, f1);
           f2 = __fma_rn(sb, b2, f2);
+#if FIBRA_GATHER_AHEAD == 2
+          ep = ep1;
+          ep1 = en;
+#else
           ep = en;
+#endif
         }
         fk[j][0] = f0;
         fk[j][1] = f1;

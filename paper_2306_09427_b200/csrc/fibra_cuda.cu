@@ -1042,7 +1042,7 @@ bool resident_fits(const fibra_ctx* c, const PackedNet& P, const Variant& v, int
   if (S.node_slots * 24 >= 65536) return false;  // 16-bit x-record offsets
   const size_t smem = align16(24 * static_cast<size_t>(TS + 32)) +
                       align16(std::max<size_t>(24ull * gd_total, 8ull * (3 * P.N + 3 * P.NFN + P.M))) +
-                      16ull * TS + 8ull * (max_pairs + 1) * TS;
+                      16ull * TS + 8ull * (max_pairs + 2) * TS;
   return smem <= static_cast<size_t>(c->max_smem);
 }
 
@@ -1361,8 +1361,8 @@ void build_resident_entry(DeviceEntry& de, const PackedNet& P, const fibra_net_d
     max_pairs = std::max(max_pairs, static_cast<int>((lists[sl].size() + 1) / 2));
   }
   // step-major pairs: pair kp of slot sl at [kp * TS + sl] (coalesced LDS.64 per step), plus
-  // one padding row of zero-record pairs (the gather loads the next step's pair ahead)
-  std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs + 1) * TS, 24 * zero_rec);
+  // two padding rows of zero-record pairs (the gather loads pairs ahead)
+  std::vector<int> npairs(TS, 0), ent(2 * static_cast<size_t>(max_pairs + 2) * TS, 24 * zero_rec);
   for (int sl = 0; sl < TS; ++sl) {
     const auto& L = lists[sl];
     const int pn = sl < S.node_slots ? S.pn_of_slot[sl] : -1;
@@ -2203,7 +2203,7 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
         est[i].x_bytes = static_cast<int>(align16(24ull * (TS + 32)));
         est[i].g_bytes = static_cast<int>(align16(std::max<size_t>(
             24ull * (de.sched.gd_slots + 17), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
-        est[i].csr_cap = 2 * (mp + 1) * TS;  // + the padding row
+        est[i].csr_cap = 2 * (mp + 2) * TS;  // + the padding rows
       }
     // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
     // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
