@@ -297,3 +297,21 @@ def test_node_kernel_force_emulation_bitwise():
             assert np.array_equal(fe.view(np.uint64), O.internal_forces(on, u).view(np.uint64))
             assert rep[2] <= rep[1]  # the placement search never adds bank conflicts
         assert checked >= 3
+
+
+def test_resident_schedule_quality():
+    """The resident schedule of the config-1 network (csrc/host/schedule.cpp): x loads
+    conflict-free (every half-warp group's tails and heads in distinct banks), and the g*d
+    record colouring -- one record per fiber, read by two gather steps and written by one
+    store group, a hypergraph colouring -- within a small excess of wavefronts per
+    iteration (54 when written; a regression of the search shows up here)."""
+    import ctypes as C
+    from paper_2306_09427_b200 import _capi, synth
+    net = P.generate_network(synth.config1_spec(), 1)
+    out = np.zeros(7, np.int64)
+    _capi.load().fibra_schedule_report(C.byref(net.desc()), 384, 3, 1,
+                                       out.ctypes.data_as(_capi._lp))
+    fits, conflicting_groups, gather_excess, _, _, node_slots, store_excess = out
+    assert fits == 1 and node_slots == 384
+    assert conflicting_groups == 0
+    assert gather_excess + store_excess <= 80, out
