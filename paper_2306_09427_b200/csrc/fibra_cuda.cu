@@ -2205,11 +2205,14 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             24ull * (de.sched.gd_slots + 17), 8ull * (3 * P.N + 3 * P.NFN + P.M))));
         est[i].csr_cap = 2 * (mp + 2) * TS;  // + the padding rows
       }
-    // cluster: the fewest CTAs, then the first shape that holds the parts (measured on
-    // 5k-fiber RVEs under full load: 2 x (512,7,2) beats 4 x (384,4,1) and 8 x (384,3,1))
-    for (int cc = force_c ? force_c : 2; cc <= 16 && kind_vi[i] < 0 && !force_stream; cc *= 2)
-        for (int v = 0; v < kNumClusterVariants && kind_vi[i] < 0; ++v) {
-          if (force_shape >= 0 && v != force_shape) continue;
+    // cluster: first the 384-thread shapes on up to 4 CTAs, then the fewest CTAs with the
+    // first shape that holds the parts (config 3 with the round-2 kernels: its 2.5k-6.7k
+    // fibre RVEs on 4 x (384,4,1) finish 0.4 s before 2 x (512,7,2), 2,448 -> 2,488
+    // RVE-solves/s; config 4's lattices need 16 x (512,7,2))
+    auto cluster_try = [&](int cc, int v) {
+      if (kind_vi[i] >= 0 || force_stream || (force_shape >= 0 && v != force_shape)) return;
+      if (force_c && cc != force_c) return;
+      {
           if (cluster_fits(c, P, kClusterVariants[v], cc, mp, plans[i])) {
             kind_vi[i] = v;
             kind_C[i] = cc;
@@ -2226,7 +2229,13 @@ int fibra_cuda_upload_library(fibra_ctx* c, const fibra_net_desc* entries, int32
             est[i].csr_cap = mp * TS;
             est[i].push_cap = plans[i].max_push * TS;
           }
-        }
+      }
+    };
+    for (int cc = 2; cc <= 4; cc *= 2)
+      for (int v = 0; v < kNumClusterVariants; ++v)
+        if (kClusterVariants[v].T == 384) cluster_try(cc, v);
+    for (int cc = 2; cc <= 16; cc *= 2)
+      for (int v = 0; v < kNumClusterVariants; ++v) cluster_try(cc, v);
     // beyond on-chip capacity: the streaming kernel, the lightest shape (fewest nodes per
     // thread) on the fewest CTAs whose slots hold the nodes
     for (int v = 0; v < kNumStreamVariants && kind_vi[i] < 0; ++v)
